@@ -1,0 +1,366 @@
+"""Pins for the CPU oracle (oracle/oracle.c) against things other than itself:
+library routines, exact rational arithmetic, invariants, special cases that
+reduce to textbook definitions, and hand-traced fixtures.  CPU only.
+
+Each test names the PAPER.md passage / DESIGN.md reading it pins.
+"""
+import collections
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+D = 128
+
+
+def _bf16(x):
+    return synth.f32_to_bf16_bits(np.asarray(x, dtype=np.float32))
+
+
+def _val(bits):
+    return synth.decode_f64(bits, synth.DT_BF16)
+
+
+# ----------------------------------------------------------------------------
+# S0 block metadata (reading R1, R16)
+# ----------------------------------------------------------------------------
+@pytest.mark.parametrize("dt", [synth.DT_BF16, synth.DT_F32])
+def test_meta_matches_numpy_min_max(dt):
+    rng = synth.rng_for(900, 1)
+    blocks = synth.kv_blocks(rng, 37, D, synth.channel_scales(rng))
+    store = synth.encode(blocks, dt)
+    meta = oracle.block_meta(store, key_stride=2 * 32 * D)
+    vals = synth.decode_f64(store, dt)[:, 0]            # [n][32][d] keys
+    got = synth.decode_f64(meta, dt)
+    np.testing.assert_array_equal(got[:, 0], vals.min(axis=1))
+    np.testing.assert_array_equal(got[:, 1], vals.max(axis=1))
+
+
+def test_meta_signed_zero_hand_cases():
+    # channel 0: tokens hold +0 and -0 only -> min is -0 (0x8000), max is +0 (0x0000)
+    # channel 1: all +0 -> both +0; channel 2: all -0 -> both -0
+    keys = np.zeros((1, 32, D), dtype=np.uint16)
+    keys[0, 5, 0] = 0x8000
+    keys[0, :, 2] = 0x8000
+    keys[0, 7, 3] = _bf16(-1.5).item()
+    keys[0, 9, 3] = _bf16(2.25).item()
+    meta = oracle.block_meta(keys)
+    assert meta[0, 0, 0] == 0x8000 and meta[0, 1, 0] == 0x0000
+    assert meta[0, 0, 1] == 0x0000 and meta[0, 1, 1] == 0x0000
+    assert meta[0, 0, 2] == 0x8000 and meta[0, 1, 2] == 0x8000
+    assert meta[0, 0, 3] == _bf16(-1.5) and meta[0, 1, 3] == _bf16(2.25)
+
+
+# ----------------------------------------------------------------------------
+# S1 block score (readings R2, R3, R4)
+# ----------------------------------------------------------------------------
+def _exact_bound(qv, mv, Mv):
+    """exact rational Quest bound sum_c max(q_c M_c, q_c m_c)."""
+    s = Fraction(0)
+    for qc, lo, hi in zip(qv, mv, Mv):
+        a, b = Fraction(qc) * Fraction(hi), Fraction(qc) * Fraction(lo)
+        s += a if a > b else b
+    return s
+
+
+def _meta_from_blocks(store, n_req, hkv, max_blk):
+    meta = oracle.block_meta(store, key_stride=2 * 32 * D)
+    return meta.reshape(n_req, hkv, max_blk, 2, D)
+
+
+def test_score_exact_when_partial_sums_are_representable():
+    # small dyadic values: every product and partial sum is exact in fp64,
+    # so the oracle must equal the exact rational bound bit-for-bit.
+    rng = np.random.default_rng(7)
+    q = (rng.integers(-8, 9, size=(1, 1, D)) / 4.0).astype(np.float32)
+    keys = (rng.integers(-16, 17, size=(6, 2, 32, D)) / 8.0).astype(np.float32)
+    qs, ks = _bf16(q), _bf16(keys)
+    meta = _meta_from_blocks(ks, 1, 1, 6)
+    sc = oracle.block_score(qs, meta, np.array([6], np.int32))
+    qv = _val(qs)[0, 0]
+    mv = _val(meta)[0, 0]
+    for j in range(6):
+        ex = _exact_bound(qv, mv[j, 0], mv[j, 1])
+        assert Fraction(sc[0, 0, j]) == ex
+
+
+def test_score_within_rounding_of_exact_and_sound():
+    rng = synth.rng_for(900, 2)
+    n = 8
+    blocks = synth.kv_blocks(rng, n, D, synth.channel_scales(rng))
+    ks = _bf16(blocks)
+    qs = _bf16(rng.standard_normal((1, 1, D)))
+    meta = _meta_from_blocks(ks, 1, 1, n)
+    sc = oracle.block_score(qs, meta, np.array([n], np.int32))
+    qv = _val(qs)[0, 0]
+    mv = _val(meta)[0, 0]
+    kv = _val(ks)[:, 0]                       # [n][32][d]
+    u = 2.0 ** -53
+    for j in range(n):
+        ex = _exact_bound(qv, mv[j, 0], mv[j, 1])
+        mag = sum(abs(Fraction(qc)) * max(abs(Fraction(a)), abs(Fraction(b)))
+                  for qc, a, b in zip(qv, mv[j, 0], mv[j, 1]))
+        assert abs(Fraction(sc[0, 0, j]) - ex) <= Fraction(D * u) * mag
+        # bound soundness (P2): exact bound >= exact q.k of every token in the block
+        best_dot = max(sum(Fraction(a) * Fraction(b) for a, b in zip(qv, kv[j, t])) for t in range(32))
+        assert ex >= best_dot
+
+
+def test_score_identical_tokens_is_exact_dot_product():
+    # special case (P3): all tokens of a block equal -> M = m = k -> bound = q.k
+    rng = synth.rng_for(900, 3)
+    k1 = rng.standard_normal((5, 1, 1, D)).astype(np.float32)
+    blocks = np.broadcast_to(k1, (5, 2, 32, D)).copy()
+    ks = _bf16(blocks)
+    qs = _bf16(rng.standard_normal((1, 1, D)))
+    meta = _meta_from_blocks(ks, 1, 1, 5)
+    sc = oracle.block_score(qs, meta, np.array([5], np.int32))
+    qv, kv = _val(qs)[0, 0], _val(ks)[:, 0, 0]
+    for j in range(5):
+        dot = sum(Fraction(a) * Fraction(b) for a, b in zip(qv, kv[j]))
+        assert abs(Fraction(sc[0, 0, j]) - dot) <= Fraction(2.0 ** -45) * (1 + abs(dot))
+    # and it ranks blocks exactly as numpy's dot products do
+    order = np.argsort(-(kv @ qv), kind="stable")
+    np.testing.assert_array_equal(np.argsort(-sc[0, 0], kind="stable"), order)
+
+
+def test_score_gqa_is_max_over_group():
+    # reading R4: score of a KV head = max over its G query heads; hq = h*G + g
+    rng = synth.rng_for(900, 4)
+    B, Hq, Hkv, n = 2, 8, 2, 4
+    G = Hq // Hkv
+    q = (rng.integers(-4, 5, size=(B, Hq, D)) / 2.0).astype(np.float32)
+    keys = (rng.integers(-8, 9, size=(B * Hkv * n, 2, 32, D)) / 4.0).astype(np.float32)
+    qs, ks = _bf16(q), _bf16(keys)
+    meta = _meta_from_blocks(ks, B, Hkv, n)
+    sc = oracle.block_score(qs, meta, np.array([n, n - 1], np.int32))
+    qv, mv = _val(qs), _val(meta)
+    for b in range(B):
+        for h in range(Hkv):
+            for j in range(n - b):
+                per = [_exact_bound(qv[b, h * G + g], mv[b, h, j, 0], mv[b, h, j, 1]) for g in range(G)]
+                assert Fraction(sc[b, h, j]) == max(per)
+    assert np.isnan(sc[1, :, n - 1]).all()   # j >= n_blk untouched
+
+
+# ----------------------------------------------------------------------------
+# S2 top-k (readings R5, R6)
+# ----------------------------------------------------------------------------
+def _lexsort_topk(s, n, k):
+    j = np.arange(n)
+    order = np.lexsort((j, -s[:n]))
+    out = np.sort(order[:min(k, n)])
+    return np.concatenate([out, -np.ones(k - out.shape[0], dtype=np.int64)])
+
+
+@pytest.mark.parametrize("k", [1, 7, 64, 300])
+def test_topk_matches_numpy_lexsort(k):
+    rng = synth.rng_for(900, 5, k)
+    B, Hkv, max_blk = 3, 4, 256
+    scores = rng.standard_normal((B, Hkv, max_blk))
+    scores[0, 1, 10:20] = scores[0, 1, 5]          # tie suite straddling the boundary
+    scores[1, 2, :] = 0.5                          # all ties
+    n_blk = np.array([256, 200, 3], np.int32)
+    sel = oracle.topk(scores, n_blk, k)
+    for b in range(B):
+        for h in range(Hkv):
+            np.testing.assert_array_equal(sel[b, h], _lexsort_topk(scores[b, h], n_blk[b], k))
+
+
+def test_topk_invariants():
+    rng = synth.rng_for(900, 6)
+    s = np.round(rng.standard_normal((1, 1, 500)) * 4) / 4    # many ties
+    sel = oracle.topk(s, np.array([500], np.int32), 50)[0, 0]
+    chosen = set(sel.tolist())
+    assert list(sel) == sorted(sel)
+    mn = min(s[0, 0, j] for j in chosen)
+    for j in range(500):
+        if j not in chosen:
+            assert s[0, 0, j] <= mn
+            if s[0, 0, j] == mn:
+                assert all(c < j for c in chosen if s[0, 0, c] == mn)
+
+
+def test_needle_block_is_selected():
+    # P4: a block holding a key = alpha * q_hat with alpha large enough that its
+    # token logit exceeds every other block's bound is provably top-1.
+    rng = synth.rng_for(900, 7)
+    n = 64
+    blocks = synth.kv_blocks(rng, n, D)
+    q = rng.standard_normal(D).astype(np.float32)
+    jstar = 41
+    blocks[jstar, 0, 3] = 100.0 * q / np.linalg.norm(q)
+    ks, qs = _bf16(blocks), _bf16(q[None, None])
+    meta = _meta_from_blocks(ks, 1, 1, n)
+    sc = oracle.block_score(qs, meta, np.array([n], np.int32))
+    qv, kv = _val(qs)[0, 0], _val(ks)[:, 0]
+    needle_dot = float(kv[jstar, 3] @ qv)
+    others = [sc[0, 0, j] for j in range(n) if j != jstar]
+    assert needle_dot > max(others)           # the premise of the pin
+    for k in (1, 4, 16):
+        assert jstar in oracle.topk(sc, np.array([n], np.int32), k)[0, 0]
+
+
+# ----------------------------------------------------------------------------
+# S3 LRU (readings R11, R12)
+# ----------------------------------------------------------------------------
+def test_lru_hand_traced_fixture():
+    fx = json.load(open(os.path.join(GOLDEN, "lru_trace.json")))
+    pool = oracle.Pool(fx["num_slots"], fwd_len=fx["max_blk"])
+    for call in fx["calls"]:
+        sel = np.array(call["sel"], np.int32).reshape(1, 1, -1)
+        before = pool.copy()
+        r = oracle.lru(pool, sel, np.array(fx["req_ids"], np.int32), fx["layer"], fx["L"],
+                       fx["max_blk"], call["stamp"])
+        assert r["counts"].tolist() == call["counts"]
+        assert pool.slot_key.tolist() == call["slot_key"]
+        assert pool.slot_stamp.tolist() == call["slot_stamp"]
+        order = np.lexsort((np.arange(pool.num_slots), pool.slot_stamp))
+        assert order.tolist() == call["order"]
+        if call["counts"][3] == 0:
+            assert r["slot"].ravel().tolist() == call["slot"]
+            assert r["hit"].ravel().tolist() == call["hit"]
+            assert r["miss_keys"].tolist() == call["miss_keys"]
+            assert r["miss_slots"].tolist() == call["miss_slots"]
+        else:   # P7: capacity error leaves the state byte-identical
+            np.testing.assert_array_equal(pool.fwd, before.fwd)
+            np.testing.assert_array_equal(pool.slot_key, before.slot_key)
+            np.testing.assert_array_equal(pool.slot_stamp, before.slot_stamp)
+        # fwd is the inverse of slot_key
+        for s, key in enumerate(pool.slot_key):
+            if key >= 0:
+                assert pool.fwd[key] == s
+        assert (pool.fwd >= 0).sum() == (pool.slot_key >= 0).sum()
+
+
+@pytest.mark.parametrize("S", [1, 2, 3, 5, 8])
+def test_lru_one_key_per_call_equals_ordereddict(S):
+    # P5: with one key per call, batch-LRU is textbook LRU (collections.OrderedDict)
+    rng = np.random.default_rng(100 + S)
+    universe = 3 * S + 2
+    pool = oracle.Pool(S, fwd_len=64)
+    od = collections.OrderedDict()      # key -> slot, LRU first
+    used = 0
+    for t in range(1, 1500):
+        key = int(rng.integers(0, universe))
+        r = oracle.lru(pool, np.array([[[key]]], np.int32), np.array([0], np.int32), 0, 1, 64, t)
+        if key in od:
+            od.move_to_end(key)
+            assert r["hit"][0, 0, 0] == 1 and r["slot"][0, 0, 0] == od[key]
+        else:
+            if len(od) == S:
+                _, slot = od.popitem(last=False)
+            else:
+                slot, used = used, used + 1
+            od[key] = slot
+            assert r["hit"][0, 0, 0] == 0 and r["slot"][0, 0, 0] == slot
+        for k_, s_ in od.items():
+            assert pool.slot_key[s_] == k_
+
+
+def test_lru_invalid_key_is_error_without_mutation():
+    pool = oracle.Pool(4, fwd_len=16)
+    before = pool.copy()
+    r = oracle.lru(pool, np.array([[[3, 20]]], np.int32), np.array([0], np.int32), 0, 1, 32, 1)
+    assert r["counts"].tolist() == [0, 0, 0, 1]
+    np.testing.assert_array_equal(pool.fwd, before.fwd)
+    np.testing.assert_array_equal(pool.slot_stamp, before.slot_stamp)
+
+
+# ----------------------------------------------------------------------------
+# S4 gather
+# ----------------------------------------------------------------------------
+def test_gather_matches_numpy_fancy_index():
+    rng = np.random.default_rng(5)
+    host = rng.integers(0, 256, size=(50, 64), dtype=np.uint8)
+    pool = rng.integers(0, 256, size=(10, 64), dtype=np.uint8)
+    keys = np.array([3, 77, 49, 120], np.int64)        # 77 and 120 alias modulo 50
+    slots = np.array([9, 0, 4, 2], np.int32)
+    exp = pool.copy()
+    exp[slots] = host[keys % 50]
+    oracle.gather(host, 50, keys, slots, pool)
+    np.testing.assert_array_equal(pool, exp)
+
+
+# ----------------------------------------------------------------------------
+# S5 attention (readings R7, R9, R10)
+# ----------------------------------------------------------------------------
+def _sdpa(q, k, v, mask=None):
+    """torch scaled_dot_product_attention in float64 on CPU (library routine)."""
+    q = torch.from_numpy(q)[None, None, None]          # [1,1,1,d]
+    k = torch.from_numpy(k)[None, None]                 # [1,1,T,d]
+    v = torch.from_numpy(v)[None, None]
+    m = None if mask is None else torch.from_numpy(mask)[None, None, None]
+    return torch.nn.functional.scaled_dot_product_attention(q, k, v, attn_mask=m)[0, 0, 0].numpy()
+
+
+@pytest.mark.parametrize("dt", [synth.DT_BF16, synth.DT_F32])
+@pytest.mark.parametrize("tail_len", [0, 17])
+def test_attention_all_blocks_equals_dense_sdpa(dt, tail_len):
+    rng = synth.rng_for(900, 8, tail_len)
+    B, Hq, Hkv, n = 2, 4, 2, 6
+    G = Hq // Hkv
+    blocks = synth.kv_blocks(rng, B * Hkv * n, D)
+    tail = synth.kv_blocks(rng, B * Hkv, D).reshape(B, Hkv, 2, 32, D)
+    pool = synth.encode(blocks, dt)
+    tails = synth.encode(tail, dt)
+    qs = synth.encode(rng.standard_normal((B, Hq, D)), dt)
+    # pool slot of (b, h, j) = (b*Hkv + h)*n + j; k = n covers every block (shuffled order)
+    slot = np.empty((B, Hkv, n), np.int32)
+    for b in range(B):
+        for h in range(Hkv):
+            slot[b, h] = (b * Hkv + h) * n + rng.permutation(n)
+    tl = np.array([tail_len, tail_len // 2], np.int32)
+    out = oracle.attention(qs, pool, slot, tails, tl, 1.0 / math.sqrt(D))
+    pv, tv, qv = synth.decode_f64(pool, dt), synth.decode_f64(tails, dt), synth.decode_f64(qs, dt)
+    for b in range(B):
+        for hq in range(Hq):
+            h = hq // G
+            ids = np.arange(n) + (b * Hkv + h) * n
+            K = np.concatenate([pv[ids, 0].reshape(-1, D), tv[b, h, 0, :tl[b]]])
+            V = np.concatenate([pv[ids, 1].reshape(-1, D), tv[b, h, 1, :tl[b]]])
+            np.testing.assert_allclose(out[hq, b], _sdpa(qv[b, hq], K, V), rtol=0, atol=1e-12)
+
+
+def test_attention_subset_equals_masked_dense():
+    # P9: attending only to the selected blocks == dense attention with -inf outside them
+    rng = synth.rng_for(900, 9)
+    n = 10
+    blocks = synth.kv_blocks(rng, n, D)
+    pool = synth.encode(blocks, synth.DT_BF16)
+    qs = synth.encode(rng.standard_normal((1, 1, D)), synth.DT_BF16)
+    chosen = np.array([1, 4, 7, -1, -1], np.int32)
+    tails = synth.encode(synth.kv_blocks(rng, 1, D).reshape(1, 1, 2, 32, D), synth.DT_BF16)
+    out = oracle.attention(qs, pool, chosen.reshape(1, 1, -1), tails, np.array([5], np.int32),
+                           1.0 / math.sqrt(D))
+    pv, tv, qv = _val(pool), _val(tails), _val(qs)
+    K = np.concatenate([pv[:, 0].reshape(-1, D), tv[0, 0, 0]])
+    V = np.concatenate([pv[:, 1].reshape(-1, D), tv[0, 0, 1]])
+    mask = np.full(K.shape[0], -np.inf)
+    for j in (1, 4, 7):
+        mask[j * 32:(j + 1) * 32] = 0.0
+    mask[n * 32:n * 32 + 5] = 0.0
+    np.testing.assert_allclose(out[0, 0], _sdpa(qv[0, 0], K, V, mask), rtol=0, atol=1e-12)
+
+
+def test_attention_empty_set_is_zero():
+    pool = np.zeros((1, 2, 32, D), np.uint16)
+    tails = np.zeros((1, 1, 2, 32, D), np.uint16)
+    out = oracle.attention(np.zeros((1, 1, D), np.uint16), pool, np.full((1, 1, 3), -1, np.int32),
+                           tails, np.array([0], np.int32), 0.1)
+    assert (out == 0).all()
+
+
+def test_block_geometry_golden():
+    fx = json.load(open(os.path.join(GOLDEN, "block_geometry.json")))
+    assert fx["block_tokens"] * fx["head_dim"] * 2 * 2 == fx["bytes_per_head_block_kv_2byte"]
+    assert synth.BLOCK_TOKENS == fx["block_tokens"] and synth.HEAD_DIM == fx["head_dim"]
+    assert fx["token_budget"] // fx["block_tokens"] == synth.C2.topk
