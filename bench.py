@@ -1,0 +1,510 @@
+"""bench.py -- decode-step throughput of the SparseServe hot path on B200.
+
+One "step" = one decode step of the whole north-star path for every layer:
+S1+S2 ss_block_select -> S3 kv_cache_lookup_insert -> S4 flash_h2d_gather ->
+S5 sparse_decode_attn (+ S6 NCCL all-gather of per-head outputs when N > 1),
+over a batch of synthetic LWM-7B-shaped requests (BASELINE.json configs[1]:
+32 layers, 32 heads, d = 128, 128K context, batch 16, top-k 2048 tokens, all
+KV in pinned host DRAM).  Attention-path only: no QKV/O projections or FFN.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "sparse-decode tokens/s/GPU at 128K ctx; FlashH2D GB/s vs link peak; HBM % peak"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# workload
+# ----------------------------------------------------------------------------
+def workload_cfg(args, world: int):
+    wl = synth.C2
+    batch = wl.batch * world                     # weak scaling: 16 requests per GPU
+    assert wl.num_kv_heads % world == 0, "KV heads must divide across ranks"
+    return dict(name=wl.name, batch=batch, layers=wl.layers, num_q_heads=wl.num_q_heads,
+                num_kv_heads=wl.num_kv_heads, n_blk=wl.n_blk, max_blk=wl.max_blk, topk=wl.topk,
+                slots=wl.slots_per_layer, rho=wl.rho, context=wl.context)
+
+
+def gen_host_blocks_on_gpu(engine, host_t, phys_blocks, seed, meta_phys, chunk_blocks=16384):
+    """Fill pinned host KV with synthetic K (scaled N(0,1)) / V (N(0,1)) drawn on
+    the GPU (Philox, seeded) and build per-physical-block metadata with S0."""
+    from paper_2509_24626_b200 import ops
+    c = engine.cfg
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    scales = torch.from_numpy(synth.channel_scales(synth.rng_for(seed, 7))).cuda()
+    be = c.block_elems
+    for s in range(0, phys_blocks, chunk_blocks):
+        n = min(chunk_blocks, phys_blocks - s)
+        x = torch.randn(n, 2, 32, 128, device="cuda", generator=g, dtype=torch.float32)
+        x[:, 0] *= scales
+        xb = x.to(c.dtype).contiguous()
+        ops.block_meta_update(xb, meta_phys[s * 2 * 128:], n, key_stride=be)
+        host_t[s * be:(s + n) * be].copy_(xb.view(-1), non_blocking=False)
+        del x, xb
+
+
+def setup_engine(args, rank: int, world: int):
+    from paper_2509_24626_b200.engine import DecodeEngine, EngineConfig
+    W = workload_cfg(args, world)
+    hkv = W["num_kv_heads"] // world
+    hq = W["num_q_heads"] // world
+    cfg = EngineConfig(batch=W["batch"], layers=W["layers"], num_q_heads=hq, num_kv_heads=hkv,
+                       max_blk=W["max_blk"], topk=W["topk"], slots_per_layer=W["slots"],
+                       num_requests=W["batch"], dtype=torch.bfloat16)
+    eng = DecodeEngine(cfg)
+    # physical host pool: a prime number of max_blk runs (aliasing, R15)
+    runs = args.host_runs
+    phys = runs * cfg.max_blk
+    host_t = torch.empty(phys * cfg.block_elems, dtype=torch.bfloat16, pin_memory=True)
+    meta_phys = torch.empty(phys * 2 * 128, dtype=torch.bfloat16, device="cuda")
+    gen_host_blocks_on_gpu(eng, host_t, phys, seed=4000 + rank, meta_phys=meta_phys)
+    eng.set_host_kv(host_t, phys)
+    # logical metadata of (b, l, h, j) = metadata of physical block key % phys:
+    # whole 32-block tiles move together (key0 % phys is a multiple of max_blk)
+    tiles_per_pair = cfg.max_blk // 32
+    tile_elems = 32 * 2 * 128
+    mp = meta_phys.view(-1, tile_elems)
+    ar = torch.arange(tiles_per_pair, device="cuda")
+    for l in range(cfg.layers):
+        t0 = torch.tensor([eng.key0(b, l, h) % phys // 32 for b in range(cfg.batch)
+                           for h in range(cfg.num_kv_heads)], device="cuda")
+        idx = (t0[:, None] + ar[None, :]).reshape(-1)
+        eng.meta[l].view(-1, tile_elems).copy_(mp.index_select(0, idx))
+    del meta_phys, mp
+    eng.n_blk.fill_(W["n_blk"])
+    eng.tail_len.zero_()
+    torch.cuda.synchronize()
+    return eng, W
+
+
+def gen_queries(eng, steps, rho, seed):
+    """q_{t+1} = rho q_t + sqrt(1-rho^2) xi per (layer, request, head), bf16."""
+    c = eng.cfg
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    shape = (c.layers, c.batch, c.num_q_heads, 128)
+    cur = torch.randn(shape, device="cuda", generator=g)
+    out = torch.empty((steps,) + shape, dtype=torch.bfloat16, device="cuda")
+    s = math.sqrt(1 - rho * rho)
+    for t in range(steps):
+        if t:
+            cur = rho * cur + s * torch.randn(shape, device="cuda", generator=g)
+        out[t] = cur.to(torch.bfloat16)
+    return out
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+class StepTimers:
+    """CUDA events around each op of each layer, on the launching stream."""
+
+    def __init__(self):
+        self.ev = {"select": [], "cache": [], "gather": [], "attn": [], "allgather": []}
+
+    def mark(self, name):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.ev[name].append((s, e))
+        return s, e
+
+    def totals_ms(self):
+        return {k: sum(s.elapsed_time(e) for s, e in v) for k, v in self.ev.items()}
+
+    def counts(self):
+        return {k: len(v) for k, v in self.ev.items()}
+
+
+def run_step(eng, q_step, stamp, timers=None, pg=None, world=1, gathered=None):
+    from paper_2509_24626_b200 import ops
+    c = eng.cfg
+    for l in range(c.layers):
+        q = q_step[l]
+        def timed(name, fn):
+            if timers is None:
+                fn()
+            else:
+                s, e = timers.mark(name)
+                s.record()
+                fn()
+                e.record()
+        timed("select", lambda: ops.ss_block_select(q, eng.meta[l], eng.n_blk, c.max_blk, c.topk,
+                                                    eng.dims, eng.sel[l], eng.ws_select))
+        timed("cache", lambda: ops.kv_cache_lookup_insert(
+            eng.pools[l], eng.sel[l], eng.req_ids, l, c.layers, c.max_blk, c.topk, eng.dims, stamp,
+            eng.slot[l], eng.hit[l], eng.miss_keys[l], eng.miss_slots[l], eng.counts[l], eng.ws_cache))
+        timed("gather", lambda: ops.flash_h2d_gather(eng.host_ptr, eng.host_blocks, eng.miss_keys[l],
+                                                     eng.miss_slots[l], eng.counts[l], eng.E,
+                                                     eng.pool_kv[l], c.block_bytes))
+        timed("attn", lambda: ops.sparse_decode_attn(q, eng.pool_kv[l], eng.slot[l], c.topk,
+                                                     eng.tail_kv[l], eng.tail_len, eng.dims, eng.scale,
+                                                     eng.out[l], eng.ws_attn, counts=eng.counts[l]))
+        if world > 1:
+            timed("allgather", lambda: torch.distributed.all_gather_into_tensor(
+                gathered[l], eng.out[l], group=pg))
+
+
+def measure_h2d_peak(nbytes=1 << 30):
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    s.record()
+    for _ in range(3):
+        d.copy_(h, non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    gbs = 3 * nbytes / (s.elapsed_time(e) * 1e-3) / 1e9
+    del h, d
+    return gbs
+
+
+def cpu_sample(eng, W, q_np_step, n_req=1, n_layers=1):
+    """Time the oracle (as it stands, single thread) on a bounded sample of the
+    same workload: n_req requests x n_layers layers x all KV heads of one step,
+    starting from an empty pool (all misses), including S0 for the sampled
+    blocks.  Returns (tokens/s extrapolated to all layers, seconds, description)."""
+    import oracle
+    c = eng.cfg
+    host_np = eng.host_kv.view(torch.int16).numpy().view(np.uint16)
+    blocks = host_np.reshape(eng.host_blocks, 2, 32, 128)
+    t0 = time.perf_counter()
+    for l in range(n_layers):
+        meta = np.empty((n_req, c.num_kv_heads, c.max_blk, 2, 128), np.uint16)
+        for b in range(n_req):
+            for h in range(c.num_kv_heads):
+                p0 = eng.key0(b, l, h) % eng.host_blocks
+                meta[b, h, :W["n_blk"]] = oracle.block_meta(blocks[p0:p0 + W["n_blk"]], key_stride=2 * 32 * 128)
+        pool = oracle.Pool(n_req * c.num_kv_heads * c.topk, c.fwd_len, c.block_bytes)
+        oracle.decode_layer(q_np_step[l, :n_req], meta, np.full(n_req, W["n_blk"], np.int32), c.topk,
+                            pool, np.arange(n_req, dtype=np.int32), l, c.layers, c.max_blk, 1,
+                            host_np.view(np.uint8).reshape(eng.host_blocks, -1), eng.host_blocks,
+                            np.zeros((n_req, c.num_kv_heads, 2, 32, 128), np.uint16),
+                            np.zeros(n_req, np.int32), eng.scale)
+    dt = time.perf_counter() - t0
+    per_step_s = dt / n_layers * c.layers / n_req        # seconds per request-step, all layers
+    desc = (f"{n_req} request(s) x {n_layers} layer(s) x {c.num_kv_heads} KV heads of one C2 decode step "
+            f"(S0 for the sampled blocks + S1..S5 from an empty pool), extrapolated x{c.layers} layers")
+    return 1.0 / per_step_s, dt, desc
+
+
+def bench_ours(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = torch.distributed.group.WORLD
+    t_setup = time.time()
+    eng, W = setup_engine(args, rank, world)
+    c = eng.cfg
+    steps_total = args.warmup + args.steps
+    qs = gen_queries(eng, steps_total + 1, W["rho"], seed=5000 + rank)
+    gathered = None
+    if world > 1:
+        gathered = torch.empty(c.layers, c.num_q_heads * world, c.batch, 128, dtype=torch.float32,
+                               device="cuda")
+    h2d_peak = measure_h2d_peak()
+    setup_s = time.time() - t_setup
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (the first step is cold: every selected block misses)
+    cold_ms = None
+    for t in range(args.warmup):
+        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+        s.record()
+        run_step(eng, qs[t], stamp=t + 1, pg=pg, world=world, gathered=gathered)
+        e.record()
+        torch.cuda.synchronize()
+        if t == 0:
+            cold_ms = s.elapsed_time(e)
+    counts_before = eng.counts.clone()
+    # timed region
+    timers = StepTimers()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    start, end = torch.cuda.Event(True), torch.cuda.Event(True)
+    hits = torch.zeros(4, dtype=torch.int64, device="cuda")
+    start.record()
+    for t in range(args.warmup, steps_total):
+        run_step(eng, qs[t], stamp=t + 1, timers=timers, pg=pg, world=world, gathered=gathered)
+        hits += eng.counts.to(torch.int64).sum(0)
+    end.record()
+    barrier()
+    clocks = sampler.stop()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    tot = timers.totals_ms()
+    nlaunch = timers.counts()
+    hc = hits.cpu().tolist()
+    n_hits, n_miss, n_evict, n_err = hc
+    lookups = n_hits + n_miss
+    hit_rate = n_hits / lookups if lookups else 0.0
+    tokens = c.batch * args.steps                       # one token per request per step (all ranks: x world / world)
+    tokens_all = tokens                                 # batch already counts every rank's requests
+    value = tokens_all / (ms * 1e-3)
+
+    # ---- roofline of each kernel (algorithmic bytes / measured time) ----
+    hbm_peak, peak_src = _peaks()
+    pairs = c.pairs
+    meta_bytes = pairs * W["n_blk"] * 2 * 128 * 2 * c.layers * args.steps       # per timed region
+    q_bytes = c.batch * c.num_q_heads * 128 * 2 * c.layers * args.steps
+    attn_units = lookups                                  # selected blocks attended (tail_len = 0)
+    attn_bytes = attn_units * c.block_bytes + c.num_q_heads * c.batch * 128 * 4 * c.layers * args.steps
+    miss_bytes = n_miss * c.block_bytes
+    sel_gbs = (meta_bytes + q_bytes) / (tot["select"] * 1e-3) / 1e9
+    attn_gbs = attn_bytes / (tot["attn"] * 1e-3) / 1e9
+    h2d_gbs = miss_bytes / (tot["gather"] * 1e-3) / 1e9 if tot["gather"] > 0 else 0.0
+    kernels = {
+        "ss_block_select": {"bound": "hbm", "achieved": round(sel_gbs, 1), "peak": hbm_peak,
+                             "unit": "GB/s", "frac": round(sel_gbs / hbm_peak, 4),
+                             "ms_per_step": round(tot["select"] / args.steps, 3),
+                             "bytes_per_launch": int((meta_bytes + q_bytes) / nlaunch["select"])},
+        "sparse_decode_attn": {"bound": "hbm", "achieved": round(attn_gbs, 1), "peak": hbm_peak,
+                                "unit": "GB/s", "frac": round(attn_gbs / hbm_peak, 4),
+                                "ms_per_step": round(tot["attn"] / args.steps, 3),
+                                "bytes_per_launch": int(attn_bytes / nlaunch["attn"])},
+        "flash_h2d_gather": {"bound": "host-link", "achieved": round(h2d_gbs, 2),
+                              "peak": round(h2d_peak, 2), "unit": "GB/s",
+                              "frac": round(h2d_gbs / h2d_peak, 4) if h2d_peak else None,
+                              "ms_per_step": round(tot["gather"] / args.steps, 3),
+                              "bytes_per_launch": int(miss_bytes / max(1, nlaunch["gather"]))},
+        "kv_cache_lookup_insert": {"bound": "latency", "ms_per_step": round(tot["cache"] / args.steps, 3)},
+    }
+    if world > 1:
+        kernels["nccl_all_gather"] = {"ms_per_step": round(tot["allgather"] / args.steps, 3)}
+    dom = max(("ss_block_select", "sparse_decode_attn", "flash_h2d_gather"),
+              key=lambda k: kernels[k]["ms_per_step"])
+    dk = kernels[dom]
+    traffic = None
+    prof_t = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof_t):
+        traffic = json.load(open(prof_t)).get(dom)
+    roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"], "peak": dk["peak"],
+                "unit": "GB/s", "frac": dk["frac"], "traffic": traffic,
+                "peak_source": peak_src if dk["bound"] == "hbm" else "bulk pinned cudaMemcpy H2D, measured in this run"}
+
+    # ---- e2e through the public API with host buffers ----
+    q_host = torch.empty_like(qs[0], device="cpu").pin_memory()
+    out_host = torch.empty(eng.out.shape, dtype=torch.float32, pin_memory=True)
+    q_dev = torch.empty_like(qs[0])
+    q_host.copy_(qs[steps_total])
+    barrier()
+    e_s, e_e = torch.cuda.Event(True), torch.cuda.Event(True)
+    e2e_steps = max(3, args.steps // 2)
+    e_s.record()
+    for i in range(e2e_steps):
+        q_dev.copy_(q_host, non_blocking=True)
+        run_step(eng, q_dev, stamp=steps_total + 1 + i, pg=pg, world=world, gathered=gathered)
+        out_host.copy_(gathered if world > 1 else eng.out, non_blocking=True)
+    e_e.record()
+    barrier()
+    e_ms = e_s.elapsed_time(e_e)
+    if world > 1:
+        tt = torch.tensor([e_ms], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e_ms = float(tt.item())
+    e2e = {"value": round(c.batch * e2e_steps / (e_ms * 1e-3), 2), "unit": "tokens/s",
+           "h2d_bytes_per_step": int(q_host.numel() * q_host.element_size()),
+           "d2h_bytes_per_step": int(out_host.numel() * out_host.element_size()),
+           "steps": e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        q_np = qs[0].view(torch.int16).cpu().numpy().view(np.uint16)
+        v, secs, desc = cpu_sample(eng, W, q_np, n_req=args.cpu_req, n_layers=1)
+        cpu = {"value": round(v, 4), "unit": "tokens/s", "cores": 1, "kind": "oracle",
+               "sample": desc, "seconds": round(secs, 2)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded K~N(0,1)*lognormal channel scales, V~N(0,1), drifting q rho=0.99)",
+            "config": {"workload": W["name"], "batch_per_gpu": W["batch"] // world, "global_batch": W["batch"],
+                       "layers": c.layers, "q_heads": W["num_q_heads"], "kv_heads": W["num_kv_heads"],
+                       "head_dim": 128, "context": W["context"], "block_tokens": 32,
+                       "topk_blocks": c.topk, "hbm_cache_slots_per_layer": c.slots_per_layer,
+                       "host_pool_blocks": eng.host_blocks, "host_kv": "pinned DRAM, zero-copy (UVA)",
+                       "parallelism": f"kv-heads/{world} per GPU" if world > 1 else "1 GPU",
+                       "l2": "no flush needed: inputs larger than L2 (32 GiB metadata streamed per step)",
+                       "scope": "attention path only (no QKV/O projections, no FFN)"},
+            "hit_rate": round(hit_rate, 4), "misses_per_step": n_miss / args.steps,
+            "h2d_bytes_per_step": miss_bytes / args.steps,
+            "flash_h2d": {"achieved_gbs": kernels["flash_h2d_gather"]["achieved"],
+                          "link_peak_gbs": round(h2d_peak, 2), "link_theoretical_gbs": 63.0,
+                          "frac": kernels["flash_h2d_gather"]["frac"]},
+            "roofline": roofline, "kernels": kernels,
+            "cold_step_ms": round(cold_ms, 2) if cold_ms else None,
+            "e2e": e2e, "gpu_launches": int(args.steps * c.layers * 10),
+            "cpu_baseline": cpu, "clocks": clocks, "setup_s": round(setup_s, 1),
+            "errors_in_timed_region": n_err,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------
+# reference arm: the CPU oracle on a bounded sample of the same workload
+# ----------------------------------------------------------------------------
+def bench_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    wl = synth.C2
+    n_req, hkv, n_blk, k = 1, 4, wl.n_blk, wl.topk        # bounded sample per step
+    max_blk = wl.max_blk
+    rng = synth.rng_for(6000, 1)
+    scales = synth.channel_scales(rng)
+    blocks = synth.encode(synth.kv_blocks(rng, hkv * n_blk, 128, scales), synth.DT_BF16)
+    host_u8 = blocks.view(np.uint8).reshape(hkv * n_blk, -1)
+    qs = synth.encode(synth.queries(rng, args.warmup + args.steps, (n_req, hkv, 128), wl.rho), synth.DT_BF16)
+    fwd_len = n_req * 1 * hkv * max_blk
+    pool = oracle.Pool(4 * hkv * k, fwd_len, 16384)
+    meta = oracle.block_meta(blocks, key_stride=2 * 32 * 128).reshape(n_req, hkv, n_blk, 2, 128)
+    times = []
+    for t in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.decode_layer(qs[t], meta, np.array([n_blk], np.int32), k, pool, np.zeros(1, np.int32), 0, 1,
+                            max_blk, t + 1, host_u8, hkv * n_blk, np.zeros((1, hkv, 2, 32, 128), np.uint16),
+                            np.zeros(1, np.int32), 1.0 / math.sqrt(128))
+        if t >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    sec = sum(times)
+    # one sampled step = 1 request x hkv of 32 KV heads x 1 of 32 layers
+    frac = (hkv / wl.num_kv_heads) / wl.layers
+    tok_s = args.steps * frac / sec
+    desc = (f"oracle S1..S5 on 1 request x {hkv} of 32 KV heads x 1 of 32 layers of C2 per step "
+            f"(metadata prebuilt), scaled to whole decode steps")
+    line = {"impl": "reference", "metric": METRIC, "value": round(tok_s, 5), "unit": "tokens/s",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 / tok_s * 1, 2), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": {"workload": wl.name},
+            "cpu_baseline": {"value": round(tok_s, 5), "unit": "tokens/s", "cores": 1, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": round(tok_s, 5), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--host-runs", type=int, default=251,
+                    help="physical host KV pool = host_runs x max_blk blocks (251 -> 15.7 GiB)")
+    ap.add_argument("--cpu-req", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "W >= 3 warm-up steps"
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()

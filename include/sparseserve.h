@@ -1,0 +1,208 @@
+/*
+ * sparseserve.h -- C ABI of the B200-native SparseServe decode hot path
+ * (arXiv 2509.24626, "SparseServe"), libsparseserve.so.
+ *
+ * One decode step, per layer, runs the calls below in this order (PAPER.md:124
+ * §3.1 "Model Executor": sparse attention for decoding requests; the indices of
+ * the required KV blocks are sent to the KV cache manager to trigger loading):
+ *
+ *   ss_block_select        S1+S2  score every full 32-token block from its
+ *                                 metadata, keep the top-k per (request, KV head)
+ *   kv_cache_lookup_insert S3     HBM block cache: hits, LRU victims, miss list
+ *   flash_h2d_gather       S4     FlashH2D: zero-copy gather of missed blocks
+ *                                 from pinned host DRAM into HBM cache slots
+ *   sparse_decode_attn     S5     attention over the selected blocks + tail
+ *
+ * and block_meta_update (S0) runs when a block fills.
+ *
+ * Conventions (all calls):
+ *  - Every pointer is caller-owned.  "device" = cudaMalloc'd (or torch) memory
+ *    on the current device; "host-mapped" = pinned host memory whose DEVICE
+ *    address is passed (cudaHostAlloc / cudaHostRegister(...Mapped...) +
+ *    cudaHostGetDevicePointer; under UVA that equals the host address).  The
+ *    library never allocates, frees or keeps global state; calls are reentrant.
+ *  - `stream` is a cudaStream_t passed as void*.  Every call is asynchronous on
+ *    it and never synchronises with the host.
+ *  - Host-side argument errors return SS_ERR_INVALID_ARG / SS_ERR_UNSUPPORTED
+ *    before anything is launched.  A failed launch returns SS_ERR_CUDA and
+ *    leaves cudaGetLastError() set.
+ *  - Device-side errors (invalid cache key, cache capacity) are reported in the
+ *    `counts` word written by kv_cache_lookup_insert; flash_h2d_gather and
+ *    sparse_decode_attn given that `counts` become no-ops when counts[3] != 0.
+ *  - Fixed geometry: head_dim = 128, block_tokens = 32 (§1:
+ *    32-token blocks, 16 KB per LWM-7B head-block).  Layouts are dense and
+ *    C-contiguous; all base pointers 16-byte aligned.
+ *  - dtype: SS_BF16 (storage bf16, the paper's 2-byte KV) or
+ *    SS_F32.  Scores are float64, attention accumulates and outputs float32.
+ *
+ * Semantics are defined by the CPU oracle (oracle/oracle.c) and DESIGN.md §3
+ * readings R1..R16; the CUDA path must match it bit-exactly for indices,
+ * masks, cache state and gathered bytes, and within 2e-3 (bf16) / 1e-5 (f32)
+ * max-abs for attention outputs.
+ */
+#ifndef SPARSESERVE_H_
+#define SPARSESERVE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SS_OK = 0,
+    SS_ERR_INVALID_ARG = 1,
+    SS_ERR_UNSUPPORTED = 2,
+    SS_ERR_CAPACITY = 3,
+    SS_ERR_CUDA = 4
+} ss_status;
+
+typedef enum { SS_BF16 = 0, SS_F32 = 1 } ss_dtype;
+
+typedef struct {
+    int32_t batch;        /* B: requests in the decode batch                       */
+    int32_t num_q_heads;  /* Hq                                                    */
+    int32_t num_kv_heads; /* Hkv; Hq % Hkv == 0, G = Hq/Hkv in {1,2,4,8}           */
+    int32_t head_dim;     /* d: must be 128                                         */
+    int32_t block_tokens; /* must be 32                                             */
+} ss_dims;
+
+/* ---------------------------------------------------------------------------
+ * Metadata layout (HBM), shared by block_meta_update and ss_block_select.
+ *
+ * Logical index of a block: idx = (b * Hkv + h) * max_blk + j, max_blk % 32 == 0.
+ * Logical content: {min[d], max[d]} per channel over the block's 32 keys
+ * (PAPER.md:94 bounding cuboid; Quest min/max, reading R1).
+ * Physical layout ("tiled", chosen so a warp reading 32 consecutive blocks
+ * issues fully coalesced 512-byte loads): blocks are grouped in tiles of 32,
+ * tile T = idx / 32, row r = idx % 32.  With CPC = 16 / sizeof(elem) channels
+ * per 16-byte chunk (8 for bf16, 4 for f32), element (channel c, mm = 0 for
+ * min / 1 for max) lives at element offset
+ *     T * (64 * d)  +  (((c / CPC) * 2 + mm) * 32 + r) * CPC  +  c % CPC.
+ * A tile is 32 * 2 * d elements (16 KiB in bf16).  This is a pure permutation
+ * of the logical [..][max_blk][2][d] array (tests/layout.py).
+ * ------------------------------------------------------------------------- */
+
+/* S0  block_meta_update -- PAPER.md:125 "Once a KV block reaches its
+ * capacity, its associated metadata is created."
+ *   keys      device, dtype dt: block i's 32 keys at keys + i*key_stride
+ *             (elements), laid out [32][d].  key_stride = 32*d for packed keys,
+ *             2*32*d to read the K half of [2][32][d] KV blocks in place.
+ *   dst_idx   device int64 [n]: logical meta index per block, or NULL = 0..n-1.
+ *   n         number of blocks (0 is a no-op).
+ *   meta      device, tiled layout above; per-channel min/max under the total
+ *             order of the bit patterns (-0 < +0; finite inputs only). */
+ss_status block_meta_update(const void* keys, int64_t key_stride, const int64_t* dst_idx,
+                            int64_t n, void* meta, ss_dtype dt, int32_t head_dim,
+                            void* stream);
+
+/* S1+S2  ss_block_select -- PAPER.md:94 "compute dot products between the
+ * metadata vectors and the query token to obtain approximate attention scores
+ * for all KV blocks ... select the top-k most critical KV blocks".
+ *   q        device [B][Hq][d] dtype dt.
+ *   meta     device, tiled layout, max_blk blocks per (b, h).
+ *   n_blk    device int32 [B]: full blocks of request b (0 <= n_blk <= max_blk).
+ *   k        >= 1 blocks per (b, h).
+ *   sel      device int32 [B][Hkv][k] out: the min(k, n_blk[b]) blocks with the
+ *            largest score S(j) = max_{g<G} sum_{c=0..d-1} max(q_c M_c, q_c m_c)
+ *            (float64, sequential in c, +0 canonical), ties -> lower j,
+ *            written in ascending j, -1 padded.
+ *   scores   device float64 [B][Hkv][max_blk] out (j < n_blk only), or NULL.
+ *   ws       device workspace of ss_workspace_size(SS_WS_SELECT, ...) bytes,
+ *            ZERO-FILLED ONCE before first use; every call leaves it zeroed. */
+ss_status ss_block_select(const void* q, const void* meta, const int32_t* n_blk,
+                          int32_t max_blk, int32_t k, ss_dims dims, ss_dtype dt, int32_t* sel,
+                          double* scores, void* ws, size_t ws_bytes, void* stream);
+
+/* S3  kv_cache_lookup_insert -- PAPER.md:124-125: the executor sends the
+ * indices of the required blocks to the KV cache manager; hot blocks are cached
+ * in the remaining HBM with LRU eviction; DRAM is the authoritative home (no
+ * write-back).  One pool per (GPU, layer), shared by all requests and heads
+ * (reading R11).  All pool arrays are device memory owned by the caller:
+ *   fwd        int32 [fwd_len]: key -> slot, -1 if not cached.  Initially -1.
+ *   slot_key   int64 [S]: slot -> key, -1 if empty.          Initially -1.
+ *   slot_stamp int64 [S]: stamp of last use, -1 if never used. Initially -1.
+ *   order      int32 [S]: slots sorted by (slot_stamp, slot).  Initially 0..S-1.
+ * Batch-LRU (reading R12): key = ((req_ids[b]*L + layer)*Hkv + h)*max_blk + j
+ * for every sel[b][h][r] >= 0, in canonical (b, h, r) order.  Hits keep their
+ * slot and get slot_stamp = stamp.  The i-th miss takes the i-th slot, in
+ * (stamp, slot) order, among slots not hit by this call with slot_stamp < stamp;
+ * a previous key of that slot is evicted (fwd = -1).
+ *   slot_out   int32 [B][Hkv][k]: cache slot per selection (-1 for padding).
+ *   hit_out    uint8 [B][Hkv][k]: 1 = hit.
+ *   miss_keys  int64 [B*Hkv*k], miss_slots int32 [B*Hkv*k]: the first counts[1]
+ *              entries list the misses in canonical order.
+ *   counts     int32 [4] = {hits, misses, evictions, status}; status 0 = OK,
+ *              1 = a key >= fwd_len (nothing counted), 3 = more misses than
+ *              evictable slots.  On status != 0 the pool is left byte-identical
+ *              and the other outputs are unspecified.
+ * Preconditions: req_ids unique; stamp >= every stamp previously used on the
+ * pool.  ws: ss_workspace_size(SS_WS_CACHE, ...) bytes, no initialisation. */
+typedef struct {
+    int32_t* fwd;
+    int64_t fwd_len;
+    int64_t* slot_key;
+    int64_t* slot_stamp;
+    int32_t* order;
+    int32_t num_slots;
+} ss_cache_pool;
+
+ss_status kv_cache_lookup_insert(ss_cache_pool pool, const int32_t* sel, const int32_t* req_ids,
+                                 int32_t layer, int32_t num_layers, int32_t max_blk, int32_t k,
+                                 ss_dims dims, int64_t stamp, int32_t* slot_out,
+                                 uint8_t* hit_out, int64_t* miss_keys, int32_t* miss_slots,
+                                 int32_t* counts, void* ws, size_t ws_bytes, void* stream);
+
+/* S4  flash_h2d_gather -- PAPER.md:143-149 §3.2.1 FlashH2D: one kernel loads
+ * all selected, missing blocks from DRAM over UVA (GPU-direct, zero-copy).
+ *   host_kv     host-mapped pinned memory, host_blocks blocks of block_bytes;
+ *               logical key -> physical host block key % host_blocks
+ *               (reading R15; host_blocks > every key = no aliasing).
+ *   miss_keys / miss_slots / counts: as written by kv_cache_lookup_insert
+ *               (device); the miss count counts[1] is read ON DEVICE, capped
+ *               at max_misses; no-op if counts[3] != 0.
+ *   pool_kv     device [S][block_bytes]; slot s <- host block, byte-exact.
+ *   block_bytes multiple of 16 (16384 for a bf16 [2][32][128] block). */
+ss_status flash_h2d_gather(const void* host_kv, int64_t host_blocks, const int64_t* miss_keys,
+                           const int32_t* miss_slots, const int32_t* counts, int32_t max_misses,
+                           void* pool_kv, int64_t block_bytes, void* stream);
+
+/* S5  sparse_decode_attn -- PAPER.md:71-72 §2.1 (S = QK^T/sqrt(d), P =
+ * softmax(S), O = PV) restricted to the selected blocks.
+ *   q         device [B][Hq][d] dtype dt.
+ *   pool_kv   device [S][2][32][d] dtype dt (K then V of one head-block,
+ *             PAPER.md:137 (H,N,D) layout).
+ *   slot      device int32 [B][Hkv][k] (slot_out of S3; -1 entries skipped).
+ *   tail_kv   device [B][Hkv][2][32][d]: the partial block of each (b, h);
+ *             its first tail_len[b] tokens are always attended (reading R7).
+ *   tail_len  device int32 [B], 0..31.
+ *   softmax_scale  normally 1/sqrt(d).
+ *   counts    device int32[4] from S3 or NULL; no-op if counts[3] != 0.
+ *   out       device float32 [Hq][B][d] (head-major).  Softmax runs over the
+ *             selected tokens + tail only (reading R9); empty set -> 0.
+ *   ws        ss_workspace_size(SS_WS_ATTN, ...) bytes, ZERO-FILLED ONCE
+ *             before first use; every call leaves it zeroed. */
+ss_status sparse_decode_attn(const void* q, const void* pool_kv, const int32_t* slot, int32_t k,
+                             const void* tail_kv, const int32_t* tail_len, ss_dims dims,
+                             ss_dtype dt, float softmax_scale, const int32_t* counts,
+                             float* out, void* ws, size_t ws_bytes, void* stream);
+
+#define SS_WS_SELECT 0
+#define SS_WS_CACHE 1
+#define SS_WS_ATTN 2
+
+/* Workspace bytes for call `which` (SS_WS_*); num_slots is used by SS_WS_CACHE. */
+size_t ss_workspace_size(int32_t which, ss_dims dims, int32_t max_blk, int32_t k,
+                         int32_t num_slots);
+
+/* Device address of pinned host memory (cudaHostGetDevicePointer). */
+ss_status ss_host_device_pointer(void* host, void** dev);
+
+const char* ss_status_string(ss_status s);
+const char* ss_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSESERVE_H_ */

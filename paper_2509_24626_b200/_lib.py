@@ -1,0 +1,74 @@
+"""ctypes loader for libsparseserve.so (the C ABI in include/sparseserve.h).
+
+There is no fallback: if the library is missing or fails to load, importing
+the ops raises.  Build it with `python -m paper_2509_24626_b200.build` or
+`__graft_entry__.build()`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libsparseserve.so")
+
+SS_OK, SS_ERR_INVALID_ARG, SS_ERR_UNSUPPORTED, SS_ERR_CAPACITY, SS_ERR_CUDA = range(5)
+SS_BF16, SS_F32 = 0, 1
+SS_WS_SELECT, SS_WS_CACHE, SS_WS_ATTN = 0, 1, 2
+
+EXPORTS = ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert", "flash_h2d_gather",
+           "sparse_decode_attn", "ss_workspace_size", "ss_host_device_pointer",
+           "ss_status_string", "ss_version")
+
+
+class SSDims(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("num_q_heads", ctypes.c_int32),
+                ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("block_tokens", ctypes.c_int32)]
+
+
+class SSCachePool(ctypes.Structure):
+    _fields_ = [("fwd", ctypes.c_void_p), ("fwd_len", ctypes.c_int64),
+                ("slot_key", ctypes.c_void_p), ("slot_stamp", ctypes.c_void_p),
+                ("order", ctypes.c_void_p), ("num_slots", ctypes.c_int32)]
+
+
+class SparseServeError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(nvcc -gencode arch=compute_100a,code=sm_100a); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, SZ, F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_float
+    L.block_meta_update.argtypes = [P, I64, P, I64, P, I32, I32, P]
+    L.ss_block_select.argtypes = [P, P, P, I32, I32, SSDims, I32, P, P, P, SZ, P]
+    L.kv_cache_lookup_insert.argtypes = [SSCachePool, P, P, I32, I32, I32, I32, SSDims, I64, P, P,
+                                         P, P, P, P, SZ, P]
+    L.flash_h2d_gather.argtypes = [P, I64, P, P, P, I32, P, I64, P]
+    L.sparse_decode_attn.argtypes = [P, P, P, I32, P, P, SSDims, I32, F, P, P, P, SZ, P]
+    L.ss_workspace_size.argtypes = [I32, SSDims, I32, I32, I32]
+    L.ss_workspace_size.restype = SZ
+    L.ss_host_device_pointer.argtypes = [P, ctypes.POINTER(ctypes.c_void_p)]
+    L.ss_status_string.argtypes = [I32]
+    L.ss_status_string.restype = ctypes.c_char_p
+    L.ss_version.restype = ctypes.c_char_p
+    for name in ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert",
+                 "flash_h2d_gather", "sparse_decode_attn", "ss_host_device_pointer"):
+        getattr(L, name).restype = I32
+    _lib = L
+    return L
+
+
+def check(status: int, what: str) -> None:
+    if status != SS_OK:
+        msg = load().ss_status_string(status).decode()
+        raise SparseServeError(f"{what} failed: {msg} ({status})")

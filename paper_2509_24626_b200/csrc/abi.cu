@@ -1,0 +1,157 @@
+// abi.cu -- the extern "C" boundary of libsparseserve.so (include/sparseserve.h):
+// host-side argument validation, then one launch sequence per call.  No state,
+// no allocation, no host synchronisation.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace ss {
+ss_status launch_meta_update(const void* keys, int64_t key_stride, const int64_t* dst_idx,
+                             int64_t n, void* meta, ss_dtype dt, cudaStream_t stream);
+ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_blk, int max_blk,
+                              int k, const ss_dims& d, ss_dtype dt, int32_t* sel, double* scores,
+                              void* ws, cudaStream_t stream);
+size_t select_ws_bytes(const ss_dims& d, int max_blk, int k);
+ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int32_t* req_ids,
+                       int layer, int num_layers, int max_blk, int k, const ss_dims& d,
+                       int64_t stamp, int32_t* slot_out, uint8_t* hit_out, int64_t* miss_keys,
+                       int32_t* miss_slots, int32_t* counts, void* ws, cudaStream_t stream);
+size_t cache_ws_bytes(const ss_dims& d, int k, int S);
+ss_status launch_flash_h2d(const void* host_kv, int64_t host_blocks, const int64_t* miss_keys,
+                           const int32_t* miss_slots, const int32_t* counts, int max_misses,
+                           void* pool_kv, int64_t block_bytes, cudaStream_t stream);
+ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* slot, int k,
+                             const void* tail_kv, const int32_t* tail_len, const ss_dims& d,
+                             ss_dtype dt, float scale, const int32_t* counts, float* out, void* ws,
+                             cudaStream_t stream);
+size_t attn_ws_bytes(const ss_dims& d, int k, ss_dtype dt);
+}  // namespace ss
+
+namespace {
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+bool dt_ok(ss_dtype dt) { return dt == SS_BF16 || dt == SS_F32; }
+bool dims_ok(const ss_dims& d) {
+    if (d.batch < 1 || d.num_q_heads < 1 || d.num_kv_heads < 1) return false;
+    if (d.num_q_heads % d.num_kv_heads) return false;
+    return true;
+}
+ss_status dims_supported(const ss_dims& d) {
+    if (d.head_dim != ss::kHeadDim || d.block_tokens != ss::kBlockTokens) return SS_ERR_UNSUPPORTED;
+    int G = d.num_q_heads / d.num_kv_heads;
+    if (G != 1 && G != 2 && G != 4 && G != 8) return SS_ERR_UNSUPPORTED;
+    return SS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+ss_status block_meta_update(const void* keys, int64_t key_stride, const int64_t* dst_idx,
+                            int64_t n, void* meta, ss_dtype dt, int32_t head_dim, void* stream) {
+    if (n < 0 || !dt_ok(dt)) return SS_ERR_INVALID_ARG;
+    if (n == 0) return SS_OK;
+    if (!keys || !meta || key_stride < 32 * head_dim) return SS_ERR_INVALID_ARG;
+    if (head_dim != ss::kHeadDim) return SS_ERR_UNSUPPORTED;
+    return ss::launch_meta_update(keys, key_stride, dst_idx, n, meta, dt, (cudaStream_t)stream);
+}
+
+ss_status ss_block_select(const void* q, const void* meta, const int32_t* n_blk, int32_t max_blk,
+                          int32_t k, ss_dims dims, ss_dtype dt, int32_t* sel, double* scores,
+                          void* ws, size_t ws_bytes, void* stream) {
+    if (!q || !meta || !n_blk || !sel || !dt_ok(dt) || !dims_ok(dims)) return SS_ERR_INVALID_ARG;
+    if (k < 1 || max_blk < 0 || (max_blk % 32) != 0) return SS_ERR_INVALID_ARG;
+    if (!aligned16(q) || !aligned16(meta)) return SS_ERR_INVALID_ARG;
+    ss_status st = dims_supported(dims);
+    if (st != SS_OK) return st;
+    size_t need = ss::select_ws_bytes(dims, max_blk, k);
+    if (ws_bytes < need || (need && !ws)) return SS_ERR_INVALID_ARG;
+    return ss::launch_block_select(q, meta, n_blk, max_blk, k, dims, dt, sel, scores, ws,
+                                   (cudaStream_t)stream);
+}
+
+ss_status kv_cache_lookup_insert(ss_cache_pool pool, const int32_t* sel, const int32_t* req_ids,
+                                 int32_t layer, int32_t num_layers, int32_t max_blk, int32_t k,
+                                 ss_dims dims, int64_t stamp, int32_t* slot_out,
+                                 uint8_t* hit_out, int64_t* miss_keys, int32_t* miss_slots,
+                                 int32_t* counts, void* ws, size_t ws_bytes, void* stream) {
+    if (!pool.fwd || !pool.slot_key || !pool.slot_stamp || !pool.order || pool.num_slots < 1 ||
+        pool.fwd_len < 1)
+        return SS_ERR_INVALID_ARG;
+    if (!sel || !req_ids || !slot_out || !hit_out || !miss_keys || !miss_slots || !counts)
+        return SS_ERR_INVALID_ARG;
+    if (!dims_ok(dims) || k < 1 || max_blk < 1 || num_layers < 1 || layer < 0 ||
+        layer >= num_layers)
+        return SS_ERR_INVALID_ARG;
+    if ((int64_t)dims.batch * dims.num_kv_heads * k > (int64_t)1 << 30) return SS_ERR_UNSUPPORTED;
+    size_t need = ss::cache_ws_bytes(dims, k, pool.num_slots);
+    if (!ws || ws_bytes < need) return SS_ERR_INVALID_ARG;
+    return ss::launch_cache(pool, sel, req_ids, layer, num_layers, max_blk, k, dims, stamp,
+                            slot_out, hit_out, miss_keys, miss_slots, counts, ws,
+                            (cudaStream_t)stream);
+}
+
+ss_status flash_h2d_gather(const void* host_kv, int64_t host_blocks, const int64_t* miss_keys,
+                           const int32_t* miss_slots, const int32_t* counts, int32_t max_misses,
+                           void* pool_kv, int64_t block_bytes, void* stream) {
+    if (!host_kv || !miss_keys || !miss_slots || !counts || !pool_kv) return SS_ERR_INVALID_ARG;
+    if (host_blocks < 1 || max_misses < 0 || block_bytes < 16 || (block_bytes % 16) != 0)
+        return SS_ERR_INVALID_ARG;
+    if (!aligned16(host_kv) || !aligned16(pool_kv)) return SS_ERR_INVALID_ARG;
+    return ss::launch_flash_h2d(host_kv, host_blocks, miss_keys, miss_slots, counts, max_misses,
+                                pool_kv, block_bytes, (cudaStream_t)stream);
+}
+
+ss_status sparse_decode_attn(const void* q, const void* pool_kv, const int32_t* slot, int32_t k,
+                             const void* tail_kv, const int32_t* tail_len, ss_dims dims,
+                             ss_dtype dt, float softmax_scale, const int32_t* counts, float* out,
+                             void* ws, size_t ws_bytes, void* stream) {
+    if (!q || !pool_kv || !slot || !tail_kv || !tail_len || !out || !dt_ok(dt) || !dims_ok(dims))
+        return SS_ERR_INVALID_ARG;
+    if (k < 1) return SS_ERR_INVALID_ARG;
+    if (!aligned16(q) || !aligned16(pool_kv) || !aligned16(tail_kv) || !aligned16(out))
+        return SS_ERR_INVALID_ARG;
+    ss_status st = dims_supported(dims);
+    if (st != SS_OK) return st;
+    size_t need = ss::attn_ws_bytes(dims, k, dt);
+    if (!ws || ws_bytes < need) return SS_ERR_INVALID_ARG;
+    return ss::launch_sparse_attn(q, pool_kv, slot, k, tail_kv, tail_len, dims, dt, softmax_scale,
+                                  counts, out, ws, (cudaStream_t)stream);
+}
+
+size_t ss_workspace_size(int32_t which, ss_dims dims, int32_t max_blk, int32_t k,
+                         int32_t num_slots) {
+    if (!dims_ok(dims) || k < 1) return 0;
+    switch (which) {
+        case SS_WS_SELECT:
+            return ss::select_ws_bytes(dims, max_blk, k);
+        case SS_WS_CACHE:
+            return ss::cache_ws_bytes(dims, k, num_slots);
+        case SS_WS_ATTN:
+            // sized for the larger (bf16 / f32 use different warp counts)
+            {
+                size_t a = ss::attn_ws_bytes(dims, k, SS_BF16), b = ss::attn_ws_bytes(dims, k, SS_F32);
+                return a > b ? a : b;
+            }
+        default:
+            return 0;
+    }
+}
+
+ss_status ss_host_device_pointer(void* host, void** dev) {
+    if (!host || !dev) return SS_ERR_INVALID_ARG;
+    return cudaHostGetDevicePointer(dev, host, 0) == cudaSuccess ? SS_OK : SS_ERR_CUDA;
+}
+
+const char* ss_status_string(ss_status s) {
+    switch (s) {
+        case SS_OK: return "SS_OK";
+        case SS_ERR_INVALID_ARG: return "SS_ERR_INVALID_ARG";
+        case SS_ERR_UNSUPPORTED: return "SS_ERR_UNSUPPORTED";
+        case SS_ERR_CAPACITY: return "SS_ERR_CAPACITY";
+        case SS_ERR_CUDA: return "SS_ERR_CUDA";
+        default: return "SS_ERR_UNKNOWN";
+    }
+}
+
+const char* ss_version(void) { return "sparseserve-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

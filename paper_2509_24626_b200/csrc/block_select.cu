@@ -1,0 +1,359 @@
+// block_select.cu -- S1 block scoring + S2 top-k ("DSAs compute
+// dot products between the metadata vectors and the query token to obtain
+// approximate attention scores for all KV blocks.  DSAs then select the top-k
+// most critical KV blocks"; readings R2-R6 in DESIGN.md).
+//
+// Score (must be bit-identical to oracle/oracle.c or_block_score):
+//   S(j) = max_g  sum_{c=0..127} max(q_{g,c} * M_{j,c}, q_{g,c} * m_{j,c})
+// in float64, summed sequentially c = 0..127 from +0.0, then +0.0.
+//
+// Exactness argument.  With q' = q * 2^896 and X' = X * 2^-896 (both exact in
+// float64 for every finite bf16/f32 X, including subnormals), the product
+// q' * X' equals q * X exactly, and one DFMA rounds (acc + q*X) once -- the same
+// rounding as the oracle's rounded sum of an exact product.  X' is built from
+// the storage bits with integer ops only (sign | exp/mantissa >> 3): no F2F
+// conversions.  max(q*M, q*m) = q+ * M + q- * m with q+ = max(q,0),
+// q- = min(q,0); the extra term is an exact +-0 and leaves acc unchanged (acc is
+// never -0), so two DFMAs per (head, channel) reproduce the oracle's sum.
+//
+// Work decomposition.  Grid (chunks, B*Hkv); a CTA scores CH = 2048 blocks of one
+// (b, h) pair.  Warp w owns metadata tiles w, w+8, ...; lane r of a warp owns
+// block r of the tile, so every 16-byte chunk load of the warp is one
+// contiguous 512-byte segment of the tiled layout (fully coalesced, streaming,
+// no L1 allocation).  Scores become order-preserving 64-bit keys in shared
+// memory; a CTA-wide radix select (8-bit digits, MSB first) finds the k-th
+// largest key, ties broken by lower block index, and the chosen blocks are
+// compacted in ascending order.  With more than one chunk per pair, chunk
+// candidates go to the workspace and the LAST CTA of the pair (atomic ticket,
+// self-resetting) merges them with the same select.  The global top-k is always
+// inside the union of per-chunk top-k sets, so the result is exact.
+//
+// Roofline: HBM-bound on the metadata stream: 512 B per block per (b, h) in
+// bf16 (1 KiB f32); fp64 work = 2*G*128 DFMA per block.
+#include "common.cuh"
+
+namespace ss {
+
+constexpr int kSelThreads = 256;
+constexpr int kSelWarps = kSelThreads / 32;
+constexpr int kSelChunk = 2048;  // blocks per CTA
+constexpr int kSelMaxMerge = 8192;
+
+struct SelSmemLayout {
+    // qpn[c*G + g] = (q+ * 2^896, q- * 2^896)
+    static size_t bytes(int G, int nkeys) {
+        return (size_t)kHeadDim * G * 16 + (size_t)nkeys * 8 + (size_t)nkeys * 4 + 256 * 4 + 64 * 4;
+    }
+};
+
+__device__ __forceinline__ uint64_t ord_key(double s) {
+    uint64_t b = (uint64_t)__double_as_longlong(s);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// bf16 pair word -> scaled float64 of the low / high element (value * 2^-896).
+__device__ __forceinline__ double bf16lo_scaled(uint32_t w) {
+    uint32_t u = w << 16;
+    return __hiloint2double((int)((u & 0x80000000u) | ((u >> 3) & 0x0FFFE000u)), 0);
+}
+__device__ __forceinline__ double bf16hi_scaled(uint32_t w) {
+    return __hiloint2double((int)((w & 0x80000000u) | ((w >> 3) & 0x0FFFE000u)), 0);
+}
+__device__ __forceinline__ double f32_scaled(uint32_t w) {
+    return __hiloint2double((int)((w & 0x80000000u) | ((w >> 3) & 0x0FFFFFFFu)), (int)(w << 29));
+}
+
+// ---------------------------------------------------------------------------
+// CTA-wide top-k over keys[0..n): largest keys, ties -> lower position.
+// Writes the selected positions, ascending, to out_pos (smem or global via
+// functor).  k_sel = min(k, n) positions are produced.
+// ---------------------------------------------------------------------------
+template <typename Emit>
+__device__ void cta_topk(const uint64_t* keys, int n, int k_sel, int* hist, int* sw, Emit emit) {
+    const int tid = threadIdx.x;
+    uint64_t prefix = 0, mask = 0;
+    int rem = k_sel;
+    if (k_sel < n) {
+        for (int shift = 56; shift >= 0; shift -= 8) {
+            for (int i = tid; i < 256; i += kSelThreads) hist[i] = 0;
+            __syncthreads();
+            for (int i = tid; i < n; i += kSelThreads) {
+                uint64_t key = keys[i];
+                if ((key & mask) == prefix) atomicAdd(&hist[(int)((key >> shift) & 0xFF)], 1);
+            }
+            __syncthreads();
+            if (tid < 32) {
+                // lane l owns digits 255-8l .. 248-8l (descending)
+                int c[8], s = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    c[i] = hist[255 - (tid * 8 + i)];
+                    s += c[i];
+                }
+                int incl = warp_incl_scan(s);
+                int above = incl - s;
+                if (above < rem && rem <= incl) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        if (above < rem && rem <= above + c[i]) {
+                            sw[40] = 255 - (tid * 8 + i);
+                            sw[41] = rem - above;
+                            sw[42] = c[i];
+                        }
+                        above += c[i];
+                    }
+                }
+            }
+            __syncthreads();
+            int digit = sw[40];
+            rem = sw[41];
+            int cnt = sw[42];
+            __syncthreads();
+            prefix |= (uint64_t)digit << shift;
+            mask |= 0xFFull << shift;
+            if (cnt == rem) break;  // every key with this prefix is taken
+        }
+    } else {
+        mask = 0;
+        prefix = 0;
+        rem = n;  // all (every key matches the empty prefix)
+    }
+    // Compaction in position order.  Thread t owns positions [t*per, (t+1)*per).
+    const int per = (n + kSelThreads - 1) / kSelThreads;
+    const int p0 = tid * per, p1 = min(n, p0 + per);
+    int eq = 0;
+    for (int p = p0; p < p1; ++p) eq += ((keys[p] & mask) == prefix);
+    int tot;
+    int eq_base = block_excl_scan<kSelThreads>(eq, sw, tot);
+    int nsel = 0;
+    {
+        int er = eq_base;
+        for (int p = p0; p < p1; ++p) {
+            uint64_t km = keys[p] & mask;
+            bool s = km > prefix || (km == prefix && er < rem);
+            er += (km == prefix);
+            nsel += s;
+        }
+    }
+    int out_base = block_excl_scan<kSelThreads>(nsel, sw, tot);
+    {
+        int er = eq_base, o = out_base;
+        for (int p = p0; p < p1; ++p) {
+            uint64_t km = keys[p] & mask;
+            bool s = km > prefix || (km == prefix && er < rem);
+            er += (km == prefix);
+            if (s) emit(o++, p);
+        }
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+template <bool BF16, int G>
+__global__ void __launch_bounds__(kSelThreads, 2)
+block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
+                    const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
+                    int nchunks, int32_t* __restrict__ sel, double* __restrict__ scores,
+                    uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_j,
+                    int32_t* __restrict__ tickets) {
+    constexpr int ES = BF16 ? 2 : 4;
+    constexpr int CPC = 16 / ES;               // channels per 16-byte chunk
+    constexpr int NCH = kHeadDim / CPC;        // chunks per row (16 bf16, 32 f32)
+    constexpr int TILE_ELEMS = 64 * kHeadDim;  // 32 blocks * 2 * d
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* qpn = (double2*)smem_raw;                                  // [128*G]
+    uint64_t* keys = (uint64_t*)(smem_raw + kHeadDim * G * 16);         // [nkeys]
+    const int nkeys_cap = max(kSelChunk, min(nchunks * k, kSelMaxMerge));
+    int32_t* jpos = (int32_t*)(keys + nkeys_cap);                       // [nkeys]
+    int* hist = (int*)(jpos + nkeys_cap);                               // [256]
+    int* sw = hist + 256;                                               // [64]
+
+    const int pair = blockIdx.y;
+    const int b = pair / Hkv, h = pair % Hkv;
+    const int chunk = blockIdx.x;
+    const int nb = n_blk_arr[b];
+    const int nch_b = max(1, (nb + kSelChunk - 1) / kSelChunk);
+    if (chunk >= nch_b) return;
+    const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+
+    // q for the G query heads of this KV head, as (q+, q-) * 2^896.
+    for (int i = tid; i < kHeadDim * G; i += kSelThreads) {
+        int g = i % G, c = i / G;
+        size_t qi = ((size_t)b * Hq + (size_t)h * G + g) * kHeadDim + c;
+        double qd;
+        if (BF16)
+            qd = (double)__uint_as_float(((uint32_t)((const uint16_t*)q)[qi]) << 16);
+        else
+            qd = (double)((const float*)q)[qi];
+        qd = qd * 0x1p896;  // exact power-of-two scaling
+        qpn[i] = make_double2(qd > 0.0 ? qd : 0.0, qd < 0.0 ? qd : 0.0);
+    }
+    __syncthreads();
+
+    const int j0 = chunk * kSelChunk;
+    const int nb_chunk = min(kSelChunk, nb - j0);  // >= 0 (0 only if nb == 0)
+    const int ntiles = (nb_chunk + 31) / 32;
+    const char* meta_pair = (const char*)meta + ((size_t)pair * (max_blk / 32)) * TILE_ELEMS * ES;
+
+    for (int tl = warp; tl < ntiles; tl += kSelWarps) {
+        const int tile = j0 / 32 + tl;
+        const char* tb = meta_pair + (size_t)tile * TILE_ELEMS * ES + lane * 16;
+        double acc[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[g] = 0.0;
+        // chunk s: min row at ((s*2+0)*32 + lane)*16 bytes, max at ((s*2+1)*32 + lane)*16
+        constexpr int U = 4;
+        uint4 mn[U], mx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            mn[u] = ldg_stream(tb + (size_t)((u * 2 + 0) * 32) * 16);
+            mx[u] = ldg_stream(tb + (size_t)((u * 2 + 1) * 32) * 16);
+        }
+#pragma unroll 1
+        for (int s0 = 0; s0 < NCH; s0 += U) {
+            uint4 cmn[U], cmx[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                cmn[u] = mn[u];
+                cmx[u] = mx[u];
+            }
+            if (s0 + U < NCH) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    mn[u] = ldg_stream(tb + (size_t)(((s0 + U + u) * 2 + 0) * 32) * 16);
+                    mx[u] = ldg_stream(tb + (size_t)(((s0 + U + u) * 2 + 1) * 32) * 16);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t wn[4] = {cmn[u].x, cmn[u].y, cmn[u].z, cmn[u].w};
+                const uint32_t wx[4] = {cmx[u].x, cmx[u].y, cmx[u].z, cmx[u].w};
+#pragma unroll
+                for (int e = 0; e < CPC; ++e) {
+                    double dmin, dmax;
+                    if (BF16) {
+                        dmin = (e & 1) ? bf16hi_scaled(wn[e >> 1]) : bf16lo_scaled(wn[e >> 1]);
+                        dmax = (e & 1) ? bf16hi_scaled(wx[e >> 1]) : bf16lo_scaled(wx[e >> 1]);
+                    } else {
+                        dmin = f32_scaled(wn[e]);
+                        dmax = f32_scaled(wx[e]);
+                    }
+                    const int c = (s0 + u) * CPC + e;
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        double2 qq = qpn[c * G + g];
+                        acc[g] = __fma_rn(qq.x, dmax, acc[g]);
+                        acc[g] = __fma_rn(qq.y, dmin, acc[g]);
+                    }
+                }
+            }
+        }
+        double s = acc[0];
+#pragma unroll
+        for (int g = 1; g < G; ++g) s = acc[g] > s ? acc[g] : s;
+        s = s + 0.0;
+        const int pos = tl * 32 + lane;
+        const int j = j0 + pos;
+        keys[pos] = ord_key(s);
+        if (scores != nullptr && j < nb) scores[(size_t)pair * max_blk + j] = s;
+    }
+    __syncthreads();
+
+    const int kc = min(k, nb_chunk);
+    int32_t* sel_pair = sel + (size_t)pair * k;
+    if (nch_b == 1) {
+        cta_topk(keys, nb_chunk, kc, hist, sw, [&](int o, int p) { sel_pair[o] = j0 + p; });
+        for (int r = kc + tid; r < k; r += kSelThreads) sel_pair[r] = -1;
+        return;
+    }
+    // Multi-chunk: emit candidates, then the last CTA of the pair merges.
+    uint64_t* ck = cand_key + ((size_t)pair * nchunks + chunk) * k;
+    int32_t* cj = cand_j + ((size_t)pair * nchunks + chunk) * k;
+    cta_topk(keys, nb_chunk, kc, hist, sw, [&](int o, int p) {
+        ck[o] = keys[p];
+        cj[o] = j0 + p;
+    });
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sw[48] = atomicAdd(&tickets[pair], 1);
+    __syncthreads();
+    if (sw[48] != nch_b - 1) return;
+    __threadfence();
+    // Merge: candidates of chunk c are ascending in j and chunks are ordered,
+    // so position order == j order and the tie rule carries over.
+    int n = 0;
+    for (int c = 0; c < nch_b; ++c) {
+        int sz = min(kSelChunk, nb - c * kSelChunk);
+        int kcc = min(k, sz);
+        const uint64_t* sk = cand_key + ((size_t)pair * nchunks + c) * k;
+        const int32_t* sj = cand_j + ((size_t)pair * nchunks + c) * k;
+        for (int i = tid; i < kcc; i += kSelThreads) {
+            keys[n + i] = __ldcg(sk + i);
+            jpos[n + i] = __ldcg(sj + i);
+        }
+        n += kcc;
+    }
+    __syncthreads();
+    const int kf = min(k, nb);
+    cta_topk(keys, n, kf, hist, sw, [&](int o, int p) { sel_pair[o] = jpos[p]; });
+    for (int r = kf + tid; r < k; r += kSelThreads) sel_pair[r] = -1;
+    if (tid == 0) tickets[pair] = 0;
+}
+
+size_t select_ws_bytes(const ss_dims& d, int max_blk, int k) {
+    int nchunks = (max_blk + kSelChunk - 1) / kSelChunk;
+    size_t pairs = (size_t)d.batch * d.num_kv_heads;
+    size_t nc = (size_t)pairs * nchunks * k;
+    size_t bytes = nc * 8 + nc * 4 + pairs * 4;
+    return (bytes + 255) & ~(size_t)255;
+}
+
+template <bool BF16, int G>
+static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_blk, int max_blk,
+                              int k, const ss_dims& d, int32_t* sel, double* scores, void* ws,
+                              cudaStream_t stream) {
+    int nchunks = (max_blk + kSelChunk - 1) / kSelChunk;
+    size_t pairs = (size_t)d.batch * d.num_kv_heads;
+    size_t nc = pairs * nchunks * k;
+    uint64_t* cand_key = (uint64_t*)ws;
+    int32_t* cand_j = (int32_t*)((char*)ws + nc * 8);
+    int32_t* tickets = (int32_t*)((char*)ws + nc * 12);
+    int nkeys = max(kSelChunk, min(nchunks * k, kSelMaxMerge));
+    size_t smem = SelSmemLayout::bytes(G, nkeys);
+    auto kern = block_select_kernel<BF16, G>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return SS_ERR_CUDA;
+    dim3 grid(nchunks, (unsigned)pairs);
+    kern<<<grid, kSelThreads, smem, stream>>>(q, meta, n_blk, max_blk, k, d.num_q_heads,
+                                              d.num_kv_heads, nchunks, sel, scores, cand_key,
+                                              cand_j, tickets);
+    SS_LAUNCH_CHECK();
+    return SS_OK;
+}
+
+ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_blk, int max_blk,
+                              int k, const ss_dims& d, ss_dtype dt, int32_t* sel, double* scores,
+                              void* ws, cudaStream_t stream) {
+    int nchunks = (max_blk + kSelChunk - 1) / kSelChunk;
+    if ((size_t)nchunks * k > kSelMaxMerge && nchunks > 1) return SS_ERR_UNSUPPORTED;
+    int G = d.num_q_heads / d.num_kv_heads;
+#define SS_SEL_CASE(GG)                                                                   \
+    case GG:                                                                              \
+        return dt == SS_BF16                                                              \
+                   ? launch_sel_t<true, GG>(q, meta, n_blk, max_blk, k, d, sel, scores, ws, \
+                                            stream)                                       \
+                   : launch_sel_t<false, GG>(q, meta, n_blk, max_blk, k, d, sel, scores, ws, \
+                                             stream);
+    switch (G) {
+        SS_SEL_CASE(1)
+        SS_SEL_CASE(2)
+        SS_SEL_CASE(4)
+        SS_SEL_CASE(8)
+        default:
+            return SS_ERR_UNSUPPORTED;
+    }
+#undef SS_SEL_CASE
+}
+
+}  // namespace ss

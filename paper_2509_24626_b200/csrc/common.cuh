@@ -1,0 +1,85 @@
+// common.cuh -- small device helpers shared by the sm_100a kernels of
+// libsparseserve.so.  No method arithmetic lives here.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sparseserve.h"
+
+namespace ss {
+
+constexpr int kBlockTokens = 32;
+constexpr int kHeadDim = 128;
+constexpr int kNumSMs = 148;  // B200
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+
+// 16-byte streaming load, no L1 allocation (read-once data).
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Inclusive warp scan (int).
+__device__ __forceinline__ int warp_incl_scan(int v) {
+    int lane = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan for NT threads (NT multiple of 32, <= 1024).
+// `sw` must hold >= 33 ints of shared memory.  Returns exclusive prefix and
+// writes the block total to `total`.  Contains __syncthreads().
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int* sw, int& total) {
+    constexpr int NWARP = NT / 32;
+    int lane = lane_id(), w = warp_id();
+    int incl = warp_incl_scan(v);
+    if (lane == 31) sw[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int x = lane < NWARP ? sw[lane] : 0;
+        int xi = warp_incl_scan(x);
+        if (lane < NWARP) sw[lane] = xi - x;
+        if (lane == NWARP - 1) sw[32] = xi;
+    }
+    __syncthreads();
+    int res = sw[w] + incl - v;
+    total = sw[32];
+    __syncthreads();
+    return res;
+}
+
+template <int NT>
+__device__ __forceinline__ int block_sum(int v, int* sw) {
+    int total;
+    (void)block_excl_scan<NT>(v, sw, total);
+    return total;
+}
+
+}  // namespace ss
+
+#define SS_LAUNCH_CHECK()                                  \
+    do {                                                   \
+        if (cudaPeekAtLastError() != cudaSuccess) return SS_ERR_CUDA; \
+    } while (0)

@@ -1,0 +1,416 @@
+// sparse_attn.cu -- S5 sparse decode attention (§2.1:
+// S = QK^T/sqrt(d), P = softmax(S), O = PV; PAPER.md:33 / :124: computed only
+// over the KV blocks selected for the query token).  Readings R7 (tail block
+// always attended), R9 (softmax renormalised over selected tokens + tail), R10
+// (float32 output) in DESIGN.md; reference: oracle/oracle.c or_attention.
+//
+// B200 design: a persistent, stream-K split over "units".  A unit is one
+// selected head-block (16 KiB K+V in bf16, contiguous in its HBM cache slot,
+// PAPER.md:137 (H,N,D) layout) or the tail block of a (b, h) pair; a pair has
+// Ku = k + 1 units (slot -1 / empty tail units are skipped).  The U = pairs*Ku
+// units are cut into W equal contiguous ranges, one per warp (W = 148 SMs x NW
+// warps), so every warp streams the same number of bytes whatever the per-pair
+// split.  Each warp double-buffers whole blocks into its own shared memory with
+// 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx; SASS UBLKCP), so
+// HBM reads are 16 KiB transactions issued by one lane while the warp computes
+// on the previous block.  Pairs covered entirely by one warp are finalised in
+// place; a pair cut by range boundaries leaves <= 1 partial (m, l, o) per
+// contributing warp in the workspace and the last contributor (atomic ticket,
+// self-resetting) merges them in warp order -- deterministic.
+//
+// Per block, lane t computes token t's logits for the G query heads of the KV
+// head (K row read with a lane-rotated chunk order: conflict-free 16-byte
+// shared loads), an online softmax in exp2 domain, and lane l accumulates
+// output dims 4l..4l+3 from the V rows.  float32 CUDA-core math: at 1 (MHA) to
+// 4 (GQA G=4) flop per HBM byte the kernel is far below the tensor-core ridge
+// and fp32 keeps the 2e-3 / 1e-5 tolerances with margin.
+//
+// Roofline: HBM-bound; algorithmic bytes = block_bytes per attended unit
+// (+ q, out: negligible).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace ss {
+
+constexpr int kAttnPartStride = 132;  // floats per (warp, seg, g) partial: m, l, pad, pad, o[128]
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    }
+}
+
+struct AttnArgs {
+    const void* q;
+    const void* pool;
+    const int32_t* slot;
+    const void* tail;
+    const int32_t* tail_len;
+    const int32_t* counts;
+    float* out;
+    float* part;
+    int32_t* tickets;
+    int k, B, Hq, Hkv;
+    float scale_log2;
+    int64_t U;  // pairs * (k + 1)
+    int W;      // total warps
+};
+
+template <bool BF16>
+struct AttnTraits {
+    static constexpr int ES = BF16 ? 2 : 4;
+    static constexpr int BLOCK_ELEMS = 2 * kBlockTokens * kHeadDim;
+    static constexpr int BLOCK_BYTES = BLOCK_ELEMS * ES;
+    static constexpr int CPC = 16 / ES;             // elements per 16-byte chunk
+    static constexpr int NCH = kHeadDim / CPC;      // chunks per K row
+    static constexpr int NW = BF16 ? 6 : 3;         // warps per CTA (smem-limited)
+};
+
+template <bool BF16, int G>
+struct WarpSmem {
+    using T = AttnTraits<BF16>;
+    alignas(128) unsigned char buf[2][T::BLOCK_BYTES];
+    alignas(16) float4 q4[G][kHeadDim / 4];  // q (fp32) in 16-byte chunks, chunk order below
+    uint64_t bar[2];
+};
+
+__device__ __forceinline__ int64_t warp_of_unit(int64_t x, int64_t U, int W) {
+    return ((x + 1) * (int64_t)W - 1) / U;
+}
+
+template <bool BF16, int G>
+__global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kernel(AttnArgs a) {
+    using T = AttnTraits<BF16>;
+    if (a.counts != nullptr && a.counts[3] != 0) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    WarpSmem<BF16, G>& sm = reinterpret_cast<WarpSmem<BF16, G>*>(smem_raw)[warp_id()];
+    const int lane = lane_id();
+    const int w = blockIdx.x * T::NW + warp_id();
+    if (w >= a.W) return;  // W = min(total warps, U): every active warp owns >= 1 unit
+    const int64_t u0 = a.U * w / a.W, u1 = a.U * (w + 1) / a.W;
+    const int Ku = a.k + 1;
+
+    if (lane == 0) {
+        mbar_init(&sm.bar[0], 1);
+        mbar_init(&sm.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    // ---- producer: next valid unit -> stage (lane 0 issues the bulk copy) ----
+    int64_t next_u = u0;
+    int64_t bu[2];
+    auto issue = [&](int stage) {
+        const char* src = nullptr;
+        while (next_u < u1) {
+            int64_t p = next_u / Ku;
+            int r = (int)(next_u % Ku);
+            if (r < a.k) {
+                int32_t s = a.slot[p * a.k + r];
+                if (s >= 0) {
+                    src = (const char*)a.pool + (int64_t)s * T::BLOCK_BYTES;
+                    break;
+                }
+            } else if (a.tail_len[p / a.Hkv] > 0) {
+                src = (const char*)a.tail + p * (int64_t)T::BLOCK_BYTES;
+                break;
+            }
+            ++next_u;
+        }
+        if (next_u < u1) {
+            if (lane == 0) {
+                // order this warp's earlier generic-proxy reads of the buffer
+                // before the async-proxy (TMA) write that refills it
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&sm.bar[stage], T::BLOCK_BYTES);
+                bulk_g2s(sm.buf[stage], src, T::BLOCK_BYTES, &sm.bar[stage]);
+            }
+            bu[stage] = next_u++;
+        } else {
+            bu[stage] = -1;
+        }
+    };
+    issue(0);
+    issue(1);
+    uint32_t phase[2] = {0u, 0u};
+    int stage = 0;
+
+    const int64_t p_first = u0 / Ku, p_last = (u1 - 1) / Ku;
+    for (int64_t p = p_first; p <= p_last; ++p) {
+        const int b = (int)(p / a.Hkv), h = (int)(p % a.Hkv);
+        // q of the G heads of this KV head -> smem (fp32)
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int64_t qi = ((int64_t)b * a.Hq + (int64_t)h * G + g) * kHeadDim + 4 * lane;
+            float4 v;
+            if (BF16) {
+                uint2 raw = *reinterpret_cast<const uint2*>((const uint16_t*)a.q + qi);
+                v = make_float4(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u),
+                                __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xFFFF0000u));
+                // element c = 4*lane + i: chunk c/8 = lane/2, half (c%8)/4 = lane&1
+                sm.q4[g][(lane >> 1) + 16 * (lane & 1)] = v;
+            } else {
+                v = *reinterpret_cast<const float4*>((const float*)a.q + qi);
+                sm.q4[g][lane] = v;
+            }
+        }
+        __syncwarp();
+        float m[G], l[G], o[G][4];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            m[g] = -INFINITY;
+            l[g] = 0.f;
+            o[g][0] = o[g][1] = o[g][2] = o[g][3] = 0.f;
+        }
+        const int tl = a.tail_len[b];
+
+        while (bu[stage] >= 0 && bu[stage] / Ku == p) {
+            const bool is_tail = (bu[stage] % Ku) == a.k;
+            mbar_wait(&sm.bar[stage], phase[stage]);
+            phase[stage] ^= 1u;
+            const unsigned char* kb = sm.buf[stage];
+            const unsigned char* vb = kb + kBlockTokens * kHeadDim * T::ES;
+            // ---- logits: lane = token ----
+            float s0[G], s1[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) s0[g] = s1[g] = 0.f;
+            const unsigned char* krow = kb + lane * kHeadDim * T::ES;
+#pragma unroll 4
+            for (int c = 0; c < T::NCH; ++c) {
+                const int cc = (c + lane) & (T::NCH - 1);
+                uint4 kv = *reinterpret_cast<const uint4*>(krow + cc * 16);
+                if (BF16) {
+                    float k0 = __uint_as_float(kv.x << 16), k1 = __uint_as_float(kv.x & 0xFFFF0000u);
+                    float k2 = __uint_as_float(kv.y << 16), k3 = __uint_as_float(kv.y & 0xFFFF0000u);
+                    float k4 = __uint_as_float(kv.z << 16), k5 = __uint_as_float(kv.z & 0xFFFF0000u);
+                    float k6 = __uint_as_float(kv.w << 16), k7 = __uint_as_float(kv.w & 0xFFFF0000u);
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        float4 qa = sm.q4[g][cc], qb = sm.q4[g][cc + 16];
+                        s0[g] = fmaf(qa.x, k0, s0[g]);
+                        s1[g] = fmaf(qa.y, k1, s1[g]);
+                        s0[g] = fmaf(qa.z, k2, s0[g]);
+                        s1[g] = fmaf(qa.w, k3, s1[g]);
+                        s0[g] = fmaf(qb.x, k4, s0[g]);
+                        s1[g] = fmaf(qb.y, k5, s1[g]);
+                        s0[g] = fmaf(qb.z, k6, s0[g]);
+                        s1[g] = fmaf(qb.w, k7, s1[g]);
+                    }
+                } else {
+                    float k0 = __uint_as_float(kv.x), k1 = __uint_as_float(kv.y);
+                    float k2 = __uint_as_float(kv.z), k3 = __uint_as_float(kv.w);
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        float4 qa = sm.q4[g][cc];
+                        s0[g] = fmaf(qa.x, k0, s0[g]);
+                        s1[g] = fmaf(qa.y, k1, s1[g]);
+                        s0[g] = fmaf(qa.z, k2, s0[g]);
+                        s1[g] = fmaf(qa.w, k3, s1[g]);
+                    }
+                }
+            }
+            const bool valid = !is_tail || lane < tl;
+            float pz[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                float z = valid ? (s0[g] + s1[g]) * a.scale_log2 : -INFINITY;
+                float mx = warp_max(z);
+                float mnew = fmaxf(m[g], mx);
+                float corr = exp2f(m[g] - mnew);
+                float pp = exp2f(z - mnew);
+                l[g] = l[g] * corr + warp_sum(pp);
+                o[g][0] *= corr;
+                o[g][1] *= corr;
+                o[g][2] *= corr;
+                o[g][3] *= corr;
+                m[g] = mnew;
+                pz[g] = pp;
+            }
+            // ---- O += P V: lane owns dims 4*lane .. 4*lane+3 ----
+            const int nt = is_tail ? tl : kBlockTokens;
+#pragma unroll 4
+            for (int t = 0; t < nt; ++t) {
+                float v0, v1, v2, v3;
+                if (BF16) {
+                    uint2 vv = *reinterpret_cast<const uint2*>(vb + (t * kHeadDim + 4 * lane) * 2);
+                    v0 = __uint_as_float(vv.x << 16);
+                    v1 = __uint_as_float(vv.x & 0xFFFF0000u);
+                    v2 = __uint_as_float(vv.y << 16);
+                    v3 = __uint_as_float(vv.y & 0xFFFF0000u);
+                } else {
+                    float4 vv = *reinterpret_cast<const float4*>(vb + (t * kHeadDim + 4 * lane) * 4);
+                    v0 = vv.x;
+                    v1 = vv.y;
+                    v2 = vv.z;
+                    v3 = vv.w;
+                }
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    float pt = __shfl_sync(0xffffffffu, pz[g], t);
+                    o[g][0] = fmaf(pt, v0, o[g][0]);
+                    o[g][1] = fmaf(pt, v1, o[g][1]);
+                    o[g][2] = fmaf(pt, v2, o[g][2]);
+                    o[g][3] = fmaf(pt, v3, o[g][3]);
+                }
+            }
+            __syncwarp();
+            issue(stage);  // refill the buffer just consumed
+            stage ^= 1;
+        }
+
+        // ---- flush pair p ----
+        const bool full = (p * Ku >= u0) && ((p + 1) * Ku <= u1);
+        if (full) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                float inv = l[g] > 0.f ? 1.f / l[g] : 0.f;
+                float4 r = make_float4(o[g][0] * inv, o[g][1] * inv, o[g][2] * inv, o[g][3] * inv);
+                const int hq = h * G + g;
+                *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) = r;
+            }
+            continue;
+        }
+        const int seg = (p == p_first) ? 0 : 1;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float* pp = a.part + (((int64_t)w * 2 + seg) * G + g) * kAttnPartStride;
+            if (lane == 0) {
+                pp[0] = m[g];
+                pp[1] = l[g];
+            }
+            *reinterpret_cast<float4*>(pp + 4 + 4 * lane) =
+                make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+        }
+        __threadfence();
+        __syncwarp();
+        int ticket = 0;
+        if (lane == 0) ticket = atomicAdd(&a.tickets[p], 1);
+        ticket = __shfl_sync(0xffffffffu, ticket, 0);
+        const int64_t wf = warp_of_unit(p * Ku, a.U, a.W);
+        const int64_t wl = warp_of_unit((p + 1) * Ku - 1, a.U, a.W);
+        if (ticket != (int)(wl - wf)) continue;
+        __threadfence();
+        for (int g = 0; g < G; ++g) {
+            float mt = -INFINITY;
+            for (int64_t w2 = wf; w2 <= wl; ++w2) {
+                const int s2 = ((a.U * w2 / a.W) / Ku == p) ? 0 : 1;
+                const float* pp = a.part + ((w2 * 2 + s2) * G + g) * kAttnPartStride;
+                mt = fmaxf(mt, __ldcg(pp));
+            }
+            float lt = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+            if (mt != -INFINITY) {
+                for (int64_t w2 = wf; w2 <= wl; ++w2) {
+                    const int s2 = ((a.U * w2 / a.W) / Ku == p) ? 0 : 1;
+                    const float* pp = a.part + ((w2 * 2 + s2) * G + g) * kAttnPartStride;
+                    float sc = exp2f(__ldcg(pp) - mt);
+                    lt += __ldcg(pp + 1) * sc;
+                    float4 ov = __ldcg(reinterpret_cast<const float4*>(pp + 4 + 4 * lane));
+                    o0 += ov.x * sc;
+                    o1 += ov.y * sc;
+                    o2 += ov.z * sc;
+                    o3 += ov.w * sc;
+                }
+            }
+            float inv = lt > 0.f ? 1.f / lt : 0.f;
+            const int hq = h * G + g;
+            *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) =
+                make_float4(o0 * inv, o1 * inv, o2 * inv, o3 * inv);
+        }
+        if (lane == 0) a.tickets[p] = 0;
+    }
+}
+
+template <bool BF16, int G>
+static size_t attn_smem_bytes() {
+    return sizeof(WarpSmem<BF16, G>) * AttnTraits<BF16>::NW;
+}
+
+static int attn_total_warps(ss_dtype dt) {
+    return kNumSMs * (dt == SS_BF16 ? AttnTraits<true>::NW : AttnTraits<false>::NW);
+}
+
+size_t attn_ws_bytes(const ss_dims& d, int k, ss_dtype dt) {
+    int G = d.num_q_heads / d.num_kv_heads;
+    size_t W = attn_total_warps(dt);
+    size_t part = W * 2 * G * kAttnPartStride * 4;
+    size_t pairs = (size_t)d.batch * d.num_kv_heads;
+    return ((part + pairs * 4) + 255) & ~(size_t)255;
+}
+
+template <bool BF16, int G>
+static ss_status launch_attn_t(AttnArgs a, cudaStream_t stream) {
+    auto kern = sparse_attn_kernel<BF16, G>;
+    size_t smem = attn_smem_bytes<BF16, G>();
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return SS_ERR_CUDA;
+    kern<<<kNumSMs, AttnTraits<BF16>::NW * 32, smem, stream>>>(a);
+    SS_LAUNCH_CHECK();
+    return SS_OK;
+}
+
+ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* slot, int k,
+                             const void* tail_kv, const int32_t* tail_len, const ss_dims& d,
+                             ss_dtype dt, float scale, const int32_t* counts, float* out, void* ws,
+                             cudaStream_t stream) {
+    AttnArgs a;
+    a.q = q;
+    a.pool = pool_kv;
+    a.slot = slot;
+    a.tail = tail_kv;
+    a.tail_len = tail_len;
+    a.counts = counts;
+    a.out = out;
+    a.k = k;
+    a.B = d.batch;
+    a.Hq = d.num_q_heads;
+    a.Hkv = d.num_kv_heads;
+    a.scale_log2 = scale * 1.4426950408889634f;
+    const int G = d.num_q_heads / d.num_kv_heads;
+    a.U = (int64_t)d.batch * d.num_kv_heads * (k + 1);
+    a.W = (int)std::min<int64_t>(attn_total_warps(dt), a.U);
+    size_t part = (size_t)a.W * 2 * G * kAttnPartStride * 4;
+    a.part = (float*)ws;
+    a.tickets = (int32_t*)((char*)ws + part);
+#define SS_ATTN_CASE(GG)                                                                    \
+    case GG:                                                                                \
+        return dt == SS_BF16 ? launch_attn_t<true, GG>(a, stream) : launch_attn_t<false, GG>(a, stream);
+    switch (G) {
+        SS_ATTN_CASE(1)
+        SS_ATTN_CASE(2)
+        SS_ATTN_CASE(4)
+        SS_ATTN_CASE(8)
+        default:
+            return SS_ERR_UNSUPPORTED;
+    }
+#undef SS_ATTN_CASE
+}
+
+}  // namespace ss

@@ -1,0 +1,146 @@
+"""Thin Python binding of the C ABI (same names as include/sparseserve.h).
+
+Argument marshalling only: torch tensors -> raw pointers + sizes + the current
+CUDA stream.  Every step of the hot path runs in the CUDA kernels of
+libsparseserve.so; nothing here computes.  Tensors must be contiguous and on
+the current CUDA device (host KV: pinned CPU tensor).
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from . import _lib
+from ._lib import SSCachePool, SSDims, check
+
+HEAD_DIM = 128
+BLOCK_TOKENS = 32
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _lib.SS_BF16
+    if t.dtype == torch.float32:
+        return _lib.SS_F32
+    raise TypeError(f"unsupported dtype {t.dtype} (bf16 or float32)")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def dims(batch: int, num_q_heads: int, num_kv_heads: int) -> SSDims:
+    return SSDims(batch, num_q_heads, num_kv_heads, HEAD_DIM, BLOCK_TOKENS)
+
+
+def workspace_size(which: int, d: SSDims, max_blk: int, k: int, num_slots: int = 0) -> int:
+    return int(_lib.load().ss_workspace_size(which, d, max_blk, k, num_slots))
+
+
+def alloc_workspace(which: int, d: SSDims, max_blk: int, k: int, num_slots: int = 0,
+                    device=None) -> torch.Tensor:
+    n = workspace_size(which, d, max_blk, k, num_slots)
+    return torch.zeros(max(n, 256), dtype=torch.uint8, device=device or "cuda")
+
+
+def meta_numel(batch: int, num_kv_heads: int, max_blk: int) -> int:
+    """Elements of a (tiled) metadata array for [B][Hkv][max_blk] blocks."""
+    assert max_blk % 32 == 0
+    return batch * num_kv_heads * max_blk * 2 * HEAD_DIM
+
+
+# ---------------------------------------------------------------------------
+def block_meta_update(keys: torch.Tensor, meta: torch.Tensor, n: int, key_stride: int,
+                      dst_idx: Optional[torch.Tensor] = None, stream=None) -> None:
+    """S0: meta[dst_idx[i]] = {min, max} over the 32 keys at keys + i*key_stride."""
+    if dst_idx is not None:
+        assert dst_idx.dtype == torch.int64
+    check(_lib.load().block_meta_update(_ptr(keys), key_stride, _ptr(dst_idx), n, _ptr(meta),
+                                        _dt(keys), HEAD_DIM, _stream(stream)),
+          "block_meta_update")
+
+
+def ss_block_select(q: torch.Tensor, meta: torch.Tensor, n_blk: torch.Tensor, max_blk: int,
+                    k: int, d: SSDims, sel: torch.Tensor, ws: torch.Tensor,
+                    scores: Optional[torch.Tensor] = None, stream=None) -> None:
+    """S1+S2: sel[b][h][:k] = ascending top-k block ids (-1 padded)."""
+    assert n_blk.dtype == torch.int32 and sel.dtype == torch.int32
+    if scores is not None:
+        assert scores.dtype == torch.float64
+    check(_lib.load().ss_block_select(_ptr(q), _ptr(meta), _ptr(n_blk), max_blk, k, d, _dt(q),
+                                      _ptr(sel), _ptr(scores), _ptr(ws), ws.numel(),
+                                      _stream(stream)), "ss_block_select")
+
+
+class CachePool:
+    """Device arrays of one (GPU, layer) HBM block-cache pool (S3 state)."""
+
+    def __init__(self, num_slots: int, fwd: torch.Tensor, device=None):
+        device = device or fwd.device
+        self.fwd = fwd                       # int32 [fwd_len], may be shared across layers
+        self.slot_key = torch.full((num_slots,), -1, dtype=torch.int64, device=device)
+        self.slot_stamp = torch.full((num_slots,), -1, dtype=torch.int64, device=device)
+        self.order = torch.arange(num_slots, dtype=torch.int32, device=device)
+        self.num_slots = num_slots
+
+    def c_struct(self) -> SSCachePool:
+        return SSCachePool(self.fwd.data_ptr(), self.fwd.numel(), self.slot_key.data_ptr(),
+                           self.slot_stamp.data_ptr(), self.order.data_ptr(), self.num_slots)
+
+
+def kv_cache_lookup_insert(pool: CachePool, sel: torch.Tensor, req_ids: torch.Tensor, layer: int,
+                           num_layers: int, max_blk: int, k: int, d: SSDims, stamp: int,
+                           slot_out: torch.Tensor, hit_out: torch.Tensor, miss_keys: torch.Tensor,
+                           miss_slots: torch.Tensor, counts: torch.Tensor, ws: torch.Tensor,
+                           stream=None) -> None:
+    """S3: batch-LRU lookup/insert; counts = {hits, misses, evictions, status} (device)."""
+    assert sel.dtype == torch.int32 and req_ids.dtype == torch.int32
+    assert hit_out.dtype == torch.uint8 and miss_keys.dtype == torch.int64
+    assert miss_slots.dtype == torch.int32 and counts.dtype == torch.int32
+    check(_lib.load().kv_cache_lookup_insert(pool.c_struct(), _ptr(sel), _ptr(req_ids), layer,
+                                             num_layers, max_blk, k, d, int(stamp),
+                                             _ptr(slot_out), _ptr(hit_out), _ptr(miss_keys),
+                                             _ptr(miss_slots), _ptr(counts), _ptr(ws), ws.numel(),
+                                             _stream(stream)), "kv_cache_lookup_insert")
+
+
+def host_device_pointer(host: torch.Tensor) -> int:
+    """Device address of a pinned host tensor."""
+    assert host.is_pinned(), "host KV must be pinned (page-locked) memory"
+    import ctypes
+    out = ctypes.c_void_p()
+    check(_lib.load().ss_host_device_pointer(host.data_ptr(), ctypes.byref(out)),
+          "ss_host_device_pointer")
+    return int(out.value)
+
+
+def flash_h2d_gather(host_kv_dev_ptr: int, host_blocks: int, miss_keys: torch.Tensor,
+                     miss_slots: torch.Tensor, counts: torch.Tensor, max_misses: int,
+                     pool_kv: torch.Tensor, block_bytes: int, stream=None) -> None:
+    """S4: pool_kv[miss_slots[i]] <- host_kv[miss_keys[i] % host_blocks], i < counts[1]."""
+    check(_lib.load().flash_h2d_gather(host_kv_dev_ptr, host_blocks, _ptr(miss_keys),
+                                       _ptr(miss_slots), _ptr(counts), max_misses,
+                                       _ptr(pool_kv), block_bytes, _stream(stream)),
+          "flash_h2d_gather")
+
+
+def sparse_decode_attn(q: torch.Tensor, pool_kv: torch.Tensor, slot: torch.Tensor, k: int,
+                       tail_kv: torch.Tensor, tail_len: torch.Tensor, d: SSDims, scale: float,
+                       out: torch.Tensor, ws: torch.Tensor, counts: Optional[torch.Tensor] = None,
+                       stream=None) -> None:
+    """S5: out[hq][b][:] = softmax(q K^T * scale) V over the selected blocks + tail."""
+    assert out.dtype == torch.float32 and slot.dtype == torch.int32
+    check(_lib.load().sparse_decode_attn(_ptr(q), _ptr(pool_kv), _ptr(slot), k, _ptr(tail_kv),
+                                         _ptr(tail_len), d, _dt(q), float(scale), _ptr(counts),
+                                         _ptr(out), _ptr(ws), ws.numel(), _stream(stream)),
+          "sparse_decode_attn")

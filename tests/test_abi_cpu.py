@@ -1,0 +1,83 @@
+"""CPU-only checks of the boundary: the C-ABI library builds for sm_100a, loads,
+and exports every function include/sparseserve.h declares; host-side argument
+validation returns the documented status without launching anything."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sparseserve.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(\w+)\s*\(", src, flags=re.M)
+    return sorted(set(n for n in names if n not in ("if", "while")))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2509_24626_b200 import build
+    build.build()
+    from paper_2509_24626_b200 import _lib
+    return _lib.load()
+
+
+def test_header_declares_the_hot_path_calls():
+    names = _declared()
+    for n in ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert",
+              "flash_h2d_gather", "sparse_decode_attn", "ss_workspace_size"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2509_24626_b200 import _lib
+    path = _lib.LIB_PATH
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    exported = set(line.split()[-1] for line in out.splitlines() if line.strip())
+    for n in _declared():
+        assert n in exported, n
+        assert hasattr(lib, n)
+    assert set(_lib.EXPORTS) <= exported
+
+
+def test_library_is_sm100a_sass(lib):
+    from paper_2509_24626_b200 import _lib
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UBLKCP" in sass          # TMA bulk copies in the attention kernel
+    assert "DFMA" in sass            # fp64 block scoring
+
+
+def test_host_validation_without_gpu(lib):
+    from paper_2509_24626_b200._lib import SSDims, SS_ERR_INVALID_ARG, SS_ERR_UNSUPPORTED, SS_OK
+    d = SSDims(1, 32, 32, 128, 32)
+    # null pointers -> invalid, nothing launched
+    assert lib.ss_block_select(None, None, None, 256, 64, d, 0, None, None, None, 0, None) == SS_ERR_INVALID_ARG
+    bad = SSDims(1, 32, 32, 64, 32)
+    assert lib.ss_block_select(16, 16, 16, 256, 64, bad, 0, 16, None, 16, 1 << 30, None) == SS_ERR_UNSUPPORTED
+    gqa3 = SSDims(1, 24, 8, 128, 32)
+    assert lib.ss_block_select(16, 16, 16, 256, 64, gqa3, 0, 16, None, 16, 1 << 30, None) == SS_ERR_UNSUPPORTED
+    assert lib.ss_block_select(16, 16, 16, 250, 64, d, 0, 16, None, 16, 1 << 30, None) == SS_ERR_INVALID_ARG
+    assert lib.ss_block_select(16, 16, 16, 256, 0, d, 0, 16, None, 16, 1 << 30, None) == SS_ERR_INVALID_ARG
+    assert lib.block_meta_update(None, 8192, None, 0, None, 0, 128, None) == SS_OK     # n == 0 no-op
+    assert lib.flash_h2d_gather(16, 0, 16, 16, 16, 1, 16, 16384, None) == SS_ERR_INVALID_ARG
+    assert lib.flash_h2d_gather(16, 4, 16, 16, 16, 1, 16, 100, None) == SS_ERR_INVALID_ARG
+    assert lib.sparse_decode_attn(16, 16, 16, 64, 16, 16, d, 0, 0.1, None, 16, 16, 1, None) == SS_ERR_INVALID_ARG
+    assert lib.ss_status_string(3) == b"SS_ERR_CAPACITY"
+    assert lib.ss_workspace_size(0, d, 4096, 64, 0) > 0
+    assert lib.ss_workspace_size(1, d, 4096, 64, 1 << 17) > (1 << 17)
+    assert lib.ss_workspace_size(7, d, 4096, 64, 0) == 0
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    from paper_2509_24626_b200 import _lib
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "nope.so"))
+    with pytest.raises(ImportError):
+        _lib.load()
