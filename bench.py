@@ -201,6 +201,7 @@ class StepTimers:
 
 def run_step(eng, q_step, stamp, timers=None, pg=None, world=1, gathered=None):
     from paper_2509_24626_b200 import ops
+    from paper_2509_24626_b200.shard import gather_outputs
     c = eng.cfg
     for l in range(c.layers):
         q = q_step[l]
@@ -224,8 +225,7 @@ def run_step(eng, q_step, stamp, timers=None, pg=None, world=1, gathered=None):
                                                      eng.tail_kv[l], eng.tail_len, eng.dims, eng.scale,
                                                      eng.out[l], eng.ws_attn, counts=eng.counts[l]))
         if world > 1:
-            timed("allgather", lambda: torch.distributed.all_gather_into_tensor(
-                gathered[l], eng.out[l], group=pg))
+            timed("allgather", lambda: gather_outputs(eng.out[l], gathered[l], group=pg))
 
 
 def measure_h2d_peak(nbytes=1 << 30):
@@ -286,7 +286,8 @@ def bench_ours(args):
     eng, W = setup_engine(args, rank, world)
     c = eng.cfg
     steps_total = args.warmup + args.steps
-    qs = gen_queries(eng, steps_total + 1, W["rho"], seed=5000 + rank)
+    e2e_steps = max(3, args.steps // 2)
+    qs = gen_queries(eng, steps_total + e2e_steps, W["rho"], seed=5000 + rank)
     gathered = None
     if world > 1:
         gathered = torch.empty(c.layers, c.num_q_heads * world, c.batch, 128, dtype=torch.float32,
@@ -382,16 +383,16 @@ def bench_ours(args):
                 "peak_source": peak_src if dk["bound"] == "hbm" else "bulk pinned cudaMemcpy H2D, measured in this run"}
 
     # ---- e2e through the public API with host buffers ----
-    q_host = torch.empty_like(qs[0], device="cpu").pin_memory()
-    out_host = torch.empty(eng.out.shape, dtype=torch.float32, pin_memory=True)
+    # fresh drifting queries per step (continuing the same q process), staged in
+    # pinned host memory; each step copies its own q in and its outputs out.
+    q_host = qs[steps_total:steps_total + e2e_steps].cpu().pin_memory()
+    out_host = torch.empty((gathered if world > 1 else eng.out).shape, dtype=torch.float32, pin_memory=True)
     q_dev = torch.empty_like(qs[0])
-    q_host.copy_(qs[steps_total])
     barrier()
     e_s, e_e = torch.cuda.Event(True), torch.cuda.Event(True)
-    e2e_steps = max(3, args.steps // 2)
     e_s.record()
     for i in range(e2e_steps):
-        q_dev.copy_(q_host, non_blocking=True)
+        q_dev.copy_(q_host[i], non_blocking=True)
         run_step(eng, q_dev, stamp=steps_total + 1 + i, pg=pg, world=world, gathered=gathered)
         out_host.copy_(gathered if world > 1 else eng.out, non_blocking=True)
     e_e.record()

@@ -30,13 +30,16 @@
 //
 // Roofline: HBM-bound on the metadata stream: 512 B per block per (b, h) in
 // bf16 (1 KiB f32); fp64 work = 2*G*128 DFMA per block.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace ss {
 
 constexpr int kSelThreads = 256;
 constexpr int kSelWarps = kSelThreads / 32;
-constexpr int kSelChunk = 2048;  // blocks per CTA
+constexpr int kSelChunkMax = 2048;  // blocks per CTA (upper bound; smem sizing)
+constexpr int kSelChunkDefault = 1024;  // measured best at C2 (tools/kbench.py)
 constexpr int kSelMaxMerge = 8192;
 
 struct SelSmemLayout {
@@ -153,7 +156,7 @@ template <bool BF16, int G>
 __global__ void __launch_bounds__(kSelThreads, 2)
 block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                     const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
-                    int nchunks, int32_t* __restrict__ sel, double* __restrict__ scores,
+                    int nchunks, int CH, int32_t* __restrict__ sel, double* __restrict__ scores,
                     uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_j,
                     int32_t* __restrict__ tickets) {
     constexpr int ES = BF16 ? 2 : 4;
@@ -163,20 +166,43 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* qpn = (double2*)smem_raw;                                  // [128*G]
     uint64_t* keys = (uint64_t*)(smem_raw + kHeadDim * G * 16);         // [nkeys]
-    const int nkeys_cap = max(kSelChunk, min(nchunks * k, kSelMaxMerge));
+    const int nkeys_cap = max(CH, min(nchunks * k, kSelMaxMerge));
     int32_t* jpos = (int32_t*)(keys + nkeys_cap);                       // [nkeys]
     int* hist = (int*)(jpos + nkeys_cap);                               // [256]
     int* sw = hist + 256;                                               // [64]
 
     const int pair = blockIdx.y;
     const int b = pair / Hkv, h = pair % Hkv;
-    const int chunk = blockIdx.x;
+    const int ci = blockIdx.x;  // chunk index
     const int nb = n_blk_arr[b];
-    const int nch_b = max(1, (nb + kSelChunk - 1) / kSelChunk);
-    if (chunk >= nch_b) return;
+    const int nch_b = max(1, (nb + CH - 1) / CH);
+    if (ci >= nch_b) return;
     const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
 
-    // q for the G query heads of this KV head, as (q+, q-) * 2^896.
+    // G == 1 (MHA): q as float64 plus per-channel select masks (q >= 0 -> max
+    // row, else min row), so each channel costs one LOP3-select, one exact
+    // f32->f64 convert and ONE DFMA: acc + q*(q>=0 ? M : m) == acc + max(qM, qm).
+    double* qd1 = (double*)smem_raw;                        // [128]
+    uint32_t* qmask1 = (uint32_t*)(smem_raw + kHeadDim * 8); // [128] (bf16 uses 64)
+    if constexpr (G == 1) {
+        for (int c = tid; c < kHeadDim; c += kSelThreads) {
+            size_t qi = ((size_t)b * Hq + h) * kHeadDim + c;
+            double qv = BF16 ? (double)__uint_as_float(((uint32_t)((const uint16_t*)q)[qi]) << 16)
+                             : (double)((const float*)q)[qi];
+            qd1[c] = qv;
+        }
+        __syncthreads();
+        for (int i = tid; i < kHeadDim / (BF16 ? 2 : 1); i += kSelThreads) {
+            uint32_t m;
+            if (BF16)
+                m = (qd1[2 * i] >= 0.0 ? 0x0000FFFFu : 0u) | (qd1[2 * i + 1] >= 0.0 ? 0xFFFF0000u : 0u);
+            else
+                m = qd1[i] >= 0.0 ? 0xFFFFFFFFu : 0u;
+            qmask1[i] = m;
+        }
+    }
+    // G > 1: q for the G query heads of this KV head, as (q+, q-) * 2^896.
+    if constexpr (G > 1)
     for (int i = tid; i < kHeadDim * G; i += kSelThreads) {
         int g = i % G, c = i / G;
         size_t qi = ((size_t)b * Hq + (size_t)h * G + g) * kHeadDim + c;
@@ -190,11 +216,55 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     }
     __syncthreads();
 
-    const int j0 = chunk * kSelChunk;
-    const int nb_chunk = min(kSelChunk, nb - j0);  // >= 0 (0 only if nb == 0)
+    const int j0 = ci * CH;
+    const int nb_chunk = min(CH, nb - j0);  // >= 0 (0 only if nb == 0)
     const int ntiles = (nb_chunk + 31) / 32;
     const char* meta_pair = (const char*)meta + ((size_t)pair * (max_blk / 32)) * TILE_ELEMS * ES;
 
+    if constexpr (G == 1)
+    for (int tl = warp; tl < ntiles; tl += kSelWarps) {
+        const int tile = j0 / 32 + tl;
+        const char* tb = meta_pair + (size_t)tile * TILE_ELEMS * ES + lane * 16;
+        // fully unrolled over the NCH chunks, loads kept D chunks ahead
+        constexpr int D = 6, R = D + 1;
+        uint4 mn[R], mx[R];
+#pragma unroll
+        for (int s = 0; s < D; ++s) {
+            mn[s] = ldg_stream(tb + (size_t)((s * 2 + 0) * 32) * 16);
+            mx[s] = ldg_stream(tb + (size_t)((s * 2 + 1) * 32) * 16);
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < NCH; ++s) {
+            if (s + D < NCH) {
+                mn[(s + D) % R] = ldg_stream(tb + (size_t)(((s + D) * 2 + 0) * 32) * 16);
+                mx[(s + D) % R] = ldg_stream(tb + (size_t)(((s + D) * 2 + 1) * 32) * 16);
+            }
+            const uint4 wn = mn[s % R], wx = mx[s % R];
+            const uint4 mk = *reinterpret_cast<const uint4*>(qmask1 + s * (BF16 ? 4 : 4));
+            const uint32_t an[4] = {wn.x, wn.y, wn.z, wn.w};
+            const uint32_t ax[4] = {wx.x, wx.y, wx.z, wx.w};
+            const uint32_t am[4] = {mk.x, mk.y, mk.z, mk.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t y = (ax[i] & am[i]) | (an[i] & ~am[i]);
+                if (BF16) {
+                    const double2 qq = *reinterpret_cast<const double2*>(qd1 + s * 8 + 2 * i);
+                    acc = __fma_rn(qq.x, (double)__uint_as_float(y << 16), acc);
+                    acc = __fma_rn(qq.y, (double)__uint_as_float(y & 0xFFFF0000u), acc);
+                } else {
+                    acc = __fma_rn(qd1[s * 4 + i], (double)__uint_as_float(y), acc);
+                }
+            }
+        }
+        const double s = acc + 0.0;
+        const int pos = tl * 32 + lane;
+        const int j = j0 + pos;
+        keys[pos] = ord_key(s);
+        if (scores != nullptr && j < nb) scores[(size_t)pair * max_blk + j] = s;
+    }
+
+    if constexpr (G > 1)
     for (int tl = warp; tl < ntiles; tl += kSelWarps) {
         const int tile = j0 / 32 + tl;
         const char* tb = meta_pair + (size_t)tile * TILE_ELEMS * ES + lane * 16;
@@ -267,8 +337,8 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
         return;
     }
     // Multi-chunk: emit candidates, then the last CTA of the pair merges.
-    uint64_t* ck = cand_key + ((size_t)pair * nchunks + chunk) * k;
-    int32_t* cj = cand_j + ((size_t)pair * nchunks + chunk) * k;
+    uint64_t* ck = cand_key + ((size_t)pair * nchunks + ci) * k;
+    int32_t* cj = cand_j + ((size_t)pair * nchunks + ci) * k;
     cta_topk(keys, nb_chunk, kc, hist, sw, [&](int o, int p) {
         ck[o] = keys[p];
         cj[o] = j0 + p;
@@ -283,7 +353,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     // so position order == j order and the tie rule carries over.
     int n = 0;
     for (int c = 0; c < nch_b; ++c) {
-        int sz = min(kSelChunk, nb - c * kSelChunk);
+        int sz = min(CH, nb - c * CH);
         int kcc = min(k, sz);
         const uint64_t* sk = cand_key + ((size_t)pair * nchunks + c) * k;
         const int32_t* sj = cand_j + ((size_t)pair * nchunks + c) * k;
@@ -300,8 +370,20 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     if (tid == 0) tickets[pair] = 0;
 }
 
+// Blocks scored per CTA.  2048 by default; SS_SEL_CHUNK (multiple of 32, <= 2048)
+// overrides it for tuning.  Workspace sizing and launches use the same value.
+static int sel_chunk() {
+    static int c = [] {
+        const char* e = getenv("SS_SEL_CHUNK");
+        int v = e ? atoi(e) : kSelChunkDefault;
+        if (v < 32 || v > kSelChunkMax || (v % 32)) v = kSelChunkMax;
+        return v;
+    }();
+    return c;
+}
+
 size_t select_ws_bytes(const ss_dims& d, int max_blk, int k) {
-    int nchunks = (max_blk + kSelChunk - 1) / kSelChunk;
+    int nchunks = (max_blk + sel_chunk() - 1) / sel_chunk();
     size_t pairs = (size_t)d.batch * d.num_kv_heads;
     size_t nc = (size_t)pairs * nchunks * k;
     size_t bytes = nc * 8 + nc * 4 + pairs * 4;
@@ -312,13 +394,13 @@ template <bool BF16, int G>
 static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_blk, int max_blk,
                               int k, const ss_dims& d, int32_t* sel, double* scores, void* ws,
                               cudaStream_t stream) {
-    int nchunks = (max_blk + kSelChunk - 1) / kSelChunk;
+    int nchunks = (max_blk + sel_chunk() - 1) / sel_chunk();
     size_t pairs = (size_t)d.batch * d.num_kv_heads;
     size_t nc = pairs * nchunks * k;
     uint64_t* cand_key = (uint64_t*)ws;
     int32_t* cand_j = (int32_t*)((char*)ws + nc * 8);
     int32_t* tickets = (int32_t*)((char*)ws + nc * 12);
-    int nkeys = max(kSelChunk, min(nchunks * k, kSelMaxMerge));
+    int nkeys = max(sel_chunk(), min(nchunks * k, kSelMaxMerge));
     size_t smem = SelSmemLayout::bytes(G, nkeys);
     auto kern = block_select_kernel<BF16, G>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -326,7 +408,7 @@ static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_
         return SS_ERR_CUDA;
     dim3 grid(nchunks, (unsigned)pairs);
     kern<<<grid, kSelThreads, smem, stream>>>(q, meta, n_blk, max_blk, k, d.num_q_heads,
-                                              d.num_kv_heads, nchunks, sel, scores, cand_key,
+                                              d.num_kv_heads, nchunks, sel_chunk(), sel, scores, cand_key,
                                               cand_j, tickets);
     SS_LAUNCH_CHECK();
     return SS_OK;
@@ -335,7 +417,7 @@ static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_
 ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_blk, int max_blk,
                               int k, const ss_dims& d, ss_dtype dt, int32_t* sel, double* scores,
                               void* ws, cudaStream_t stream) {
-    int nchunks = (max_blk + kSelChunk - 1) / kSelChunk;
+    int nchunks = (max_blk + sel_chunk() - 1) / sel_chunk();
     if ((size_t)nchunks * k > kSelMaxMerge && nchunks > 1) return SS_ERR_UNSUPPORTED;
     int G = d.num_q_heads / d.num_kv_heads;
 #define SS_SEL_CASE(GG)                                                                   \

@@ -33,7 +33,8 @@
 
 namespace ss {
 
-constexpr int kAttnPartStride = 132;  // floats per (warp, seg, g) partial: m, l, pad, pad, o[128]
+constexpr int kAttnPartStride = 132;
+constexpr int kMinUnitsPerWarp = 4;  // floats per (warp, seg, g) partial: m, l, pad, pad, o[128]
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -97,11 +98,28 @@ struct WarpSmem {
     using T = AttnTraits<BF16>;
     alignas(128) unsigned char buf[2][T::BLOCK_BYTES];
     alignas(16) float4 q4[G][kHeadDim / 4];  // q (fp32) in 16-byte chunks, chunk order below
+    alignas(16) float p[G][kBlockTokens];    // softmax numerators of the current block
     uint64_t bar[2];
 };
 
 __device__ __forceinline__ int64_t warp_of_unit(int64_t x, int64_t U, int W) {
     return ((x + 1) * (int64_t)W - 1) / U;
+}
+
+// q of the G heads of KV head (b, h): lane loads elements 4*lane .. 4*lane+3.
+template <bool BF16, int G>
+__device__ __forceinline__ void load_q(const AttnArgs& a, int b, int h, int lane, float4 (&r)[G]) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int64_t qi = ((int64_t)b * a.Hq + (int64_t)h * G + g) * kHeadDim + 4 * lane;
+        if (BF16) {
+            uint2 raw = __ldg(reinterpret_cast<const uint2*>((const uint16_t*)a.q + qi));
+            r[g] = make_float4(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u),
+                               __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xFFFF0000u));
+        } else {
+            r[g] = __ldg(reinterpret_cast<const float4*>((const float*)a.q + qi));
+        }
+    }
 }
 
 template <bool BF16, int G>
@@ -125,19 +143,19 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
 
     // ---- producer: next valid unit -> stage (lane 0 issues the bulk copy) ----
     int64_t next_u = u0;
-    int64_t bu[2];
+    int64_t bu0 = -1, bu1 = -1;  // unit held by stage 0 / 1 (-1: none)
     auto issue = [&](int stage) {
         const char* src = nullptr;
         while (next_u < u1) {
             int64_t p = next_u / Ku;
             int r = (int)(next_u % Ku);
             if (r < a.k) {
-                int32_t s = a.slot[p * a.k + r];
+                int32_t s = __ldg(a.slot + p * a.k + r);
                 if (s >= 0) {
                     src = (const char*)a.pool + (int64_t)s * T::BLOCK_BYTES;
                     break;
                 }
-            } else if (a.tail_len[p / a.Hkv] > 0) {
+            } else if (__ldg(a.tail_len + p / a.Hkv) > 0) {
                 src = (const char*)a.tail + p * (int64_t)T::BLOCK_BYTES;
                 break;
             }
@@ -151,36 +169,31 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
                 mbar_expect_tx(&sm.bar[stage], T::BLOCK_BYTES);
                 bulk_g2s(sm.buf[stage], src, T::BLOCK_BYTES, &sm.bar[stage]);
             }
-            bu[stage] = next_u++;
+            (stage ? bu1 : bu0) = next_u++;
         } else {
-            bu[stage] = -1;
+            (stage ? bu1 : bu0) = -1;
         }
     };
     issue(0);
     issue(1);
-    uint32_t phase[2] = {0u, 0u};
+    uint32_t phases = 0u;  // bit s = mbarrier phase of stage s
     int stage = 0;
 
     const int64_t p_first = u0 / Ku, p_last = (u1 - 1) / Ku;
+    float4 qn[G];  // q of the next pair, prefetched in registers
+    load_q<BF16, G>(a, (int)(p_first / a.Hkv), (int)(p_first % a.Hkv), lane, qn);
     for (int64_t p = p_first; p <= p_last; ++p) {
         const int b = (int)(p / a.Hkv), h = (int)(p % a.Hkv);
-        // q of the G heads of this KV head -> smem (fp32)
         __syncwarp();
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            const int64_t qi = ((int64_t)b * a.Hq + (int64_t)h * G + g) * kHeadDim + 4 * lane;
-            float4 v;
-            if (BF16) {
-                uint2 raw = *reinterpret_cast<const uint2*>((const uint16_t*)a.q + qi);
-                v = make_float4(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u),
-                                __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xFFFF0000u));
-                // element c = 4*lane + i: chunk c/8 = lane/2, half (c%8)/4 = lane&1
-                sm.q4[g][(lane >> 1) + 16 * (lane & 1)] = v;
-            } else {
-                v = *reinterpret_cast<const float4*>((const float*)a.q + qi);
-                sm.q4[g][lane] = v;
-            }
+            // element c = 4*lane + i.  bf16: chunk c/8 = lane/2, half (c%8)/4 = lane&1
+            if (BF16)
+                sm.q4[g][(lane >> 1) + 16 * (lane & 1)] = qn[g];
+            else
+                sm.q4[g][lane] = qn[g];
         }
+        if (p < p_last) load_q<BF16, G>(a, (int)((p + 1) / a.Hkv), (int)((p + 1) % a.Hkv), lane, qn);
         __syncwarp();
         float m[G], l[G], o[G][4];
 #pragma unroll
@@ -189,83 +202,84 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
             l[g] = 0.f;
             o[g][0] = o[g][1] = o[g][2] = o[g][3] = 0.f;
         }
-        const int tl = a.tail_len[b];
+        const int tl = __ldg(a.tail_len + b);
 
-        while (bu[stage] >= 0 && bu[stage] / Ku == p) {
-            const bool is_tail = (bu[stage] % Ku) == a.k;
-            mbar_wait(&sm.bar[stage], phase[stage]);
-            phase[stage] ^= 1u;
+        while (true) {
+            const int64_t cu = stage ? bu1 : bu0;
+            if (cu < 0 || cu / Ku != p) break;
+            const bool is_tail = (cu % Ku) == a.k;
+            mbar_wait(&sm.bar[stage], (phases >> stage) & 1u);
+            phases ^= 1u << stage;
             const unsigned char* kb = sm.buf[stage];
             const unsigned char* vb = kb + kBlockTokens * kHeadDim * T::ES;
-            // ---- logits: lane = token ----
-            float s0[G], s1[G];
+            // ---- logits: lane = token; 4 independent accumulators per head ----
+            float sacc[G][4];
 #pragma unroll
-            for (int g = 0; g < G; ++g) s0[g] = s1[g] = 0.f;
+            for (int g = 0; g < G; ++g) sacc[g][0] = sacc[g][1] = sacc[g][2] = sacc[g][3] = 0.f;
             const unsigned char* krow = kb + lane * kHeadDim * T::ES;
-#pragma unroll 4
+#pragma unroll
             for (int c = 0; c < T::NCH; ++c) {
                 const int cc = (c + lane) & (T::NCH - 1);
-                uint4 kv = *reinterpret_cast<const uint4*>(krow + cc * 16);
+                const uint4 kv = *reinterpret_cast<const uint4*>(krow + cc * 16);
+                const int a0 = (c & 1) * 2;
                 if (BF16) {
-                    float k0 = __uint_as_float(kv.x << 16), k1 = __uint_as_float(kv.x & 0xFFFF0000u);
-                    float k2 = __uint_as_float(kv.y << 16), k3 = __uint_as_float(kv.y & 0xFFFF0000u);
-                    float k4 = __uint_as_float(kv.z << 16), k5 = __uint_as_float(kv.z & 0xFFFF0000u);
-                    float k6 = __uint_as_float(kv.w << 16), k7 = __uint_as_float(kv.w & 0xFFFF0000u);
+                    const float k0 = __uint_as_float(kv.x << 16), k1 = __uint_as_float(kv.x & 0xFFFF0000u);
+                    const float k2 = __uint_as_float(kv.y << 16), k3 = __uint_as_float(kv.y & 0xFFFF0000u);
+                    const float k4 = __uint_as_float(kv.z << 16), k5 = __uint_as_float(kv.z & 0xFFFF0000u);
+                    const float k6 = __uint_as_float(kv.w << 16), k7 = __uint_as_float(kv.w & 0xFFFF0000u);
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
-                        float4 qa = sm.q4[g][cc], qb = sm.q4[g][cc + 16];
-                        s0[g] = fmaf(qa.x, k0, s0[g]);
-                        s1[g] = fmaf(qa.y, k1, s1[g]);
-                        s0[g] = fmaf(qa.z, k2, s0[g]);
-                        s1[g] = fmaf(qa.w, k3, s1[g]);
-                        s0[g] = fmaf(qb.x, k4, s0[g]);
-                        s1[g] = fmaf(qb.y, k5, s1[g]);
-                        s0[g] = fmaf(qb.z, k6, s0[g]);
-                        s1[g] = fmaf(qb.w, k7, s1[g]);
+                        const float4 qa = sm.q4[g][cc], qb = sm.q4[g][cc + 16];
+                        sacc[g][a0] = fmaf(qa.x, k0, sacc[g][a0]);
+                        sacc[g][a0 + 1] = fmaf(qa.y, k1, sacc[g][a0 + 1]);
+                        sacc[g][a0] = fmaf(qa.z, k2, sacc[g][a0]);
+                        sacc[g][a0 + 1] = fmaf(qa.w, k3, sacc[g][a0 + 1]);
+                        sacc[g][a0] = fmaf(qb.x, k4, sacc[g][a0]);
+                        sacc[g][a0 + 1] = fmaf(qb.y, k5, sacc[g][a0 + 1]);
+                        sacc[g][a0] = fmaf(qb.z, k6, sacc[g][a0]);
+                        sacc[g][a0 + 1] = fmaf(qb.w, k7, sacc[g][a0 + 1]);
                     }
                 } else {
-                    float k0 = __uint_as_float(kv.x), k1 = __uint_as_float(kv.y);
-                    float k2 = __uint_as_float(kv.z), k3 = __uint_as_float(kv.w);
+                    const float k0 = __uint_as_float(kv.x), k1 = __uint_as_float(kv.y);
+                    const float k2 = __uint_as_float(kv.z), k3 = __uint_as_float(kv.w);
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
-                        float4 qa = sm.q4[g][cc];
-                        s0[g] = fmaf(qa.x, k0, s0[g]);
-                        s1[g] = fmaf(qa.y, k1, s1[g]);
-                        s0[g] = fmaf(qa.z, k2, s0[g]);
-                        s1[g] = fmaf(qa.w, k3, s1[g]);
+                        const float4 qa = sm.q4[g][cc];
+                        sacc[g][a0] = fmaf(qa.x, k0, sacc[g][a0]);
+                        sacc[g][a0 + 1] = fmaf(qa.y, k1, sacc[g][a0 + 1]);
+                        sacc[g][a0] = fmaf(qa.z, k2, sacc[g][a0]);
+                        sacc[g][a0 + 1] = fmaf(qa.w, k3, sacc[g][a0 + 1]);
                     }
                 }
             }
             const bool valid = !is_tail || lane < tl;
-            float pz[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                float z = valid ? (s0[g] + s1[g]) * a.scale_log2 : -INFINITY;
-                float mx = warp_max(z);
-                float mnew = fmaxf(m[g], mx);
-                float corr = exp2f(m[g] - mnew);
-                float pp = exp2f(z - mnew);
+                const float s = (sacc[g][0] + sacc[g][1]) + (sacc[g][2] + sacc[g][3]);
+                const float z = valid ? s * a.scale_log2 : -INFINITY;
+                const float mnew = fmaxf(m[g], warp_max(z));
+                const float corr = exp2f(m[g] - mnew);
+                const float pp = exp2f(z - mnew);
+                sm.p[g][lane] = pp;
                 l[g] = l[g] * corr + warp_sum(pp);
                 o[g][0] *= corr;
                 o[g][1] *= corr;
                 o[g][2] *= corr;
                 o[g][3] *= corr;
                 m[g] = mnew;
-                pz[g] = pp;
             }
+            __syncwarp();
             // ---- O += P V: lane owns dims 4*lane .. 4*lane+3 ----
-            const int nt = is_tail ? tl : kBlockTokens;
-#pragma unroll 4
-            for (int t = 0; t < nt; ++t) {
+            auto pv_token = [&](int t, const float (&pt)[G]) {
                 float v0, v1, v2, v3;
                 if (BF16) {
-                    uint2 vv = *reinterpret_cast<const uint2*>(vb + (t * kHeadDim + 4 * lane) * 2);
+                    const uint2 vv = *reinterpret_cast<const uint2*>(vb + (t * kHeadDim + 4 * lane) * 2);
                     v0 = __uint_as_float(vv.x << 16);
                     v1 = __uint_as_float(vv.x & 0xFFFF0000u);
                     v2 = __uint_as_float(vv.y << 16);
                     v3 = __uint_as_float(vv.y & 0xFFFF0000u);
                 } else {
-                    float4 vv = *reinterpret_cast<const float4*>(vb + (t * kHeadDim + 4 * lane) * 4);
+                    const float4 vv = *reinterpret_cast<const float4*>(vb + (t * kHeadDim + 4 * lane) * 4);
                     v0 = vv.x;
                     v1 = vv.y;
                     v2 = vv.z;
@@ -273,11 +287,39 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
                 }
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    float pt = __shfl_sync(0xffffffffu, pz[g], t);
-                    o[g][0] = fmaf(pt, v0, o[g][0]);
-                    o[g][1] = fmaf(pt, v1, o[g][1]);
-                    o[g][2] = fmaf(pt, v2, o[g][2]);
-                    o[g][3] = fmaf(pt, v3, o[g][3]);
+                    o[g][0] = fmaf(pt[g], v0, o[g][0]);
+                    o[g][1] = fmaf(pt[g], v1, o[g][1]);
+                    o[g][2] = fmaf(pt[g], v2, o[g][2]);
+                    o[g][3] = fmaf(pt[g], v3, o[g][3]);
+                }
+            };
+            if (!is_tail) {
+#pragma unroll
+                for (int t4 = 0; t4 < kBlockTokens; t4 += 4) {
+                    float4 p4[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) p4[g] = *reinterpret_cast<const float4*>(&sm.p[g][t4]);
+                    float pt[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) pt[g] = p4[g].x;
+                    pv_token(t4 + 0, pt);
+#pragma unroll
+                    for (int g = 0; g < G; ++g) pt[g] = p4[g].y;
+                    pv_token(t4 + 1, pt);
+#pragma unroll
+                    for (int g = 0; g < G; ++g) pt[g] = p4[g].z;
+                    pv_token(t4 + 2, pt);
+#pragma unroll
+                    for (int g = 0; g < G; ++g) pt[g] = p4[g].w;
+                    pv_token(t4 + 3, pt);
+                }
+            } else {
+                // tail block: only the first tl rows hold data (the rest may be garbage)
+                for (int t = 0; t < tl; ++t) {
+                    float pt[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) pt[g] = sm.p[g][t];
+                    pv_token(t, pt);
                 }
             }
             __syncwarp();
@@ -290,10 +332,10 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
         if (full) {
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                float inv = l[g] > 0.f ? 1.f / l[g] : 0.f;
-                float4 r = make_float4(o[g][0] * inv, o[g][1] * inv, o[g][2] * inv, o[g][3] * inv);
+                const float inv = l[g] > 0.f ? 1.f / l[g] : 0.f;
                 const int hq = h * G + g;
-                *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) = r;
+                *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) =
+                    make_float4(o[g][0] * inv, o[g][1] * inv, o[g][2] * inv, o[g][3] * inv);
             }
             continue;
         }
@@ -317,28 +359,41 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
         const int64_t wl = warp_of_unit((p + 1) * Ku - 1, a.U, a.W);
         if (ticket != (int)(wl - wf)) continue;
         __threadfence();
+        // merge the contributors' partials in warp order (deterministic); the
+        // per-partial (m, l) are read lane-parallel, o with independent loads
+        const int nc = (int)(wl - wf + 1);
         for (int g = 0; g < G; ++g) {
             float mt = -INFINITY;
-            for (int64_t w2 = wf; w2 <= wl; ++w2) {
+            for (int i = lane; i < nc; i += 32) {
+                const int64_t w2 = wf + i;
                 const int s2 = ((a.U * w2 / a.W) / Ku == p) ? 0 : 1;
-                const float* pp = a.part + ((w2 * 2 + s2) * G + g) * kAttnPartStride;
-                mt = fmaxf(mt, __ldcg(pp));
+                mt = fmaxf(mt, __ldcg(a.part + ((w2 * 2 + s2) * G + g) * kAttnPartStride));
             }
-            float lt = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+            mt = warp_max(mt);
+            float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f, lt = 0.f;
             if (mt != -INFINITY) {
-                for (int64_t w2 = wf; w2 <= wl; ++w2) {
+                float lpart = 0.f;
+                for (int i = lane; i < nc; i += 32) {
+                    const int64_t w2 = wf + i;
                     const int s2 = ((a.U * w2 / a.W) / Ku == p) ? 0 : 1;
                     const float* pp = a.part + ((w2 * 2 + s2) * G + g) * kAttnPartStride;
-                    float sc = exp2f(__ldcg(pp) - mt);
-                    lt += __ldcg(pp + 1) * sc;
-                    float4 ov = __ldcg(reinterpret_cast<const float4*>(pp + 4 + 4 * lane));
-                    o0 += ov.x * sc;
-                    o1 += ov.y * sc;
-                    o2 += ov.z * sc;
-                    o3 += ov.w * sc;
+                    lpart += __ldcg(pp + 1) * exp2f(__ldcg(pp) - mt);
+                }
+                lt = warp_sum(lpart);
+#pragma unroll 4
+                for (int i = 0; i < nc; ++i) {
+                    const int64_t w2 = wf + i;
+                    const int s2 = ((a.U * w2 / a.W) / Ku == p) ? 0 : 1;
+                    const float* pp = a.part + ((w2 * 2 + s2) * G + g) * kAttnPartStride;
+                    const float sc = exp2f(__ldcg(pp) - mt);
+                    const float4 ov = __ldcg(reinterpret_cast<const float4*>(pp + 4 + 4 * lane));
+                    o0 = fmaf(ov.x, sc, o0);
+                    o1 = fmaf(ov.y, sc, o1);
+                    o2 = fmaf(ov.z, sc, o2);
+                    o3 = fmaf(ov.w, sc, o3);
                 }
             }
-            float inv = lt > 0.f ? 1.f / lt : 0.f;
+            const float inv = lt > 0.f ? 1.f / lt : 0.f;
             const int hq = h * G + g;
             *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) =
                 make_float4(o0 * inv, o1 * inv, o2 * inv, o3 * inv);
@@ -395,7 +450,9 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
     a.scale_log2 = scale * 1.4426950408889634f;
     const int G = d.num_q_heads / d.num_kv_heads;
     a.U = (int64_t)d.batch * d.num_kv_heads * (k + 1);
-    a.W = (int)std::min<int64_t>(attn_total_warps(dt), a.U);
+    // at least kMinUnitsPerWarp units per warp: fewer, longer ranges when the
+    // problem is small (fewer partials to merge); W <= U keeps every range non-empty
+    a.W = (int)std::max<int64_t>(1, std::min<int64_t>(attn_total_warps(dt), a.U / kMinUnitsPerWarp));
     size_t part = (size_t)a.W * 2 * G * kAttnPartStride * 4;
     a.part = (float*)ws;
     a.tickets = (int32_t*)((char*)ws + part);

@@ -1,0 +1,128 @@
+"""Per-kernel microbenchmarks at C2 / C3 shapes (CUDA events, many launches,
+inputs larger than L2).  Development tool; bench.py is the contract.
+
+  python tools/kbench.py [select|attn|gather|cache|all] [--cfg C2|C3]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2509_24626_b200 import ops  # noqa: E402
+
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6550.0
+
+CFG = {"C2": dict(B=16, Hq=32, Hkv=32, n_blk=4096, k=64, S=131072),
+       "C3": dict(B=4, Hq=32, Hkv=8, n_blk=32768, k=128, S=8192)}
+
+
+def timeit(fn, iters=20, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def bench_select(c, iters):
+    B, Hq, Hkv, n, k = c["B"], c["Hq"], c["Hkv"], c["n_blk"], c["k"]
+    nm = 2
+    metas = [torch.randn(B * Hkv * n * 2 * 128, device="cuda").to(torch.bfloat16) for _ in range(nm)]
+    q = torch.randn(B, Hq, 128, device="cuda").to(torch.bfloat16)
+    d = ops.dims(B, Hq, Hkv)
+    ws = ops.alloc_workspace(0, d, n, k)
+    sel = torch.empty(B, Hkv, k, dtype=torch.int32, device="cuda")
+    nb = torch.full((B,), n, dtype=torch.int32, device="cuda")
+    i = [0]
+
+    def f():
+        ops.ss_block_select(q, metas[i[0] % nm], nb, n, k, d, sel, ws)
+        i[0] += 1
+    ms = timeit(f, iters)
+    byts = B * Hkv * n * 512 + q.numel() * 2
+    return {"kernel": "select", "us": ms * 1e3, "GBps": byts / ms / 1e6, "frac": byts / ms / 1e6 / PEAK}
+
+
+def bench_attn(c, iters):
+    B, Hq, Hkv, k, S = c["B"], c["Hq"], c["Hkv"], c["k"], c["S"]
+    pool = torch.randn(S * 2 * 32 * 128, device="cuda").to(torch.bfloat16)
+    slot = torch.stack([torch.randperm(S, device="cuda")[:k] for _ in range(B * Hkv)]).view(B, Hkv, k)
+    slot = slot.sort(-1).values.to(torch.int32).contiguous()
+    q = torch.randn(B, Hq, 128, device="cuda").to(torch.bfloat16)
+    tail = torch.zeros(B * Hkv * 2 * 32 * 128, dtype=torch.bfloat16, device="cuda")
+    tl = torch.zeros(B, dtype=torch.int32, device="cuda")
+    d = ops.dims(B, Hq, Hkv)
+    ws = ops.alloc_workspace(2, d, 32, k)
+    out = torch.empty(Hq, B, 128, dtype=torch.float32, device="cuda")
+    # flush between iterations: pool per-call bytes may fit in L2 (C3: 64 MB)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def f():
+        ops.sparse_decode_attn(q, pool, slot, k, tail, tl, d, 1 / math.sqrt(128), out, ws)
+    ms_total = 0.0
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    for _ in range(3):
+        f()
+    ts = []
+    for _ in range(iters):
+        flush.zero_()
+        s.record()
+        f()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    ms = sorted(ts)[len(ts) // 2]
+    byts = B * Hkv * k * 16384
+    return {"kernel": "attn", "us": ms * 1e3, "GBps": byts / ms / 1e6, "frac": byts / ms / 1e6 / PEAK}
+
+
+def bench_gather(c, iters, nmiss=2500):
+    hb = 1 << 18  # 4 GiB host
+    host = torch.empty(hb * 8192, dtype=torch.bfloat16, pin_memory=True)
+    ptr = ops.host_device_pointer(host)
+    S = c["S"]
+    pool = torch.empty(S * 8192, dtype=torch.bfloat16, device="cuda")
+    keys = torch.randint(0, hb, (nmiss,), device="cuda", dtype=torch.int64)
+    slots = torch.randperm(S, device="cuda")[:nmiss].to(torch.int32)
+    counts = torch.tensor([0, nmiss, 0, 0], dtype=torch.int32, device="cuda")
+
+    def f():
+        ops.flash_h2d_gather(ptr, hb, keys, slots, counts, nmiss, pool, 16384)
+    ms = timeit(f, iters)
+    return {"kernel": "gather", "misses": nmiss, "us": ms * 1e3, "GBps": nmiss * 16384 / ms / 1e6}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", nargs="?", default="all")
+    ap.add_argument("--cfg", default="C2")
+    ap.add_argument("--iters", type=int, default=20)
+    a = ap.parse_args()
+    c = CFG[a.cfg]
+    res = []
+    if a.what in ("select", "all"):
+        res.append(bench_select(c, a.iters))
+    if a.what in ("attn", "all"):
+        res.append(bench_attn(c, a.iters))
+    if a.what in ("gather", "all"):
+        for m in (64, 2500, 20000):
+            res.append(bench_gather(c, a.iters, m))
+    for r in res:
+        r["cfg"] = a.cfg
+        print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}))
+
+
+if __name__ == "__main__":
+    main()
