@@ -135,7 +135,7 @@ def setup_engine(args, rank: int, world: int):
     hq = W["num_q_heads"] // world
     cfg = EngineConfig(batch=W["batch"], layers=W["layers"], num_q_heads=hq, num_kv_heads=hkv,
                        max_blk=W["max_blk"], topk=W["topk"], slots_per_layer=W["slots"],
-                       num_requests=W["batch"], dtype=torch.bfloat16)
+                       num_requests=W["batch"], dtype=torch.bfloat16, groups=args.groups)
     eng = DecodeEngine(cfg)
     # physical host pool: a prime number of max_blk runs (aliasing, R15)
     runs = args.host_runs
@@ -182,15 +182,23 @@ def gen_queries(eng, steps, rho, seed):
 # our arm
 # ----------------------------------------------------------------------------
 class StepTimers:
-    """CUDA events around each op of each layer, on the launching stream."""
+    """CUDA events around each op of each layer, recorded on the launching
+    stream (each request group's own stream)."""
 
     def __init__(self):
         self.ev = {"select": [], "cache": [], "gather": [], "attn": [], "allgather": []}
+        self.trace = []          # (name, group, layer, start_event, end_event) in issue order
 
-    def mark(self, name):
+    def mark(self, name, group=0, layer=0):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         self.ev[name].append((s, e))
+        self.trace.append((name, group, layer, s, e))
         return s, e
+
+    def timeline(self, ref, first_n):
+        """[(op, group, layer, start_ms, end_ms)] relative to event `ref`."""
+        return [(n, g, l, round(ref.elapsed_time(s), 4), round(ref.elapsed_time(e), 4))
+                for n, g, l, s, e in self.trace[:first_n]]
 
     def totals_ms(self):
         return {k: sum(s.elapsed_time(e) for s, e in v) for k, v in self.ev.items()}
@@ -199,33 +207,23 @@ class StepTimers:
         return {k: len(v) for k, v in self.ev.items()}
 
 
-def run_step(eng, q_step, stamp, timers=None, pg=None, world=1, gathered=None):
-    from paper_2509_24626_b200 import ops
-    from paper_2509_24626_b200.shard import gather_outputs
-    c = eng.cfg
-    for l in range(c.layers):
-        q = q_step[l]
-        def timed(name, fn):
+def run_step(eng, q_step, stamp, timers=None, pgs=None, world=1, gathered=None):
+    """One decode step of every layer through the engine (S1..S5 per layer and
+    request group); with N > 1 ranks, S6 = all-gather of each layer's per-head
+    outputs on the group's stream right after its attention."""
+    hook = None
+    if world > 1:
+        from paper_2509_24626_b200.shard import gather_outputs
+
+        def hook(gi, g, l):
             if timers is None:
-                fn()
+                gather_outputs(g.out[l], gathered[gi][l], group=pgs[gi])
             else:
-                s, e = timers.mark(name)
+                s, e = timers.mark("allgather")
                 s.record()
-                fn()
+                gather_outputs(g.out[l], gathered[gi][l], group=pgs[gi])
                 e.record()
-        timed("select", lambda: ops.ss_block_select(q, eng.meta[l], eng.n_blk, c.max_blk, c.topk,
-                                                    eng.dims, eng.sel[l], eng.ws_select))
-        timed("cache", lambda: ops.kv_cache_lookup_insert(
-            eng.pools[l], eng.sel[l], eng.req_ids, l, c.layers, c.max_blk, c.topk, eng.dims, stamp,
-            eng.slot[l], eng.hit[l], eng.miss_keys[l], eng.miss_slots[l], eng.counts[l], eng.ws_cache))
-        timed("gather", lambda: ops.flash_h2d_gather(eng.host_ptr, eng.host_blocks, eng.miss_keys[l],
-                                                     eng.miss_slots[l], eng.counts[l], eng.E,
-                                                     eng.pool_kv[l], c.block_bytes))
-        timed("attn", lambda: ops.sparse_decode_attn(q, eng.pool_kv[l], eng.slot[l], c.topk,
-                                                     eng.tail_kv[l], eng.tail_len, eng.dims, eng.scale,
-                                                     eng.out[l], eng.ws_attn, counts=eng.counts[l]))
-        if world > 1:
-            timed("allgather", lambda: gather_outputs(eng.out[l], gathered[l], group=pg))
+    eng.step(q_step, stamp, timers=timers, post_attn=hook)
 
 
 def measure_h2d_peak(nbytes=1 << 30):
@@ -278,10 +276,9 @@ def bench_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    pg = None
+    pgs = None
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
-        pg = torch.distributed.group.WORLD
     t_setup = time.time()
     eng, W = setup_engine(args, rank, world)
     c = eng.cfg
@@ -290,8 +287,10 @@ def bench_ours(args):
     qs = gen_queries(eng, steps_total + e2e_steps, W["rho"], seed=5000 + rank)
     gathered = None
     if world > 1:
-        gathered = torch.empty(c.layers, c.num_q_heads * world, c.batch, 128, dtype=torch.float32,
-                               device="cuda")
+        # one communicator per request group (their all-gathers run on different streams)
+        pgs = [torch.distributed.new_group(list(range(world))) for _ in eng.groups]
+        gathered = [torch.empty(c.layers, c.num_q_heads * world, g.nb, 128, dtype=torch.float32,
+                                device="cuda") for g in eng.groups]
     h2d_peak = measure_h2d_peak()
     setup_s = time.time() - t_setup
 
@@ -305,12 +304,11 @@ def bench_ours(args):
     for t in range(args.warmup):
         s, e = torch.cuda.Event(True), torch.cuda.Event(True)
         s.record()
-        run_step(eng, qs[t], stamp=t + 1, pg=pg, world=world, gathered=gathered)
+        run_step(eng, qs[t], stamp=t + 1, pgs=pgs, world=world, gathered=gathered)
         e.record()
         torch.cuda.synchronize()
         if t == 0:
             cold_ms = s.elapsed_time(e)
-    counts_before = eng.counts.clone()
     # timed region
     timers = StepTimers()
     sampler = ClockSampler(local)
@@ -321,12 +319,17 @@ def bench_ours(args):
     hits = torch.zeros(4, dtype=torch.int64, device="cuda")
     start.record()
     for t in range(args.warmup, steps_total):
-        run_step(eng, qs[t], stamp=t + 1, timers=timers, pg=pg, world=world, gathered=gathered)
-        hits += eng.counts.to(torch.int64).sum(0)
+        run_step(eng, qs[t], stamp=t + 1, timers=timers, pgs=pgs, world=world, gathered=gathered)
+        for g in eng.groups:
+            hits += g.counts.to(torch.int64).sum(0)
     end.record()
     barrier()
     clocks = sampler.stop()
     ms = start.elapsed_time(end)
+    if args.timeline and rank == 0:
+        ops_per_step = len(timers.trace) // args.steps
+        with open(args.timeline, "w") as f:
+            json.dump(timers.timeline(start, ops_per_step), f)
     if world > 1:
         tt = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -386,15 +389,17 @@ def bench_ours(args):
     # fresh drifting queries per step (continuing the same q process), staged in
     # pinned host memory; each step copies its own q in and its outputs out.
     q_host = qs[steps_total:steps_total + e2e_steps].cpu().pin_memory()
-    out_host = torch.empty((gathered if world > 1 else eng.out).shape, dtype=torch.float32, pin_memory=True)
+    outs = gathered if world > 1 else eng.outputs()
+    out_host = [torch.empty(o.shape, dtype=torch.float32, pin_memory=True) for o in outs]
     q_dev = torch.empty_like(qs[0])
     barrier()
     e_s, e_e = torch.cuda.Event(True), torch.cuda.Event(True)
     e_s.record()
     for i in range(e2e_steps):
         q_dev.copy_(q_host[i], non_blocking=True)
-        run_step(eng, q_dev, stamp=steps_total + 1 + i, pg=pg, world=world, gathered=gathered)
-        out_host.copy_(gathered if world > 1 else eng.out, non_blocking=True)
+        run_step(eng, q_dev, stamp=steps_total + 1 + i, pgs=pgs, world=world, gathered=gathered)
+        for oh, o in zip(out_host, outs):
+            oh.copy_(o, non_blocking=True)
     e_e.record()
     barrier()
     e_ms = e_s.elapsed_time(e_e)
@@ -404,7 +409,7 @@ def bench_ours(args):
         e_ms = float(tt.item())
     e2e = {"value": round(c.batch * e2e_steps / (e_ms * 1e-3), 2), "unit": "tokens/s",
            "h2d_bytes_per_step": int(q_host.numel() * q_host.element_size()),
-           "d2h_bytes_per_step": int(out_host.numel() * out_host.element_size()),
+           "d2h_bytes_per_step": int(sum(o.numel() * o.element_size() for o in out_host)),
            "steps": e2e_steps}
 
     cpu = None
@@ -426,6 +431,7 @@ def bench_ours(args):
                        "topk_blocks": c.topk, "hbm_cache_slots_per_layer": c.slots_per_layer,
                        "host_pool_blocks": eng.host_blocks, "host_kv": "pinned DRAM, zero-copy (UVA)",
                        "parallelism": f"kv-heads/{world} per GPU" if world > 1 else "1 GPU",
+                       "request_groups": len(eng.groups),
                        "l2": "no flush needed: inputs larger than L2 (32 GiB metadata streamed per step)",
                        "scope": "attention path only (no QKV/O projections, no FFN)"},
             "hit_rate": round(hit_rate, 4), "misses_per_step": n_miss / args.steps,
@@ -435,7 +441,7 @@ def bench_ours(args):
                           "frac": kernels["flash_h2d_gather"]["frac"]},
             "roofline": roofline, "kernels": kernels,
             "cold_step_ms": round(cold_ms, 2) if cold_ms else None,
-            "e2e": e2e, "gpu_launches": int(args.steps * c.layers * 10),
+            "e2e": e2e, "gpu_launches": int(args.steps * c.layers * 10 * len(eng.groups)),
             "cpu_baseline": cpu, "clocks": clocks, "setup_s": round(setup_s, 1),
             "errors_in_timed_region": n_err,
         }
@@ -498,6 +504,9 @@ def main():
     ap.add_argument("--host-runs", type=int, default=251,
                     help="physical host KV pool = host_runs x max_blk blocks (251 -> 15.7 GiB)")
     ap.add_argument("--cpu-req", type=int, default=1)
+    ap.add_argument("--timeline", default=None, help="write the first timed step's op timeline (json)")
+    ap.add_argument("--groups", type=int, default=2,
+                    help="request groups pipelined on separate streams (PCIe of one overlaps HBM work of another)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"

@@ -124,6 +124,7 @@ ss_status ss_block_select(const void* q, const void* meta, const int32_t* n_blk,
  *   slot_key   int64 [S]: slot -> key, -1 if empty.          Initially -1.
  *   slot_stamp int64 [S]: stamp of last use, -1 if never used. Initially -1.
  *   order      int32 [S]: slots sorted by (slot_stamp, slot).  Initially 0..S-1.
+ *   order_pos  int32 [S]: position of each slot in `order`.    Initially 0..S-1.
  * Batch-LRU (reading R12): key = ((req_ids[b]*L + layer)*Hkv + h)*max_blk + j
  * for every sel[b][h][r] >= 0, in canonical (b, h, r) order.  Hits keep their
  * slot and get slot_stamp = stamp.  The i-th miss takes the i-th slot, in
@@ -145,7 +146,13 @@ typedef struct {
     int64_t* slot_key;
     int64_t* slot_stamp;
     int32_t* order;
+    int32_t* order_pos;  /* inverse permutation of order.      Initially 0..S-1. */
     int32_t num_slots;
+    /* Optional device int64 "clock" (NULL = use the `stamp` argument).  When
+     * set, the call's stamp is *clock + 1 (the `stamp` argument is ignored)
+     * and *clock is advanced to it on success (left unchanged on error), so a
+     * captured CUDA graph can replay decode steps without host-side scalars. */
+    int64_t* clock;
 } ss_cache_pool;
 
 ss_status kv_cache_lookup_insert(ss_cache_pool pool, const int32_t* sel, const int32_t* req_ids,

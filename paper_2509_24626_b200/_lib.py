@@ -30,7 +30,9 @@ class SSDims(ctypes.Structure):
 class SSCachePool(ctypes.Structure):
     _fields_ = [("fwd", ctypes.c_void_p), ("fwd_len", ctypes.c_int64),
                 ("slot_key", ctypes.c_void_p), ("slot_stamp", ctypes.c_void_p),
-                ("order", ctypes.c_void_p), ("num_slots", ctypes.c_int32)]
+                ("order", ctypes.c_void_p), ("order_pos", ctypes.c_void_p),
+                ("num_slots", ctypes.c_int32),
+                ("clock", ctypes.c_void_p)]
 
 
 class SparseServeError(RuntimeError):

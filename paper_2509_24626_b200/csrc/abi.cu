@@ -73,7 +73,8 @@ ss_status kv_cache_lookup_insert(ss_cache_pool pool, const int32_t* sel, const i
                                  ss_dims dims, int64_t stamp, int32_t* slot_out,
                                  uint8_t* hit_out, int64_t* miss_keys, int32_t* miss_slots,
                                  int32_t* counts, void* ws, size_t ws_bytes, void* stream) {
-    if (!pool.fwd || !pool.slot_key || !pool.slot_stamp || !pool.order || pool.num_slots < 1 ||
+    if (!pool.fwd || !pool.slot_key || !pool.slot_stamp || !pool.order || !pool.order_pos ||
+        pool.num_slots < 1 ||
         pool.fwd_len < 1)
         return SS_ERR_INVALID_ARG;
     if (!sel || !req_ids || !slot_out || !hit_out || !miss_keys || !miss_slots || !counts)

@@ -7,17 +7,18 @@
 //   S(j) = max_g  sum_{c=0..127} max(q_{g,c} * M_{j,c}, q_{g,c} * m_{j,c})
 // in float64, summed sequentially c = 0..127 from +0.0, then +0.0.
 //
-// Exactness argument.  With q' = q * 2^896 and X' = X * 2^-896 (both exact in
-// float64 for every finite bf16/f32 X, including subnormals), the product
-// q' * X' equals q * X exactly, and one DFMA rounds (acc + q*X) once -- the same
-// rounding as the oracle's rounded sum of an exact product.  X' is built from
-// the storage bits with integer ops only (sign | exp/mantissa >> 3): no F2F
-// conversions.  max(q*M, q*m) = q+ * M + q- * m with q+ = max(q,0),
-// q- = min(q,0); the extra term is an exact +-0 and leaves acc unchanged (acc is
-// never -0), so two DFMAs per (head, channel) reproduce the oracle's sum.
+// Exactness argument.  A bf16 (or f32) metadata element X converts EXACTLY to
+// float64 (F2F), q*X is exact in float64 (<= 48 significant bits), and one
+// DFMA rounds (acc + q*X) once -- the same rounding as the oracle's
+// `acc = acc + max(q*M, q*m)` with its exact product.  G == 1: the sign of q
+// is warp-uniform per channel, so a per-channel LOP3 mask picks M (q >= 0) or
+// m (q < 0) from the two bf16 words before the convert: one select, one F2F,
+// one DFMA per channel.  G > 1: min and max are converted once per channel and
+// each head adds q+ * M then q- * m (q+ = max(q,0), q- = min(q,0)); the extra
+// term is an exact +-0 and leaves acc unchanged (acc is never -0).
 //
-// Work decomposition.  Grid (chunks, B*Hkv); a CTA scores CH = 2048 blocks of one
-// (b, h) pair.  Warp w owns metadata tiles w, w+8, ...; lane r of a warp owns
+// Work decomposition.  One CTA per (pair, chunk) work item; a CTA scores
+// CH = 1024 blocks (SS_SEL_CHUNK) of one (b, h) pair.  Warp w owns metadata tiles w, w+8, ...; lane r of a warp owns
 // block r of the tile, so every 16-byte chunk load of the warp is one
 // contiguous 512-byte segment of the tiled layout (fully coalesced, streaming,
 // no L1 allocation).  Scores become order-preserving 64-bit keys in shared
@@ -43,7 +44,7 @@ constexpr int kSelChunkDefault = 1024;  // measured best at C2 (tools/kbench.py)
 constexpr int kSelMaxMerge = 8192;
 
 struct SelSmemLayout {
-    // qpn[c*G + g] = (q+ * 2^896, q- * 2^896)
+    // G > 1: qpn[c*G + g] = (q+, q-); G == 1: q (f64) [128] + masks [128]
     static size_t bytes(int G, int nkeys) {
         return (size_t)kHeadDim * G * 16 + (size_t)nkeys * 8 + (size_t)nkeys * 4 + 256 * 4 + 64 * 4;
     }
@@ -52,18 +53,6 @@ struct SelSmemLayout {
 __device__ __forceinline__ uint64_t ord_key(double s) {
     uint64_t b = (uint64_t)__double_as_longlong(s);
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
-
-// bf16 pair word -> scaled float64 of the low / high element (value * 2^-896).
-__device__ __forceinline__ double bf16lo_scaled(uint32_t w) {
-    uint32_t u = w << 16;
-    return __hiloint2double((int)((u & 0x80000000u) | ((u >> 3) & 0x0FFFE000u)), 0);
-}
-__device__ __forceinline__ double bf16hi_scaled(uint32_t w) {
-    return __hiloint2double((int)((w & 0x80000000u) | ((w >> 3) & 0x0FFFE000u)), 0);
-}
-__device__ __forceinline__ double f32_scaled(uint32_t w) {
-    return __hiloint2double((int)((w & 0x80000000u) | ((w >> 3) & 0x0FFFFFFFu)), (int)(w << 29));
 }
 
 // ---------------------------------------------------------------------------
@@ -156,7 +145,7 @@ template <bool BF16, int G>
 __global__ void __launch_bounds__(kSelThreads, 2)
 block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                     const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
-                    int nchunks, int CH, int32_t* __restrict__ sel, double* __restrict__ scores,
+                    int nchunks, int CH, int npairs, int l2pf, int32_t* __restrict__ sel, double* __restrict__ scores,
                     uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_j,
                     int32_t* __restrict__ tickets) {
     constexpr int ES = BF16 ? 2 : 4;
@@ -171,13 +160,17 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     int* hist = (int*)(jpos + nkeys_cap);                               // [256]
     int* sw = hist + 256;                                               // [64]
 
-    const int pair = blockIdx.y;
+    const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+    // persistent: CTAs stride over (pair, chunk) work items, so the grid is fully
+    // resident and a FlashH2D kernel of another request group can co-reside
+    for (int item = blockIdx.x; item < nchunks * npairs; item += gridDim.x) {
+    __syncthreads();  // previous item's shared-memory readers are done
+    const int pair = item / nchunks;
     const int b = pair / Hkv, h = pair % Hkv;
-    const int ci = blockIdx.x;  // chunk index
+    const int ci = item % nchunks;  // chunk index
     const int nb = n_blk_arr[b];
     const int nch_b = max(1, (nb + CH - 1) / CH);
-    if (ci >= nch_b) return;
-    const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+    if (ci >= nch_b) continue;
 
     // G == 1 (MHA): q as float64 plus per-channel select masks (q >= 0 -> max
     // row, else min row), so each channel costs one LOP3-select, one exact
@@ -201,7 +194,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
             qmask1[i] = m;
         }
     }
-    // G > 1: q for the G query heads of this KV head, as (q+, q-) * 2^896.
+    // G > 1: q for the G query heads of this KV head, as (q+, q-) = (max(q,0), min(q,0)).
     if constexpr (G > 1)
     for (int i = tid; i < kHeadDim * G; i += kSelThreads) {
         int g = i % G, c = i / G;
@@ -211,7 +204,6 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
             qd = (double)__uint_as_float(((uint32_t)((const uint16_t*)q)[qi]) << 16);
         else
             qd = (double)((const float*)q)[qi];
-        qd = qd * 0x1p896;  // exact power-of-two scaling
         qpn[i] = make_double2(qd > 0.0 ? qd : 0.0, qd < 0.0 ? qd : 0.0);
     }
     __syncthreads();
@@ -225,6 +217,8 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     for (int tl = warp; tl < ntiles; tl += kSelWarps) {
         const int tile = j0 / 32 + tl;
         const char* tb = meta_pair + (size_t)tile * TILE_ELEMS * ES + lane * 16;
+        if (l2pf && lane == 0 && tl + kSelWarps < ntiles)  // next tile of this warp -> L2
+            prefetch_l2_bulk(meta_pair + (size_t)(tile + kSelWarps) * TILE_ELEMS * ES, TILE_ELEMS * ES);
         // fully unrolled over the NCH chunks, loads kept D chunks ahead
         constexpr int D = 6, R = D + 1;
         uint4 mn[R], mx[R];
@@ -268,53 +262,45 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     for (int tl = warp; tl < ntiles; tl += kSelWarps) {
         const int tile = j0 / 32 + tl;
         const char* tb = meta_pair + (size_t)tile * TILE_ELEMS * ES + lane * 16;
+        if (l2pf && lane == 0 && tl + kSelWarps < ntiles)  // next tile of this warp -> L2
+            prefetch_l2_bulk(meta_pair + (size_t)(tile + kSelWarps) * TILE_ELEMS * ES, TILE_ELEMS * ES);
         double acc[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) acc[g] = 0.0;
-        // chunk s: min row at ((s*2+0)*32 + lane)*16 bytes, max at ((s*2+1)*32 + lane)*16
-        constexpr int U = 4;
-        uint4 mn[U], mx[U];
+        // fully unrolled over the NCH chunks, loads kept D chunks ahead; the
+        // min / max elements are converted once (exact f32 -> f64) and shared
+        // by the G heads: acc_g += q+_g * M + q-_g * m (one term is an exact 0)
+        constexpr int D = 4, R = D + 1;
+        uint4 mn[R], mx[R];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            mn[u] = ldg_stream(tb + (size_t)((u * 2 + 0) * 32) * 16);
-            mx[u] = ldg_stream(tb + (size_t)((u * 2 + 1) * 32) * 16);
+        for (int s = 0; s < D; ++s) {
+            mn[s] = ldg_stream(tb + (size_t)((s * 2 + 0) * 32) * 16);
+            mx[s] = ldg_stream(tb + (size_t)((s * 2 + 1) * 32) * 16);
         }
-#pragma unroll 1
-        for (int s0 = 0; s0 < NCH; s0 += U) {
-            uint4 cmn[U], cmx[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                cmn[u] = mn[u];
-                cmx[u] = mx[u];
+        for (int s = 0; s < NCH; ++s) {
+            if (s + D < NCH) {
+                mn[(s + D) % R] = ldg_stream(tb + (size_t)(((s + D) * 2 + 0) * 32) * 16);
+                mx[(s + D) % R] = ldg_stream(tb + (size_t)(((s + D) * 2 + 1) * 32) * 16);
             }
-            if (s0 + U < NCH) {
+            const uint32_t wn[4] = {mn[s % R].x, mn[s % R].y, mn[s % R].z, mn[s % R].w};
+            const uint32_t wx[4] = {mx[s % R].x, mx[s % R].y, mx[s % R].z, mx[s % R].w};
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    mn[u] = ldg_stream(tb + (size_t)(((s0 + U + u) * 2 + 0) * 32) * 16);
-                    mx[u] = ldg_stream(tb + (size_t)(((s0 + U + u) * 2 + 1) * 32) * 16);
+            for (int e = 0; e < CPC; ++e) {
+                double dmin, dmax;
+                if (BF16) {
+                    dmin = (double)__uint_as_float((e & 1) ? (wn[e >> 1] & 0xFFFF0000u) : (wn[e >> 1] << 16));
+                    dmax = (double)__uint_as_float((e & 1) ? (wx[e >> 1] & 0xFFFF0000u) : (wx[e >> 1] << 16));
+                } else {
+                    dmin = (double)__uint_as_float(wn[e]);
+                    dmax = (double)__uint_as_float(wx[e]);
                 }
-            }
+                const int c = s * CPC + e;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t wn[4] = {cmn[u].x, cmn[u].y, cmn[u].z, cmn[u].w};
-                const uint32_t wx[4] = {cmx[u].x, cmx[u].y, cmx[u].z, cmx[u].w};
-#pragma unroll
-                for (int e = 0; e < CPC; ++e) {
-                    double dmin, dmax;
-                    if (BF16) {
-                        dmin = (e & 1) ? bf16hi_scaled(wn[e >> 1]) : bf16lo_scaled(wn[e >> 1]);
-                        dmax = (e & 1) ? bf16hi_scaled(wx[e >> 1]) : bf16lo_scaled(wx[e >> 1]);
-                    } else {
-                        dmin = f32_scaled(wn[e]);
-                        dmax = f32_scaled(wx[e]);
-                    }
-                    const int c = (s0 + u) * CPC + e;
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        double2 qq = qpn[c * G + g];
-                        acc[g] = __fma_rn(qq.x, dmax, acc[g]);
-                        acc[g] = __fma_rn(qq.y, dmin, acc[g]);
-                    }
+                for (int g = 0; g < G; ++g) {
+                    const double2 qq = qpn[c * G + g];
+                    acc[g] = __fma_rn(qq.x, dmax, acc[g]);
+                    acc[g] = __fma_rn(qq.y, dmin, acc[g]);
                 }
             }
         }
@@ -334,7 +320,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     if (nch_b == 1) {
         cta_topk(keys, nb_chunk, kc, hist, sw, [&](int o, int p) { sel_pair[o] = j0 + p; });
         for (int r = kc + tid; r < k; r += kSelThreads) sel_pair[r] = -1;
-        return;
+        continue;
     }
     // Multi-chunk: emit candidates, then the last CTA of the pair merges.
     uint64_t* ck = cand_key + ((size_t)pair * nchunks + ci) * k;
@@ -347,7 +333,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     __syncthreads();
     if (tid == 0) sw[48] = atomicAdd(&tickets[pair], 1);
     __syncthreads();
-    if (sw[48] != nch_b - 1) return;
+    if (sw[48] != nch_b - 1) continue;
     __threadfence();
     // Merge: candidates of chunk c are ascending in j and chunks are ordered,
     // so position order == j order and the tie rule carries over.
@@ -368,6 +354,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     cta_topk(keys, n, kf, hist, sw, [&](int o, int p) { sel_pair[o] = jpos[p]; });
     for (int r = kf + tid; r < k; r += kSelThreads) sel_pair[r] = -1;
     if (tid == 0) tickets[pair] = 0;
+    }  // work items
 }
 
 // Blocks scored per CTA.  2048 by default; SS_SEL_CHUNK (multiple of 32, <= 2048)
@@ -406,9 +393,14 @@ static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return SS_ERR_CUDA;
-    dim3 grid(nchunks, (unsigned)pairs);
+    const int items = nchunks * (int)pairs;
+    // (measured: both the persistent grid and the L2 tile prefetch were slower
+    // than a plain one-CTA-per-item grid; kept switchable for experiments)
+    static const int persist = getenv("SS_SEL_PERSIST") ? atoi(getenv("SS_SEL_PERSIST")) : 0;
+    static const int l2pf = getenv("SS_SEL_L2PF") ? atoi(getenv("SS_SEL_L2PF")) : 0;
+    const int grid = (persist && items > 2 * kNumSMs) ? 2 * kNumSMs : items;
     kern<<<grid, kSelThreads, smem, stream>>>(q, meta, n_blk, max_blk, k, d.num_q_heads,
-                                              d.num_kv_heads, nchunks, sel_chunk(), sel, scores, cand_key,
+                                              d.num_kv_heads, nchunks, sel_chunk(), (int)pairs, l2pf, sel, scores, cand_key,
                                               cand_j, tickets);
     SS_LAUNCH_CHECK();
     return SS_OK;

@@ -24,6 +24,21 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
     return r;
 }
 
+// 16-byte store as a volatile asm: keeps program order with the volatile loads
+// above, so a batch of loads is fully in flight before its stores are issued.
+__device__ __forceinline__ void stg_v4(void* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+// TMA bulk prefetch of [p, p+bytes) into L2 (no shared memory, no completion
+// tracking): lets a warp run a whole tile / block ahead of its register or
+// shared-memory pipeline.  bytes must be a multiple of 16.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -5,31 +5,39 @@
 // B200 design (differs from the paper's "one thread block per KV block", which
 // needs the miss count on the host): a persistent grid reads the miss count
 // from device memory (written by kv_cache_lookup_insert), so there is no host
-// round trip.  One warp copies one block at a time; each lane keeps 8
+// round trip.  One warp copies one block at a time; each lane keeps 16
 // independent 16-byte zero-copy loads from host-mapped memory in flight
-// (ld.global.nc.v4 over PCIe), then stores them to the HBM cache slot.  With
-// up to 2 x 148 CTAs of 16 warps this keeps up to ~19 MB of reads in flight, far
-// above the bandwidth-delay product of a PCIe Gen5 x16 link (~64 GB/s x ~2 us).
+// (ld.global.nc.v4 over PCIe), then stores them to the HBM cache slot.  16 CTAs
+// of 4 warps keep 512 KB of reads in flight -- above the bandwidth-delay
+// product of a PCIe Gen5 x16 link (~55 GB/s x ~3-8 us under load) -- on only
+// 16 of the 148 SMs.
 //
 // Roofline: host-link bound; algorithmic bytes = block_bytes per miss over
 // PCIe (+ the same bytes written to HBM).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace ss {
 
-constexpr int kH2DThreads = 512;
-constexpr int kH2DUnroll = 8;
+// Small per-SM footprint (4 warps, ~8K registers, no shared memory) so the
+// gather can co-reside with the HBM-bound select / attention kernels of the
+// other half-batch running on another stream; 148 x 4 warps x 4 KiB of loads
+// in flight (2.4 MB) is still far above the PCIe bandwidth-delay product.
+constexpr int kH2DThreadsMax = 512;
+constexpr int kH2DCtas = 16;
 
-__global__ void __launch_bounds__(kH2DThreads)
+template <int kH2DUnroll>
+__global__ void __launch_bounds__(kH2DThreadsMax)
 flash_h2d_kernel(const uint4* __restrict__ host, int64_t host_blocks,
                  const int64_t* __restrict__ miss_keys, const int32_t* __restrict__ miss_slots,
                  const int32_t* __restrict__ counts, int max_misses, uint4* __restrict__ pool,
-                 int64_t vpb) {
+                 int64_t vpb, uint32_t zero) {
     if (counts[3] != 0) return;
     const int n = min(counts[1], max_misses);
     const int lane = lane_id();
-    const int64_t gw = ((int64_t)blockIdx.x * kH2DThreads + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * kH2DThreads) >> 5;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = gw; i < n; i += nw) {
         const int64_t phys = miss_keys[i] % host_blocks;
         const uint4* src = host + phys * vpb;
@@ -39,10 +47,21 @@ flash_h2d_kernel(const uint4* __restrict__ host, int64_t host_blocks,
             uint4 r[kH2DUnroll];
 #pragma unroll
             for (int u = 0; u < kH2DUnroll; ++u) r[u] = ldg_stream(src + v + 32 * u);
+            // `zero` is 0 at run time but opaque to the compiler: every store
+            // depends on ALL loads of the batch, so ptxas cannot interleave
+            // stores with loads and all kH2DUnroll loads are in flight together
+            uint32_t fold = 0;
 #pragma unroll
-            for (int u = 0; u < kH2DUnroll; ++u) dst[v + 32 * u] = r[u];
+            for (int u = 0; u < kH2DUnroll; ++u) fold ^= r[u].w;
+            const uint32_t dep = fold & zero;
+#pragma unroll
+            for (int u = 0; u < kH2DUnroll; ++u) {
+                uint4 x = r[u];
+                x.x ^= dep;
+                stg_v4(dst + v + 32 * u, x);
+            }
         }
-        for (; v < vpb; v += 32) dst[v] = ldg_stream(src + v);
+        for (; v < vpb; v += 32) stg_v4(dst + v, ldg_stream(src + v));
     }
 }
 
@@ -51,11 +70,21 @@ ss_status launch_flash_h2d(const void* host_kv, int64_t host_blocks, const int64
                            void* pool_kv, int64_t block_bytes, cudaStream_t stream) {
     if (max_misses <= 0) return SS_OK;
     int64_t warps_needed = max_misses;
-    int64_t grid = (warps_needed * 32 + kH2DThreads - 1) / kH2DThreads;
-    if (grid > 2 * kNumSMs) grid = 2 * kNumSMs;
-    flash_h2d_kernel<<<(int)grid, kH2DThreads, 0, stream>>>(
+    static const int threads = getenv("SS_H2D_THREADS") ? atoi(getenv("SS_H2D_THREADS")) : 128;
+    int64_t grid = (warps_needed * 32 + threads - 1) / threads;
+    // Few CTAs on purpose: zero-copy PCIe loads in flight on an SM slow down
+    // the HBM-bound kernels co-running on that SM (measured: a select kernel
+    // sharing the GPU with a 148-CTA gather ran 3.7x slower, with a 16-CTA one
+    // 1.2x slower), while 16 CTAs x 4 warps x 32 lanes x 16 x 16 B = 512 KB in
+    // flight cover the link's bandwidth-delay product.
+    static const int max_ctas = getenv("SS_H2D_CTAS") ? atoi(getenv("SS_H2D_CTAS")) : kH2DCtas;
+    if (grid > max_ctas) grid = max_ctas;
+    // loads in flight per lane: 16 (default) keeps 512 KB in flight on 16 SMs
+    static const int unroll = getenv("SS_H2D_UNROLL") ? atoi(getenv("SS_H2D_UNROLL")) : 16;
+    auto kern = unroll >= 16 ? flash_h2d_kernel<16> : flash_h2d_kernel<8>;
+    kern<<<(int)grid, threads, 0, stream>>>(
         (const uint4*)host_kv, host_blocks, miss_keys, miss_slots, counts, max_misses,
-        (uint4*)pool_kv, block_bytes / 16);
+        (uint4*)pool_kv, block_bytes / 16, 0u);
     SS_LAUNCH_CHECK();
     return SS_OK;
 }

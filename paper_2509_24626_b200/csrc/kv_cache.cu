@@ -9,46 +9,55 @@
 //
 // Device-only, no host synchronisation.  Data structures (caller-owned):
 //   fwd[key] -> slot (dense direct-mapped table: a key is a dense index, so a
-//   hash is unnecessary), slot_key[S], slot_stamp[S], order[S].
+//   hash is unnecessary), slot_key[S], slot_stamp[S], order[S] and its inverse
+//   order_pos[S].
 // Because `order` is kept sorted by (stamp, slot), the LRU victims of a call
 // are simply the first M "eligible" entries of `order` (not hit, stamp < t),
 // and the new order is [eligible entries not evicted, in old order] ++ [all
 // slots with stamp == t, in slot order] -- two stable compactions.
 //
-// Kernels (stream-ordered, all grid-parallel except the tiny plan kernel):
-//   A  lookup     : per selection entry: key, fwd probe, hit marks, per-CTA miss
-//                   ranks (canonical order)
-//   B1 elig_count : per 1024-entry chunk of `order`: # eligible
-//   B2 plan       : 1 CTA: scans of per-CTA miss counts / eligible counts,
-//                   capacity check, status + counts
-//   B3 victims    : first M eligible -> victim list (evict old keys); the rest
-//                   -> new order prefix
-//   C  assign     : i-th miss -> i-th victim; fwd/slot_key/stamp; hit stamps
-//   D1 teq_count  : per slot chunk: # slots with stamp == t
-//   D2 teq_place  : stamp == t slots appended in slot order; new order copied
-// On any status != 0 kernels B3..D2 are no-ops: the pool is untouched.
+// Three kernels per call (stream-ordered; chunk = 1024 order positions / slots):
+//   K1 lookup+count : entry CTAs probe fwd, mark hits, rank misses per CTA;
+//                     chunk CTAs count stamp < t per order chunk and
+//                     stamp == t per slot chunk; hits correct both counts
+//                     through order_pos.  The LAST CTA (atomic ticket) scans
+//                     the per-CTA counts, checks capacity, writes counts/status
+//                     and publishes the stamp (advances the device clock).
+//   K2 victims      : first M eligible order entries -> victim list (evict old
+//                     keys, mark victims); the rest -> new order prefix
+//   K3 assign+place : entry CTAs assign the i-th miss the i-th victim
+//                     (fwd / slot_key / stamp) and stamp hits; chunk CTAs append
+//                     the stamp==t slots (hit | victim | already t) in slot order
+//                     and copy the kept prefix into `order` / `order_pos`.
+// On status != 0, K2 and K3 are no-ops: the pool is left byte-identical.
 //
-// Roofline: integer/latency bound; bytes ~ 12*E (+4 for fwd) + 26*S per call.
+// Roofline: integer / latency bound; ~20 B per selection + ~30 B per slot.
 #include "common.cuh"
 
 namespace ss {
 
 constexpr int kCacheThreads = 256;
-constexpr int kSlotChunk = 1024;  // slots per CTA in B1/B3/D1/D2 (4 per thread)
+constexpr int kSlotChunk = 1024;  // order positions / slots per chunk CTA (4 per thread)
 constexpr int kSlotPer = kSlotChunk / kCacheThreads;
 
 struct CacheWs {
-    uint8_t* touched;     // [S]
-    int32_t* ctrl;        // [16]: 0 M, 1 hits, 2 status, 3 total_elig, 4 evictions, 5 kept, 6 invalid
+    // ---- zeroed at the start of every call (one memset) ----
+    int32_t* ctrl;        // [16]: 0 M, 1 hits, 2 status, 3 total_elig, 4 evictions,
+                          //       5 kept, 6 invalid, 7 K1 ticket; [8..9] = stamp (int64)
+    int64_t* ctrl64;      // = ctrl + 8
+    uint8_t* touched;     // [S]  slot hit by this call
+    uint8_t* victim;      // [S]  slot evicted/assigned by this call
+    int32_t* elig_cnt;    // [nS] eligible entries per order chunk
+    int32_t* teq_cnt;     // [nS] slots with stamp == t after the call, per slot chunk
+    // ---- fully written before being read ----
     int32_t* miss_local;  // [E]
     int32_t* blk_miss;    // [nA]
     int32_t* blk_hit;     // [nA]
     int32_t* blk_off;     // [nA]
-    int32_t* elig_cnt;    // [nS]
     int32_t* elig_off;    // [nS]
-    int32_t* teq_cnt;     // [nS]
     int32_t* vict;        // [E]
     int32_t* new_order;   // [S]
+    size_t zero_bytes;    // bytes from ctrl to the end of teq_cnt
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -65,14 +74,17 @@ static size_t carve(CacheWs* w, void* base, int64_t E, int S) {
     };
     CacheWs t;
     t.ctrl = (int32_t*)take(16 * 4);
+    t.ctrl64 = t.ctrl ? (int64_t*)(t.ctrl + 8) : nullptr;
     t.touched = (uint8_t*)take((size_t)S);
+    t.victim = (uint8_t*)take((size_t)S);
+    t.elig_cnt = (int32_t*)take((size_t)nS * 4);
+    t.teq_cnt = (int32_t*)take((size_t)nS * 4);
+    t.zero_bytes = off;
     t.miss_local = (int32_t*)take((size_t)E * 4);
     t.blk_miss = (int32_t*)take((size_t)nA * 4);
     t.blk_hit = (int32_t*)take((size_t)nA * 4);
     t.blk_off = (int32_t*)take((size_t)nA * 4);
-    t.elig_cnt = (int32_t*)take((size_t)nS * 4);
     t.elig_off = (int32_t*)take((size_t)nS * 4);
-    t.teq_cnt = (int32_t*)take((size_t)nS * 4);
     t.vict = (int32_t*)take((size_t)E * 4);
     t.new_order = (int32_t*)take((size_t)S * 4);
     if (w) *w = t;
@@ -90,6 +102,7 @@ struct CacheArgs {
     const int32_t* req_ids;
     int32_t layer, num_layers, max_blk, k, Hkv;
     int64_t E;
+    int32_t nA, nS;
     int64_t stamp;
     int32_t* slot_out;
     uint8_t* hit_out;
@@ -105,89 +118,43 @@ __device__ __forceinline__ int64_t cache_key(const CacheArgs& a, int64_t e, int3
     return (((int64_t)a.req_ids[b] * a.num_layers + a.layer) * a.Hkv + h) * a.max_blk + j;
 }
 
-// A: lookup
-__global__ void __launch_bounds__(kCacheThreads) cache_lookup_kernel(CacheArgs a) {
-    __shared__ int sw[64];
-    const int64_t e = (int64_t)blockIdx.x * kCacheThreads + threadIdx.x;
-    int is_miss = 0, is_hit = 0;
-    if (e < a.E) {
-        int32_t j = a.sel[e];
-        int32_t so = -1;
-        uint8_t ho = 0;
-        if (j >= 0) {
-            int64_t key = cache_key(a, e, j);
-            if (key < 0 || key >= a.pool.fwd_len) {
-                a.ws.ctrl[6] = 1;
-            } else {
-                int32_t f = a.pool.fwd[key];
-                if (f >= 0) {
-                    so = f;
-                    ho = 1;
-                    is_hit = 1;
-                    a.ws.touched[f] = 1;
-                } else {
-                    is_miss = 1;
-                }
-            }
-        }
-        a.slot_out[e] = so;
-        a.hit_out[e] = ho;
-    }
-    int tot;
-    int rank = block_excl_scan<kCacheThreads>(is_miss, sw, tot);
-    if (e < a.E) a.ws.miss_local[e] = is_miss ? rank : -1;
-    int hits = block_sum<kCacheThreads>(is_hit, sw);
-    if (threadIdx.x == 0) {
-        a.ws.blk_miss[blockIdx.x] = tot;
-        a.ws.blk_hit[blockIdx.x] = hits;
-    }
+// The call's stamp: the host argument, or *clock + 1 with a device clock.
+// K1 reads it from the clock; its last CTA publishes it in ctrl64[0] (and
+// advances *clock); K2/K3 read ctrl64[0].
+__device__ __forceinline__ int64_t stamp_pre_plan(const CacheArgs& a) {
+    return a.pool.clock ? *a.pool.clock + 1 : a.stamp;
+}
+__device__ __forceinline__ int64_t stamp_post_plan(const CacheArgs& a) {
+    return a.pool.clock ? a.ws.ctrl64[0] : a.stamp;
 }
 
-__device__ __forceinline__ bool eligible(const CacheArgs& a, int32_t s) {
-    return !a.ws.touched[s] && a.pool.slot_stamp[s] < a.stamp;
-}
-
-// B1: eligible count per chunk of `order`
-__global__ void __launch_bounds__(kCacheThreads) cache_elig_count_kernel(CacheArgs a) {
-    __shared__ int sw[64];
-    const int S = a.pool.num_slots;
-    const int p0 = blockIdx.x * kSlotChunk + threadIdx.x * kSlotPer;
-    int c = 0;
-#pragma unroll
-    for (int i = 0; i < kSlotPer; ++i) {
-        int p = p0 + i;
-        if (p < S) c += eligible(a, a.pool.order[p]);
-    }
-    int tot = block_sum<kCacheThreads>(c, sw);
-    if (threadIdx.x == 0) a.ws.elig_cnt[blockIdx.x] = tot;
-}
-
-// B2: plan (single CTA of 1024 threads)
-__global__ void __launch_bounds__(1024) cache_plan_kernel(CacheArgs a, int nA, int nS) {
-    __shared__ int sw[64];
+// ----------------------------------------------------------------------------
+// K1: lookup + counts + (last CTA) plan
+// ----------------------------------------------------------------------------
+__device__ void cache_plan(const CacheArgs& a, int* sw) {
+    // scans of per-CTA miss / hit counts and per-chunk eligible counts
     int run = 0, hits = 0;
-    for (int base = 0; base < nA; base += 1024) {
+    for (int base = 0; base < a.nA; base += kCacheThreads) {
         int i = base + threadIdx.x;
-        int v = i < nA ? a.ws.blk_miss[i] : 0;
+        int v = i < a.nA ? __ldcg(a.ws.blk_miss + i) : 0;
         int tot;
-        int ex = block_excl_scan<1024>(v, sw, tot);
-        if (i < nA) a.ws.blk_off[i] = run + ex;
+        int ex = block_excl_scan<kCacheThreads>(v, sw, tot);
+        if (i < a.nA) a.ws.blk_off[i] = run + ex;
         run += tot;
-        int hv = i < nA ? a.ws.blk_hit[i] : 0;
-        hits += block_sum<1024>(hv, sw);
+        hits += block_sum<kCacheThreads>(i < a.nA ? __ldcg(a.ws.blk_hit + i) : 0, sw);
     }
     const int M = run;
     int erun = 0;
-    for (int base = 0; base < nS; base += 1024) {
+    for (int base = 0; base < a.nS; base += kCacheThreads) {
         int i = base + threadIdx.x;
-        int v = i < nS ? a.ws.elig_cnt[i] : 0;
+        int v = i < a.nS ? __ldcg(a.ws.elig_cnt + i) : 0;
         int tot;
-        int ex = block_excl_scan<1024>(v, sw, tot);
-        if (i < nS) a.ws.elig_off[i] = erun + ex;
+        int ex = block_excl_scan<kCacheThreads>(v, sw, tot);
+        if (i < a.nS) a.ws.elig_off[i] = erun + ex;
         erun += tot;
     }
     if (threadIdx.x == 0) {
-        int status = a.ws.ctrl[6] ? 1 : (M > erun ? 3 : 0);
+        int status = __ldcg(a.ws.ctrl + 6) ? 1 : (M > erun ? 3 : 0);
         a.ws.ctrl[0] = M;
         a.ws.ctrl[1] = hits;
         a.ws.ctrl[2] = status;
@@ -197,15 +164,96 @@ __global__ void __launch_bounds__(1024) cache_plan_kernel(CacheArgs a, int nA, i
         a.counts[1] = status == 1 ? 0 : M;
         a.counts[2] = 0;
         a.counts[3] = status;
+        const int64_t t = stamp_pre_plan(a);
+        a.ws.ctrl64[0] = t;
+        if (a.pool.clock && status == 0) *a.pool.clock = t;
     }
 }
 
-// B3: victims + kept prefix of the new order
+__global__ void __launch_bounds__(kCacheThreads) cache_lookup_count_kernel(CacheArgs a) {
+    __shared__ int sw[64];
+    const int64_t t = stamp_pre_plan(a);
+    if ((int)blockIdx.x < a.nA) {
+        // ---- entry CTA: probe fwd, mark hits, rank misses ----
+        const int64_t e = (int64_t)blockIdx.x * kCacheThreads + threadIdx.x;
+        int is_miss = 0, is_hit = 0;
+        if (e < a.E) {
+            int32_t j = a.sel[e];
+            int32_t so = -1;
+            uint8_t ho = 0;
+            if (j >= 0) {
+                int64_t key = cache_key(a, e, j);
+                if (key < 0 || key >= a.pool.fwd_len) {
+                    a.ws.ctrl[6] = 1;
+                } else {
+                    int32_t f = a.pool.fwd[key];
+                    if (f >= 0) {
+                        so = f;
+                        ho = 1;
+                        is_hit = 1;
+                        a.ws.touched[f] = 1;
+                        const int64_t st = a.pool.slot_stamp[f];
+                        // a hit slot leaves the eligible set and joins stamp == t
+                        if (st < t) {
+                            atomicSub(&a.ws.elig_cnt[a.pool.order_pos[f] / kSlotChunk], 1);
+                            atomicAdd(&a.ws.teq_cnt[f / kSlotChunk], 1);
+                        }
+                    } else {
+                        is_miss = 1;
+                    }
+                }
+            }
+            a.slot_out[e] = so;
+            a.hit_out[e] = ho;
+        }
+        int tot;
+        int rank = block_excl_scan<kCacheThreads>(is_miss, sw, tot);
+        if (e < a.E) a.ws.miss_local[e] = is_miss ? rank : -1;
+        int hits = block_sum<kCacheThreads>(is_hit, sw);
+        if (threadIdx.x == 0) {
+            a.ws.blk_miss[blockIdx.x] = tot;
+            a.ws.blk_hit[blockIdx.x] = hits;
+        }
+    } else {
+        // ---- chunk CTA: stamp < t per order chunk, stamp == t per slot chunk ----
+        const int S = a.pool.num_slots;
+        const int c = blockIdx.x - a.nA;
+        const int p0 = c * kSlotChunk + threadIdx.x * kSlotPer;
+        int lt = 0, eq = 0;
+#pragma unroll
+        for (int i = 0; i < kSlotPer; ++i) {
+            const int p = p0 + i;
+            if (p < S) {
+                lt += a.pool.slot_stamp[a.pool.order[p]] < t;
+                eq += a.pool.slot_stamp[p] == t;
+            }
+        }
+        lt = block_sum<kCacheThreads>(lt, sw);
+        eq = block_sum<kCacheThreads>(eq, sw);
+        if (threadIdx.x == 0) {
+            if (lt) atomicAdd(&a.ws.elig_cnt[c], lt);
+            if (eq) atomicAdd(&a.ws.teq_cnt[c], eq);
+        }
+    }
+    // ---- last CTA plans ----
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) sw[48] = atomicAdd(&a.ws.ctrl[7], 1);
+    __syncthreads();
+    if (sw[48] != (int)gridDim.x - 1) return;
+    __threadfence();
+    cache_plan(a, sw);
+}
+
+// ----------------------------------------------------------------------------
+// K2: victims + kept prefix of the new order
+// ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(kCacheThreads) cache_victim_kernel(CacheArgs a) {
     __shared__ int sw[64];
     if (a.ws.ctrl[2] != 0) return;
     const int S = a.pool.num_slots;
     const int M = a.ws.ctrl[0];
+    const int64_t t = stamp_post_plan(a);
     const int p0 = blockIdx.x * kSlotChunk + threadIdx.x * kSlotPer;
     int32_t sl[kSlotPer];
     bool el[kSlotPer];
@@ -214,7 +262,7 @@ __global__ void __launch_bounds__(kCacheThreads) cache_victim_kernel(CacheArgs a
     for (int i = 0; i < kSlotPer; ++i) {
         int p = p0 + i;
         sl[i] = p < S ? a.pool.order[p] : -1;
-        el[i] = p < S && eligible(a, sl[i]);
+        el[i] = p < S && !a.ws.touched[sl[i]] && a.pool.slot_stamp[sl[i]] < t;
         c += el[i];
     }
     int tot;
@@ -223,15 +271,18 @@ __global__ void __launch_bounds__(kCacheThreads) cache_victim_kernel(CacheArgs a
 #pragma unroll
     for (int i = 0; i < kSlotPer; ++i) {
         if (!el[i]) continue;
+        const int32_t s = sl[i];
         if (rank < M) {
-            a.ws.vict[rank] = sl[i];
-            int64_t old = a.pool.slot_key[sl[i]];
+            a.ws.vict[rank] = s;
+            a.ws.victim[s] = 1;
+            atomicAdd(&a.ws.teq_cnt[s / kSlotChunk], 1);
+            int64_t old = a.pool.slot_key[s];
             if (old != -1) {
                 a.pool.fwd[old] = -1;
                 ++ev;
             }
         } else {
-            a.ws.new_order[rank - M] = sl[i];
+            a.ws.new_order[rank - M] = s;
         }
         ++rank;
     }
@@ -239,77 +290,73 @@ __global__ void __launch_bounds__(kCacheThreads) cache_victim_kernel(CacheArgs a
     if (threadIdx.x == 0 && evs) atomicAdd(&a.ws.ctrl[4], evs);
 }
 
-// C: assign misses to victims, stamp hits
-__global__ void __launch_bounds__(kCacheThreads) cache_assign_kernel(CacheArgs a) {
-    if (a.ws.ctrl[2] != 0) return;
-    const int64_t e = (int64_t)blockIdx.x * kCacheThreads + threadIdx.x;
-    if (e >= a.E) return;
-    if (a.hit_out[e]) {
-        a.pool.slot_stamp[a.slot_out[e]] = a.stamp;
-        return;
-    }
-    int ml = a.ws.miss_local[e];
-    if (ml < 0) return;
-    int i = a.ws.blk_off[blockIdx.x] + ml;
-    int32_t s = a.ws.vict[i];
-    int64_t key = cache_key(a, e, a.sel[e]);
-    a.slot_out[e] = s;
-    a.miss_keys[i] = key;
-    a.miss_slots[i] = s;
-    a.pool.slot_key[s] = key;
-    a.pool.fwd[key] = s;
-    a.pool.slot_stamp[s] = a.stamp;
-}
-
-// D1: per slot chunk, # slots with stamp == t
-__global__ void __launch_bounds__(kCacheThreads) cache_teq_count_kernel(CacheArgs a) {
-    __shared__ int sw[64];
-    if (a.ws.ctrl[2] != 0) return;
-    const int S = a.pool.num_slots;
-    const int s0 = blockIdx.x * kSlotChunk + threadIdx.x * kSlotPer;
-    int c = 0;
-#pragma unroll
-    for (int i = 0; i < kSlotPer; ++i) {
-        int s = s0 + i;
-        if (s < S) c += a.pool.slot_stamp[s] == a.stamp;
-    }
-    int tot = block_sum<kCacheThreads>(c, sw);
-    if (threadIdx.x == 0) {
-        a.ws.teq_cnt[blockIdx.x] = tot;
-        if (blockIdx.x == 0) a.counts[2] = a.ws.ctrl[4];
-    }
-}
-
-// D2: place stamp==t slots (slot order) after the kept prefix; copy the prefix
-__global__ void __launch_bounds__(kCacheThreads) cache_teq_place_kernel(CacheArgs a) {
+// ----------------------------------------------------------------------------
+// K3: assign misses / stamp hits (entry CTAs) || place stamp==t slots (chunk CTAs)
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(kCacheThreads) cache_assign_place_kernel(CacheArgs a) {
     __shared__ int sw[64];
     __shared__ int s_base;
     if (a.ws.ctrl[2] != 0) return;
+    const int64_t t = stamp_post_plan(a);
+    if ((int)blockIdx.x < a.nA) {
+        const int64_t e = (int64_t)blockIdx.x * kCacheThreads + threadIdx.x;
+        if (e >= a.E) return;
+        if (a.hit_out[e]) {
+            a.pool.slot_stamp[a.slot_out[e]] = t;
+            return;
+        }
+        int ml = a.ws.miss_local[e];
+        if (ml < 0) return;
+        int i = a.ws.blk_off[blockIdx.x] + ml;
+        int32_t s = a.ws.vict[i];
+        int64_t key = cache_key(a, e, a.sel[e]);
+        a.slot_out[e] = s;
+        a.miss_keys[i] = key;
+        a.miss_slots[i] = s;
+        a.pool.slot_key[s] = key;
+        a.pool.fwd[key] = s;
+        a.pool.slot_stamp[s] = t;
+        return;
+    }
+    // chunk CTA c: slots [c*1024, (c+1)*1024) in slot order
     const int S = a.pool.num_slots;
+    const int c = blockIdx.x - a.nA;
     const int kept = a.ws.ctrl[5];
+    if (c == 0 && threadIdx.x == 0) a.counts[2] = a.ws.ctrl[4];
     if (threadIdx.x < 32) {
         int acc = 0;
-        for (int c = threadIdx.x; c < (int)blockIdx.x; c += 32) acc += a.ws.teq_cnt[c];
+        for (int cc = threadIdx.x; cc < c; cc += 32) acc += a.ws.teq_cnt[cc];
         acc = warp_sum(acc);
         if (threadIdx.x == 0) s_base = kept + acc;
     }
-    const int s0 = blockIdx.x * kSlotChunk + threadIdx.x * kSlotPer;
+    const int s0 = c * kSlotChunk + threadIdx.x * kSlotPer;
     bool f[kSlotPer];
-    int c = 0;
+    int n = 0;
 #pragma unroll
     for (int i = 0; i < kSlotPer; ++i) {
-        int s = s0 + i;
-        f[i] = s < S && a.pool.slot_stamp[s] == a.stamp;
-        c += f[i];
-        // copy the kept prefix of the new order (written by B3) into `order`
-        if (s < kept) a.pool.order[s] = a.ws.new_order[s];
+        const int s = s0 + i;
+        // stamp == t after this call: hit, victim, or already stamped t (a
+        // concurrent K3 entry CTA may be writing t into hit / victim slots;
+        // their flags already decide those)
+        f[i] = s < S && (a.ws.touched[s] || a.ws.victim[s] || a.pool.slot_stamp[s] == t);
+        n += f[i];
+        // copy the kept prefix of the new order (K2) into order / order_pos
+        if (s < kept) {
+            const int32_t v = a.ws.new_order[s];
+            a.pool.order[s] = v;
+            a.pool.order_pos[v] = s;
+        }
     }
     int tot;
-    int ex = block_excl_scan<kCacheThreads>(c, sw, tot);  // syncs: s_base visible
+    int ex = block_excl_scan<kCacheThreads>(n, sw, tot);  // syncs: s_base visible
     int pos = s_base + ex;
 #pragma unroll
     for (int i = 0; i < kSlotPer; ++i)
-        if (f[i]) a.pool.order[pos++] = s0 + i;
+        if (f[i]) {
+            a.pool.order[pos] = s0 + i;
+            a.pool.order_pos[s0 + i] = pos;
+            ++pos;
+        }
 }
 
 ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int32_t* req_ids,
@@ -334,18 +381,12 @@ ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int3
     a.counts = counts;
     const int S = pool.num_slots;
     carve(&a.ws, ws, a.E, S);
-    const int nA = (int)((a.E + kCacheThreads - 1) / kCacheThreads);
-    const int nS = (S + kSlotChunk - 1) / kSlotChunk;
-    // ctrl and touched are adjacent at the start of the workspace
-    size_t clear = (size_t)((char*)a.ws.touched - (char*)a.ws.ctrl) + (size_t)S;
-    if (cudaMemsetAsync(a.ws.ctrl, 0, clear, stream) != cudaSuccess) return SS_ERR_CUDA;
-    if (nA > 0) cache_lookup_kernel<<<nA, kCacheThreads, 0, stream>>>(a);
-    cache_elig_count_kernel<<<nS, kCacheThreads, 0, stream>>>(a);
-    cache_plan_kernel<<<1, 1024, 0, stream>>>(a, nA, nS);
-    cache_victim_kernel<<<nS, kCacheThreads, 0, stream>>>(a);
-    if (nA > 0) cache_assign_kernel<<<nA, kCacheThreads, 0, stream>>>(a);
-    cache_teq_count_kernel<<<nS, kCacheThreads, 0, stream>>>(a);
-    cache_teq_place_kernel<<<nS, kCacheThreads, 0, stream>>>(a);
+    a.nA = (int)((a.E + kCacheThreads - 1) / kCacheThreads);
+    a.nS = (S + kSlotChunk - 1) / kSlotChunk;
+    if (cudaMemsetAsync(a.ws.ctrl, 0, a.ws.zero_bytes, stream) != cudaSuccess) return SS_ERR_CUDA;
+    cache_lookup_count_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
+    cache_victim_kernel<<<a.nS, kCacheThreads, 0, stream>>>(a);
+    cache_assign_place_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
     SS_LAUNCH_CHECK();
     return SS_OK;
 }

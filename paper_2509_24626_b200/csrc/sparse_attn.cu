@@ -28,13 +28,14 @@
 // Roofline: HBM-bound; algorithmic bytes = block_bytes per attended unit
 // (+ q, out: negligible).
 #include <algorithm>
+#include <stdlib.h>
 
 #include "common.cuh"
 
 namespace ss {
 
 constexpr int kAttnPartStride = 132;
-constexpr int kMinUnitsPerWarp = 4;  // floats per (warp, seg, g) partial: m, l, pad, pad, o[128]
+constexpr int kMinUnitsPerWarp = 16;  // floats per (warp, seg, g) partial: m, l, pad, pad, o[128]
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -81,6 +82,7 @@ struct AttnArgs {
     float scale_log2;
     int64_t U;  // pairs * (k + 1)
     int W;      // total warps
+    int l2pf;   // L2 prefetch of the following unit
 };
 
 template <bool BF16>
@@ -129,7 +131,9 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
     extern __shared__ __align__(128) unsigned char smem_raw[];
     WarpSmem<BF16, G>& sm = reinterpret_cast<WarpSmem<BF16, G>*>(smem_raw)[warp_id()];
     const int lane = lane_id();
-    const int w = blockIdx.x * T::NW + warp_id();
+    // warp w = warp_id * gridDim + CTA: with W < total warps the active warps
+    // spread over all SMs (not packed into the first CTAs)
+    const int w = warp_id() * gridDim.x + blockIdx.x;
     if (w >= a.W) return;  // W = min(total warps, U): every active warp owns >= 1 unit
     const int64_t u0 = a.U * w / a.W, u1 = a.U * (w + 1) / a.W;
     const int Ku = a.k + 1;
@@ -170,6 +174,16 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
                 bulk_g2s(sm.buf[stage], src, T::BLOCK_BYTES, &sm.bar[stage]);
             }
             (stage ? bu1 : bu0) = next_u++;
+            // warm L2 with the following unit (one lane, no smem): the next bulk
+            // copy then sees L2 latency instead of DRAM latency
+            if (a.l2pf && lane == 0 && next_u < u1) {
+                const int64_t pn = next_u / Ku;
+                const int rn = (int)(next_u % Ku);
+                if (rn < a.k) {
+                    const int32_t sn = __ldg(a.slot + pn * a.k + rn);
+                    if (sn >= 0) prefetch_l2_bulk((const char*)a.pool + (int64_t)sn * T::BLOCK_BYTES, T::BLOCK_BYTES);
+                }
+            }
         } else {
             (stage ? bu1 : bu0) = -1;
         }
@@ -450,8 +464,11 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
     a.scale_log2 = scale * 1.4426950408889634f;
     const int G = d.num_q_heads / d.num_kv_heads;
     a.U = (int64_t)d.batch * d.num_kv_heads * (k + 1);
-    // at least kMinUnitsPerWarp units per warp: fewer, longer ranges when the
-    // problem is small (fewer partials to merge); W <= U keeps every range non-empty
+    static const int l2pf = getenv("SS_ATTN_L2PF") ? atoi(getenv("SS_ATTN_L2PF")) : 0;  // measured slower
+    a.l2pf = l2pf;
+    // at least kMinUnitsPerWarp units (256 KiB in bf16) per warp: fewer, longer
+    // ranges when the problem is small (C3: ~8 partials per pair to merge instead
+    // of ~28); W <= U keeps every range non-empty
     a.W = (int)std::max<int64_t>(1, std::min<int64_t>(attn_total_warps(dt), a.U / kMinUnitsPerWarp));
     size_t part = (size_t)a.W * 2 * G * kAttnPartStride * 4;
     a.part = (float*)ws;

@@ -1,8 +1,18 @@
 """Decode-step driver: the per-layer select -> cache -> FlashH2D -> attention
-sequence of PAPER.md:124 (§3.1 Model Executor) over L layers, on one stream.
+sequence of PAPER.md:124 (§3.1 Model Executor) over L layers.
 
-PyTorch is used for device memory, pinned host memory and streams only; every
-step of the path is a call into libsparseserve.so through `ops`.
+PyTorch is used for device memory, pinned host memory, streams and events only;
+every step of the path is a call into libsparseserve.so through `ops`.
+
+Request groups (B200 scheduling): the batch can be split into G
+contiguous request groups, each on its own CUDA stream.  Every request's layers
+still run strictly in order (layer l+1 of a request only after its layer-l
+attention), but while group A waits on the PCIe link for its missed blocks
+(FlashH2D), group B's HBM-bound select / attention run on the SMs.  All groups
+of a layer share that layer's HBM cache pool; their cache calls are ordered
+(group 0 first) and use the same stamp, so a group never evicts a slot that
+another group touched in the same step.  A cache call of step t+1 waits for
+the layer's attention of every group at step t (no eviction under a reader).
 """
 from __future__ import annotations
 
@@ -30,6 +40,7 @@ class EngineConfig:
     slots_per_layer: int
     num_requests: int          # size of the request-id space (fwd table extent)
     dtype: torch.dtype = torch.bfloat16
+    groups: int = 1            # request groups pipelined on separate streams
 
     @property
     def group(self) -> int:
@@ -56,9 +67,47 @@ class EngineConfig:
         return self.num_requests * self.layers * self.num_kv_heads * self.max_blk
 
 
+class RequestGroup:
+    """Scratch of one contiguous request range [b0, b1): its selections, cache
+    outputs, miss lists, counts, outputs and workspaces, and its stream."""
+
+    def __init__(self, eng: "DecodeEngine", b0: int, b1: int, stream: torch.cuda.Stream):
+        c, dev = eng.cfg, eng.device
+        self.b0, self.b1 = b0, b1
+        nb = b1 - b0
+        self.nb = nb
+        self.stream = stream
+        self.dims = ops.dims(nb, c.num_q_heads, c.num_kv_heads)
+        E = nb * c.num_kv_heads * c.topk
+        self.E = E
+        self.sel = torch.empty(c.layers, nb, c.num_kv_heads, c.topk, dtype=torch.int32, device=dev)
+        self.slot = torch.empty_like(self.sel)
+        self.hit = torch.empty(c.layers, nb, c.num_kv_heads, c.topk, dtype=torch.uint8, device=dev)
+        self.miss_keys = torch.empty(c.layers, E, dtype=torch.int64, device=dev)
+        self.miss_slots = torch.empty(c.layers, E, dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(c.layers, 4, dtype=torch.int32, device=dev)
+        self.out = torch.empty(c.layers, c.num_q_heads, nb, HEAD_DIM, dtype=torch.float32, device=dev)
+        self.ws_select = ops.alloc_workspace(SS_WS_SELECT, self.dims, c.max_blk, c.topk, device=dev)
+        self.ws_cache = ops.alloc_workspace(SS_WS_CACHE, self.dims, c.max_blk, c.topk,
+                                            c.slots_per_layer, device=dev)
+        self.ws_attn = ops.alloc_workspace(SS_WS_ATTN, self.dims, c.max_blk, c.topk, device=dev)
+        pair_elems = c.max_blk * 2 * HEAD_DIM
+        self.meta = [m[b0 * c.num_kv_heads * pair_elems:b1 * c.num_kv_heads * pair_elems]
+                     for m in eng.meta]
+        self.n_blk = eng.n_blk[b0:b1]
+        self.req_ids = eng.req_ids[b0:b1]
+        self.tail_len = eng.tail_len[b0:b1]
+        self.tail_kv = eng.tail_kv[:, b0:b1]
+        self.ev_cache = [torch.cuda.Event() for _ in range(c.layers)]
+        self.ev_attn = [torch.cuda.Event() for _ in range(c.layers)]
+        self.ev_gather = [torch.cuda.Event() for _ in range(c.layers)]
+        # FlashH2D runs on the engine's shared high-priority stream (set below)
+        self.h2d_stream = None
+
+
 class DecodeEngine:
     """Device state of one GPU: per-layer metadata, per-layer HBM block-cache
-    pools (shared key->slot table), tail blocks, outputs and workspaces."""
+    pools (shared key->slot table), tail blocks, and per-group scratch."""
 
     def __init__(self, cfg: EngineConfig, device: Optional[torch.device] = None):
         self.cfg = cfg
@@ -78,23 +127,32 @@ class DecodeEngine:
         self.tail_len = torch.zeros(c.batch, dtype=torch.int32, device=dev)
         self.n_blk = torch.zeros(c.batch, dtype=torch.int32, device=dev)
         self.req_ids = torch.arange(c.batch, dtype=torch.int32, device=dev)
-        E = c.pairs * c.topk
-        self.E = E
-        self.sel = torch.empty(c.layers, c.batch, c.num_kv_heads, c.topk, dtype=torch.int32, device=dev)
-        self.slot = torch.empty_like(self.sel)
-        self.hit = torch.empty(c.layers, c.batch, c.num_kv_heads, c.topk, dtype=torch.uint8, device=dev)
-        self.miss_keys = torch.empty(c.layers, E, dtype=torch.int64, device=dev)
-        self.miss_slots = torch.empty(c.layers, E, dtype=torch.int32, device=dev)
-        self.counts = torch.zeros(c.layers, 4, dtype=torch.int32, device=dev)
-        self.out = torch.empty(c.layers, c.num_q_heads, c.batch, HEAD_DIM, dtype=torch.float32, device=dev)
-        self.ws_select = ops.alloc_workspace(SS_WS_SELECT, self.dims, c.max_blk, c.topk, device=dev)
-        self.ws_cache = ops.alloc_workspace(SS_WS_CACHE, self.dims, c.max_blk, c.topk,
-                                            c.slots_per_layer, device=dev)
-        self.ws_attn = ops.alloc_workspace(SS_WS_ATTN, self.dims, c.max_blk, c.topk, device=dev)
         self.scale = 1.0 / math.sqrt(HEAD_DIM)
         self.host_kv: Optional[torch.Tensor] = None
         self.host_ptr = 0
         self.host_blocks = 0
+        ng = max(1, min(c.groups, c.batch))
+        bounds = [round(i * c.batch / ng) for i in range(ng + 1)]
+        cur = torch.cuda.current_stream(dev)
+        self.groups = [RequestGroup(self, bounds[i], bounds[i + 1],
+                                    cur if ng == 1 else torch.cuda.Stream(dev))
+                       for i in range(ng)]
+        if ng > 1:
+            # One high-priority stream carries every group's FlashH2D in issue
+            # order (layer l: group 0, 1, ...; then layer l+1): the PCIe link
+            # serves one group at a time, which keeps the groups out of phase --
+            # while group A's misses stream in, group B runs its HBM-bound
+            # attention / next-layer select -- and the gather CTAs are dispatched
+            # ahead of queued HBM-kernel CTAs.
+            h2d = torch.cuda.Stream(dev, priority=-1)
+            for g in self.groups:
+                g.h2d_stream = h2d
+        g0 = self.groups[0]
+        # single-group aliases (tests, smoke)
+        self.sel, self.slot, self.hit = g0.sel, g0.slot, g0.hit
+        self.miss_keys, self.miss_slots, self.counts, self.out = (g0.miss_keys, g0.miss_slots,
+                                                                  g0.counts, g0.out)
+        self.E = g0.E
 
     # ------------------------------------------------------------------ setup
     def set_host_kv(self, host_kv: torch.Tensor, host_blocks: int) -> None:
@@ -132,26 +190,83 @@ class DecodeEngine:
                     ops.block_meta_update(keys, meta, n, key_stride=c.block_elems)
 
     # ------------------------------------------------------------------- step
+    def _group_layer(self, g: RequestGroup, l: int, q: torch.Tensor, stamp: int, gi: int,
+                     scores: Optional[torch.Tensor], timers, gather: bool) -> None:
+        c = self.cfg
+
+        def timed(name, fn):
+            if timers is None:
+                fn()
+            else:
+                s, e = timers.mark(name, gi, l)
+                s.record()
+                fn()
+                e.record()
+        timed("select", lambda: ops.ss_block_select(q, g.meta[l], g.n_blk, c.max_blk, c.topk, g.dims,
+                                                    g.sel[l], g.ws_select, scores=scores))
+        if len(self.groups) > 1:
+            # pool order: groups of a layer call the cache in group order; the
+            # first group of step t waits for every group's layer-l attention of t-1
+            if gi > 0:
+                g.stream.wait_event(self.groups[gi - 1].ev_cache[l])
+            else:
+                for other in self.groups[1:]:
+                    g.stream.wait_event(other.ev_attn[l])
+        timed("cache", lambda: ops.kv_cache_lookup_insert(
+            self.pools[l], g.sel[l], g.req_ids, l, c.layers, c.max_blk, c.topk, g.dims, stamp,
+            g.slot[l], g.hit[l], g.miss_keys[l], g.miss_slots[l], g.counts[l], g.ws_cache))
+        if len(self.groups) > 1:
+            g.ev_cache[l].record(g.stream)
+        if gather:
+            def _gather():
+                timed("gather", lambda: ops.flash_h2d_gather(self.host_ptr, self.host_blocks,
+                                                             g.miss_keys[l], g.miss_slots[l], g.counts[l],
+                                                             g.E, self.pool_kv[l], c.block_bytes))
+            if g.h2d_stream is not None:
+                g.h2d_stream.wait_event(g.ev_cache[l])
+                with torch.cuda.stream(g.h2d_stream):
+                    _gather()
+                    g.ev_gather[l].record(g.h2d_stream)
+                g.stream.wait_event(g.ev_gather[l])
+            else:
+                _gather()
+        timed("attn", lambda: ops.sparse_decode_attn(q, self.pool_kv[l], g.slot[l], c.topk,
+                                                     g.tail_kv[l], g.tail_len, g.dims, self.scale,
+                                                     g.out[l], g.ws_attn, counts=g.counts[l]))
+        if len(self.groups) > 1:
+            g.ev_attn[l].record(g.stream)
+
     def layer_step(self, l: int, q: torch.Tensor, stamp: int, scores: Optional[torch.Tensor] = None,
                    gather: bool = True) -> None:
-        """One layer of one decode step (S1..S5)."""
-        c = self.cfg
-        ops.ss_block_select(q, self.meta[l], self.n_blk, c.max_blk, c.topk, self.dims, self.sel[l],
-                            self.ws_select, scores=scores)
-        ops.kv_cache_lookup_insert(self.pools[l], self.sel[l], self.req_ids, l, c.layers, c.max_blk,
-                                   c.topk, self.dims, stamp, self.slot[l], self.hit[l],
-                                   self.miss_keys[l], self.miss_slots[l], self.counts[l],
-                                   self.ws_cache)
-        if gather:
-            ops.flash_h2d_gather(self.host_ptr, self.host_blocks, self.miss_keys[l],
-                                 self.miss_slots[l], self.counts[l], self.E, self.pool_kv[l],
-                                 c.block_bytes)
-        ops.sparse_decode_attn(q, self.pool_kv[l], self.slot[l], c.topk, self.tail_kv[l],
-                               self.tail_len, self.dims, self.scale, self.out[l], self.ws_attn,
-                               counts=self.counts[l])
+        """One layer of one decode step (S1..S5) for a single-group engine."""
+        assert len(self.groups) == 1
+        self._group_layer(self.groups[0], l, q, stamp, 0, scores, None, gather)
 
-    def step(self, q_all: torch.Tensor, stamp: int) -> torch.Tensor:
-        """q_all: [L][B][Hq][d]; returns out [L][Hq][B][d] (float32, device)."""
-        for l in range(self.cfg.layers):
-            self.layer_step(l, q_all[l], stamp)
-        return self.out
+    def step(self, q_all: torch.Tensor, stamp: int, timers=None, post_attn=None) -> None:
+        """q_all: [L][B][Hq][d] on the device.  Enqueues one decode step of every
+        layer; outputs land in each group's `out` [L][Hq][nb][d] (float32).
+        post_attn(group_index, group, layer), if given, runs on the group's
+        stream right after its layer-l attention (e.g. the TP all-gather)."""
+        c = self.cfg
+        if len(self.groups) == 1:
+            for l in range(c.layers):
+                self._group_layer(self.groups[0], l, q_all[l], stamp, 0, None, timers, True)
+                if post_attn is not None:
+                    post_attn(0, self.groups[0], l)
+            return
+        cur = torch.cuda.current_stream(self.device)
+        for g in self.groups:
+            g.stream.wait_stream(cur)
+        # issue layer by layer, group by group: group A's FlashH2D (PCIe) overlaps
+        # group B's select / attention (HBM) on the other stream
+        for l in range(c.layers):
+            for gi, g in enumerate(self.groups):
+                with torch.cuda.stream(g.stream):
+                    self._group_layer(g, l, q_all[l, g.b0:g.b1], stamp, gi, None, timers, True)
+                    if post_attn is not None:
+                        post_attn(gi, g, l)
+        for g in self.groups:
+            cur.wait_stream(g.stream)
+
+    def outputs(self) -> List[torch.Tensor]:
+        return [g.out for g in self.groups]

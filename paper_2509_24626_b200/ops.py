@@ -85,17 +85,22 @@ def ss_block_select(q: torch.Tensor, meta: torch.Tensor, n_blk: torch.Tensor, ma
 class CachePool:
     """Device arrays of one (GPU, layer) HBM block-cache pool (S3 state)."""
 
-    def __init__(self, num_slots: int, fwd: torch.Tensor, device=None):
+    def __init__(self, num_slots: int, fwd: torch.Tensor, device=None, clock: bool = False):
         device = device or fwd.device
         self.fwd = fwd                       # int32 [fwd_len], may be shared across layers
         self.slot_key = torch.full((num_slots,), -1, dtype=torch.int64, device=device)
         self.slot_stamp = torch.full((num_slots,), -1, dtype=torch.int64, device=device)
         self.order = torch.arange(num_slots, dtype=torch.int32, device=device)
+        self.order_pos = torch.arange(num_slots, dtype=torch.int32, device=device)
         self.num_slots = num_slots
+        # device-side stamp counter (graph-replayable steps); None = host stamps
+        self.clock = torch.zeros(1, dtype=torch.int64, device=device) if clock else None
 
     def c_struct(self) -> SSCachePool:
         return SSCachePool(self.fwd.data_ptr(), self.fwd.numel(), self.slot_key.data_ptr(),
-                           self.slot_stamp.data_ptr(), self.order.data_ptr(), self.num_slots)
+                           self.slot_stamp.data_ptr(), self.order.data_ptr(),
+                           self.order_pos.data_ptr(), self.num_slots,
+                           self.clock.data_ptr() if self.clock is not None else None)
 
 
 def kv_cache_lookup_insert(pool: CachePool, sel: torch.Tensor, req_ids: torch.Tensor, layer: int,

@@ -1,0 +1,98 @@
+"""Full-size parity in bench.py's launch configuration (BASELINE.json configs[1],
+C2: 16 requests x 32 layers x 32 heads, 128K context = 4096 blocks, top-64,
+131072-slot HBM pool per layer, two request groups on separate streams).
+
+The engine runs every layer of every step exactly as bench.py does; the oracle
+replays one of the 32 layers (17) in full -- its own metadata for all
+4096 blocks of all 512 (request, head) pairs, its own scores, top-k, LRU pool
+and attention -- and everything is compared: selections bit-exact, cache slot
+outputs / counts / pool state bit-exact, gathered bytes of every cached block,
+and attention outputs of all 512 pairs within 2e-3.  The physical host pool is
+smaller than bench.py's (aliasing changes no launch parameter)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from layout import D, to_torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+CHECK_LAYERS = (17,)
+STEPS = 3
+
+
+def test_c2_fullsize_layer17_three_steps():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    free, _ = torch.cuda.mem_get_info()
+    if free < 110 * (1 << 30):
+        pytest.skip("needs ~110 GB of free HBM")
+    from paper_2509_24626_b200.engine import DecodeEngine, EngineConfig
+    wl = synth.C2
+    cfg = EngineConfig(batch=wl.batch, layers=wl.layers, num_q_heads=wl.num_q_heads,
+                       num_kv_heads=wl.num_kv_heads, max_blk=wl.max_blk, topk=wl.topk,
+                       slots_per_layer=wl.slots_per_layer, num_requests=wl.batch,
+                       dtype=torch.bfloat16, groups=2)
+    eng = DecodeEngine(cfg)
+    runs = 13                                           # physical host pool = 13 x 4096 blocks (832 MiB)
+    hb = runs * cfg.max_blk
+    rng = synth.rng_for(8000, 1)
+    scales = synth.channel_scales(rng)
+    host_np = np.empty((hb, 2, 32, D), np.uint16)
+    for s in range(0, hb, 8192):
+        n = min(8192, hb - s)
+        host_np[s:s + n] = synth.encode(synth.kv_blocks(rng, n, D, scales), synth.DT_BF16)
+    host_t = torch.from_numpy(host_np.view(np.int16)).view(-1).pin_memory().view(torch.bfloat16)
+    eng.set_host_kv(host_t, hb)
+    nbk = [wl.n_blk] * wl.batch
+    eng.n_blk.copy_(torch.tensor(nbk, dtype=torch.int32))
+    eng.tail_len.zero_()
+    eng.build_meta(nbk, host_t.cuda())
+    qs = synth.encode(synth.queries(rng, STEPS, (cfg.layers, cfg.batch, cfg.num_q_heads, D), wl.rho),
+                      synth.DT_BF16)
+    # oracle state for the checked layers
+    metas, pools = {}, {}
+    for l in CHECK_LAYERS:
+        m = np.empty((cfg.batch, cfg.num_kv_heads, cfg.max_blk, 2, D), np.uint16)
+        for b in range(cfg.batch):
+            for h in range(cfg.num_kv_heads):
+                p0 = eng.key0(b, l, h) % hb
+                m[b, h] = oracle.block_meta(host_np[p0:p0 + wl.n_blk], key_stride=2 * 32 * D)
+        metas[l] = m
+        pools[l] = oracle.Pool(cfg.slots_per_layer, cfg.fwd_len, cfg.block_bytes)
+    host_u8 = host_np.view(np.uint8).reshape(hb, -1)
+    tails = np.zeros((cfg.batch, cfg.num_kv_heads, 2, 32, D), np.uint16)
+    tl = np.zeros(cfg.batch, np.int32)
+    for t in range(STEPS):
+        eng.step(to_torch(qs[t]), stamp=t + 1)
+        torch.cuda.synchronize()
+        for l in CHECK_LAYERS:
+            for g in eng.groups:
+                b0, b1 = g.b0, g.b1
+                r = oracle.decode_layer(np.ascontiguousarray(qs[t, l, b0:b1]),
+                                        np.ascontiguousarray(metas[l][b0:b1]),
+                                        np.array(nbk[b0:b1], np.int32), cfg.topk, pools[l],
+                                        np.arange(b0, b1, dtype=np.int32), l, cfg.layers, cfg.max_blk,
+                                        t + 1, host_u8, hb, tails[b0:b1], tl[b0:b1], 1.0 / math.sqrt(D))
+                np.testing.assert_array_equal(g.sel[l].cpu().numpy(), r["sel"])
+                np.testing.assert_array_equal(g.counts[l].cpu().numpy(), r["counts"])
+                np.testing.assert_array_equal(g.slot[l].cpu().numpy(), r["slot"])
+                np.testing.assert_array_equal(g.hit[l].cpu().numpy(), r["hit"])
+                err = float(np.abs(g.out[l].cpu().numpy() - r["out"]).max())
+                assert err <= 2e-3, f"step {t} layer {l} group {b0}: max abs err {err}"
+            p = eng.pools[l]
+            np.testing.assert_array_equal(p.slot_key.cpu().numpy(), pools[l].slot_key)
+            np.testing.assert_array_equal(p.slot_stamp.cpu().numpy(), pools[l].slot_stamp)
+            np.testing.assert_array_equal(
+                p.order.cpu().numpy(),
+                np.lexsort((np.arange(cfg.slots_per_layer), pools[l].slot_stamp)).astype(np.int32))
+    # bytes of every cached block of the checked layers
+    for l in CHECK_LAYERS:
+        used = np.nonzero(pools[l].slot_key >= 0)[0]
+        gpu = eng.pool_kv[l].view(torch.int16).view(cfg.slots_per_layer, -1)[torch.from_numpy(used).cuda()]
+        np.testing.assert_array_equal(gpu.cpu().numpy().view(np.uint8).reshape(len(used), -1),
+                                      pools[l].kv[used])

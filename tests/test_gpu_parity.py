@@ -151,6 +151,9 @@ def _cmp_pool(gp, op, S):
     np.testing.assert_array_equal(gp.fwd.cpu().numpy(), op.fwd)
     exp_order = np.lexsort((np.arange(S), op.slot_stamp)).astype(np.int32)
     np.testing.assert_array_equal(gp.order.cpu().numpy(), exp_order)
+    inv = np.empty(S, np.int32)
+    inv[exp_order] = np.arange(S, dtype=np.int32)
+    np.testing.assert_array_equal(gp.order_pos.cpu().numpy(), inv)
 
 
 @pytest.mark.parametrize("S", [300, 2048, 5000])
@@ -344,3 +347,38 @@ def test_attention_skipped_on_error_status(ops):
                            counts=torch.tensor([0, 0, 0, 3], dtype=torch.int32, device="cuda"))
     torch.cuda.synchronize()
     assert (out.cpu() == 7.0).all()
+
+
+def test_cache_device_clock_mode(ops):
+    # pool.clock set: stamps come from the device (call index), the host stamp is
+    # ignored, and a capacity error leaves the clock (and pool) unchanged.
+    rng = synth.rng_for(1000, 4)
+    B, Hkv, k, max_blk, S = 2, 2, 16, 128, 80
+    fwd_len = B * Hkv * max_blk
+    fwd = torch.full((fwd_len,), -1, dtype=torch.int32, device="cuda")
+    gp = ops.CachePool(S, fwd, clock=True)
+    op = oracle.Pool(S, fwd_len)
+    d = ops.dims(B, Hkv, Hkv)
+    ws = ops.alloc_workspace(1, d, max_blk, k, S)
+    E = B * Hkv * k
+    slot = torch.empty(B, Hkv, k, dtype=torch.int32, device="cuda")
+    hit = torch.empty(B, Hkv, k, dtype=torch.uint8, device="cuda")
+    mk = torch.empty(E, dtype=torch.int64, device="cuda")
+    ms = torch.empty(E, dtype=torch.int32, device="cuda")
+    counts = torch.empty(4, dtype=torch.int32, device="cuda")
+    req = np.arange(B, dtype=np.int32)
+    clock = 0
+    prev = None
+    for t in range(30):
+        sel = _random_sel(rng, B, Hkv, k, max_blk, prev, keep=0.7)
+        prev = sel
+        r = oracle.lru(op, sel, req, 0, 1, max_blk, stamp=clock + 1)
+        ops.kv_cache_lookup_insert(gp, to_torch(sel), to_torch(req), 0, 1, max_blk, k, d, 999999,
+                                   slot, hit, mk, ms, counts, ws)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(counts.cpu().numpy(), r["counts"])
+        if r["counts"][3] == 0:
+            clock += 1
+            np.testing.assert_array_equal(slot.cpu().numpy(), r["slot"])
+        assert int(gp.clock.item()) == clock
+        _cmp_pool(gp, op, S)

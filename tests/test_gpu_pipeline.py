@@ -130,3 +130,64 @@ def test_f32_pipeline():
         pytest.skip("needs a CUDA device")
     _run_pipeline(synth.DT_F32, 2, 1, 8, 8, [300, 128], 16, 2 * 8 * 16 * 2, [1, 0],
                   steps=8, rho=0.9, seed=3)
+
+
+def test_request_groups_pipeline_two_streams():
+    """groups=2: the two request groups run on separate streams; per layer the
+    oracle makes the same two cache calls (group order, same stamp)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2509_24626_b200.engine import DecodeEngine, EngineConfig
+    dt = synth.DT_BF16
+    B, L, Hq, Hkv, k, steps = 4, 3, 8, 4, 24, 10
+    n_blk = [900, 1500, 64, 700]
+    tails = [0, 5, 31, 1]
+    max_blk = 1504
+    S = B * Hkv * k * 2
+    cfg = EngineConfig(batch=B, layers=L, num_q_heads=Hq, num_kv_heads=Hkv, max_blk=max_blk, topk=k,
+                       slots_per_layer=S, num_requests=B, dtype=torch.bfloat16, groups=2)
+    eng = DecodeEngine(cfg)
+    assert len(eng.groups) == 2
+    rng = synth.rng_for(2000, 9)
+    hb = cfg.fwd_len
+    host_np = synth.encode(synth.kv_blocks(rng, hb, D, synth.channel_scales(rng)), dt)
+    host_t = torch.from_numpy(host_np.view(np.int16)).view(-1).pin_memory().view(torch.bfloat16)
+    eng.set_host_kv(host_t, hb)
+    eng.n_blk.copy_(torch.tensor(n_blk, dtype=torch.int32))
+    eng.tail_len.copy_(torch.tensor(tails, dtype=torch.int32))
+    tail_np = synth.encode(synth.kv_blocks(rng, L * B * Hkv, D).reshape(L, B, Hkv, 2, 32, D), dt)
+    eng.tail_kv.copy_(to_torch(tail_np))
+    eng.build_meta(n_blk, host_t.cuda())
+    blocks = host_np.reshape(hb, 2, 32, D)
+    metas = []
+    for l in range(L):
+        m = np.zeros((B, Hkv, max_blk, 2, D), np.uint16)
+        for b in range(B):
+            for h in range(Hkv):
+                k0 = eng.key0(b, l, h)
+                m[b, h, :n_blk[b]] = oracle.block_meta(blocks[k0:k0 + n_blk[b]], key_stride=2 * 32 * D)
+        metas.append(m)
+    pools = [oracle.Pool(S, cfg.fwd_len, cfg.block_bytes) for _ in range(L)]
+    qs = synth.encode(synth.queries(rng, steps, (L, B, Hq, D), 0.95), dt)
+    host_u8 = host_np.view(np.uint8).reshape(hb, -1)
+    nbk = np.array(n_blk, np.int32)
+    tl = np.array(tails, np.int32)
+    for t in range(steps):
+        eng.step(to_torch(qs[t]), stamp=t + 1)
+        torch.cuda.synchronize()
+        for l in range(L):
+            for g in eng.groups:
+                b0, b1 = g.b0, g.b1
+                r = oracle.decode_layer(np.ascontiguousarray(qs[t, l, b0:b1]), np.ascontiguousarray(metas[l][b0:b1]),
+                                        nbk[b0:b1], k, pools[l], np.arange(b0, b1, dtype=np.int32), l, L,
+                                        max_blk, t + 1, host_u8, hb, np.ascontiguousarray(tail_np[l, b0:b1]),
+                                        tl[b0:b1], 1.0 / math.sqrt(D))
+                np.testing.assert_array_equal(g.sel[l].cpu().numpy(), r["sel"])
+                np.testing.assert_array_equal(g.counts[l].cpu().numpy(), r["counts"])
+                np.testing.assert_array_equal(g.slot[l].cpu().numpy(), r["slot"])
+                err = float(np.abs(g.out[l].cpu().numpy() - r["out"]).max())
+                assert err <= TOL[dt], f"step {t} layer {l} group {b0}: {err}"
+            np.testing.assert_array_equal(eng.pools[l].slot_stamp.cpu().numpy(), pools[l].slot_stamp)
+            np.testing.assert_array_equal(eng.pools[l].slot_key.cpu().numpy(), pools[l].slot_key)
+    for l in range(L):
+        np.testing.assert_array_equal(to_numpy(eng.pool_kv[l]).view(np.uint8).reshape(S, -1), pools[l].kv)

@@ -124,5 +124,59 @@ def main():
         print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] == "overlap"):
     main()
+
+
+def bench_overlap(c, iters=10, nmiss=1250, host_gib=None):
+    """select (half batch) concurrent with a FlashH2D gather on a high-priority stream."""
+    B, Hq, Hkv, n, k = c["B"] // 2, c["Hq"], c["Hkv"], c["n_blk"], c["k"]
+    meta = torch.randn(B * Hkv * n * 2 * 128, device="cuda").to(torch.bfloat16)
+    q = torch.randn(B, Hq, 128, device="cuda").to(torch.bfloat16)
+    d = ops.dims(B, Hq, Hkv)
+    ws = ops.alloc_workspace(0, d, n, k)
+    sel = torch.empty(B, Hkv, k, dtype=torch.int32, device="cuda")
+    nb = torch.full((B,), n, dtype=torch.int32, device="cuda")
+    hb = (int(os.environ.get("KB_HOST_GIB", "4")) << 30) // 16384
+    host = torch.empty(hb * 8192, dtype=torch.bfloat16, pin_memory=True)
+    ptr = ops.host_device_pointer(host)
+    S = c["S"]
+    pool = torch.empty(S * 8192, dtype=torch.bfloat16, device="cuda")
+    keys = torch.randint(0, hb, (nmiss,), device="cuda", dtype=torch.int64)
+    slots = torch.randperm(S, device="cuda")[:nmiss].to(torch.int32)
+    counts = torch.tensor([0, nmiss, 0, 0], dtype=torch.int32, device="cuda")
+    hi = torch.cuda.Stream(priority=-1)
+    main = torch.cuda.current_stream()
+
+    def sel_f():
+        ops.ss_block_select(q, meta, nb, n, k, d, sel, ws)
+
+    def gat_f():
+        ops.flash_h2d_gather(ptr, hb, keys, slots, counts, nmiss, pool, 16384)
+    res = {}
+    res["select_solo_us"] = timeit(sel_f, iters) * 1e3
+    res["gather_solo_us"] = timeit(gat_f, iters) * 1e3
+    ts, tg = [], []
+    for _ in range(iters + 2):
+        a0, a1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        b0, b1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        hi.wait_stream(main)
+        with torch.cuda.stream(hi):
+            b0.record()
+            gat_f()
+            b1.record()
+        a0.record()
+        sel_f()
+        a1.record()
+        main.wait_stream(hi)
+        torch.cuda.synchronize()
+        ts.append(a0.elapsed_time(a1))
+        tg.append(b0.elapsed_time(b1))
+    res["select_with_gather_us"] = sorted(ts[2:])[len(ts[2:]) // 2] * 1e3
+    res["gather_with_select_us"] = sorted(tg[2:])[len(tg[2:]) // 2] * 1e3
+    res["gather_GBps_solo"] = nmiss * 16384 / res["gather_solo_us"] / 1e3
+    return res
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "overlap":
+    print(json.dumps({k: round(v, 2) for k, v in bench_overlap(CFG["C2"]).items()}))

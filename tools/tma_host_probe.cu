@@ -14,15 +14,15 @@ __global__ void tma_gather(const char* host, const int64_t* idx, int n, char* ds
     extern __shared__ __align__(128) char sm[];
     __shared__ uint64_t bar[2];
     int w = threadIdx.x / 32, lane = threadIdx.x % 32;
-    char* buf = sm + w * 2 * BB;
-    uint64_t* b = (uint64_t*)(sm + 8 * 2 * BB) + w * 2;
+    char* buf = sm + w * 2 * BB;  // 4 warps per CTA
+    uint64_t* b = (uint64_t*)(sm + 4 * 2 * BB) + w * 2;
     if (lane == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&b[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&b[1])));
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     __syncwarp();
-    int gw = blockIdx.x * 8 + w, nw = gridDim.x * 8;
+    int gw = blockIdx.x * 4 + w, nw = gridDim.x * 4;
     uint32_t ph[2] = {0, 0};
     int st = 0;
     for (int i = gw; i < n; i += nw) {
@@ -80,22 +80,22 @@ int main() {
     cudaMalloc(&dst2, (int64_t)n * BB);
     char* hd;
     cudaHostGetDevicePointer((void**)&hd, h, 0);
-    int smem = 8 * 2 * BB + 1024;
+    int smem = 4 * 2 * BB + 1024;
     cudaFuncSetAttribute(tma_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     for (int grid : {148, 296}) {
-        tma_gather<<<grid / 2, 256, smem>>>(hd, idx, n, dst);
+        tma_gather<<<grid, 128, smem>>>(hd, idx, n, dst);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("tma_gather error: %s\n", cudaGetErrorString(e)); return 1; }
         cudaEventRecord(a);
-        for (int r = 0; r < 3; ++r) tma_gather<<<grid / 2, 256, smem>>>(hd, idx, n, dst);
+        for (int r = 0; r < 3; ++r) tma_gather<<<grid, 128, smem>>>(hd, idx, n, dst);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
         cudaEventElapsedTime(&ms, a, b);
-        printf("TMA bulk from host  ctas=%d: %.1f GB/s\n", grid / 2, 3.0 * n * BB / ms / 1e6);
+        printf("TMA bulk from host  ctas=%d: %.1f GB/s\n", grid, 3.0 * n * BB / ms / 1e6);
     }
     ldg_gather<<<296, 512>>>((const uint4*)hd, idx, n, (uint4*)dst2);
     cudaDeviceSynchronize();
