@@ -259,59 +259,81 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     }
 
     if constexpr (G > 1)
-    for (int tl = warp; tl < ntiles; tl += kSelWarps) {
-        const int tile = j0 / 32 + tl;
-        const char* tb = meta_pair + (size_t)tile * TILE_ELEMS * ES + lane * 16;
-        if (l2pf && lane == 0 && tl + kSelWarps < ntiles)  // next tile of this warp -> L2
-            prefetch_l2_bulk(meta_pair + (size_t)(tile + kSelWarps) * TILE_ELEMS * ES, TILE_ELEMS * ES);
-        double acc[G];
+    for (int tl = warp; tl < ntiles; tl += 2 * kSelWarps) {
+        // two tiles per warp pass (lane r scores block r of tile tl and of tile
+        // tl + 8): each shared-memory (q+, q-) load serves two blocks and two
+        // independent DFMA chains / load streams are in flight per lane
+        const bool two = tl + kSelWarps < ntiles;
+        const char* tbA = meta_pair + (size_t)(j0 / 32 + tl) * TILE_ELEMS * ES + lane * 16;
+        const char* tbB = two ? tbA + (size_t)kSelWarps * TILE_ELEMS * ES : tbA;
+        double accA[G], accB[G];
 #pragma unroll
-        for (int g = 0; g < G; ++g) acc[g] = 0.0;
+        for (int g = 0; g < G; ++g) accA[g] = accB[g] = 0.0;
         // fully unrolled over the NCH chunks, loads kept D chunks ahead; the
         // min / max elements are converted once (exact f32 -> f64) and shared
         // by the G heads: acc_g += q+_g * M + q-_g * m (one term is an exact 0)
-        constexpr int D = 4, R = D + 1;
-        uint4 mn[R], mx[R];
+        constexpr int D = 3, R = D + 1;
+        uint4 mnA[R], mxA[R], mnB[R], mxB[R];
 #pragma unroll
         for (int s = 0; s < D; ++s) {
-            mn[s] = ldg_stream(tb + (size_t)((s * 2 + 0) * 32) * 16);
-            mx[s] = ldg_stream(tb + (size_t)((s * 2 + 1) * 32) * 16);
+            mnA[s] = ldg_stream(tbA + (size_t)((s * 2 + 0) * 32) * 16);
+            mxA[s] = ldg_stream(tbA + (size_t)((s * 2 + 1) * 32) * 16);
+            mnB[s] = ldg_stream(tbB + (size_t)((s * 2 + 0) * 32) * 16);
+            mxB[s] = ldg_stream(tbB + (size_t)((s * 2 + 1) * 32) * 16);
         }
 #pragma unroll
         for (int s = 0; s < NCH; ++s) {
             if (s + D < NCH) {
-                mn[(s + D) % R] = ldg_stream(tb + (size_t)(((s + D) * 2 + 0) * 32) * 16);
-                mx[(s + D) % R] = ldg_stream(tb + (size_t)(((s + D) * 2 + 1) * 32) * 16);
+                mnA[(s + D) % R] = ldg_stream(tbA + (size_t)(((s + D) * 2 + 0) * 32) * 16);
+                mxA[(s + D) % R] = ldg_stream(tbA + (size_t)(((s + D) * 2 + 1) * 32) * 16);
+                mnB[(s + D) % R] = ldg_stream(tbB + (size_t)(((s + D) * 2 + 0) * 32) * 16);
+                mxB[(s + D) % R] = ldg_stream(tbB + (size_t)(((s + D) * 2 + 1) * 32) * 16);
             }
-            const uint32_t wn[4] = {mn[s % R].x, mn[s % R].y, mn[s % R].z, mn[s % R].w};
-            const uint32_t wx[4] = {mx[s % R].x, mx[s % R].y, mx[s % R].z, mx[s % R].w};
+            const uint32_t wnA[4] = {mnA[s % R].x, mnA[s % R].y, mnA[s % R].z, mnA[s % R].w};
+            const uint32_t wxA[4] = {mxA[s % R].x, mxA[s % R].y, mxA[s % R].z, mxA[s % R].w};
+            const uint32_t wnB[4] = {mnB[s % R].x, mnB[s % R].y, mnB[s % R].z, mnB[s % R].w};
+            const uint32_t wxB[4] = {mxB[s % R].x, mxB[s % R].y, mxB[s % R].z, mxB[s % R].w};
 #pragma unroll
             for (int e = 0; e < CPC; ++e) {
-                double dmin, dmax;
+                double dminA, dmaxA, dminB, dmaxB;
                 if (BF16) {
-                    dmin = (double)__uint_as_float((e & 1) ? (wn[e >> 1] & 0xFFFF0000u) : (wn[e >> 1] << 16));
-                    dmax = (double)__uint_as_float((e & 1) ? (wx[e >> 1] & 0xFFFF0000u) : (wx[e >> 1] << 16));
+                    const int w = e >> 1;
+                    dminA = (double)__uint_as_float((e & 1) ? (wnA[w] & 0xFFFF0000u) : (wnA[w] << 16));
+                    dmaxA = (double)__uint_as_float((e & 1) ? (wxA[w] & 0xFFFF0000u) : (wxA[w] << 16));
+                    dminB = (double)__uint_as_float((e & 1) ? (wnB[w] & 0xFFFF0000u) : (wnB[w] << 16));
+                    dmaxB = (double)__uint_as_float((e & 1) ? (wxB[w] & 0xFFFF0000u) : (wxB[w] << 16));
                 } else {
-                    dmin = (double)__uint_as_float(wn[e]);
-                    dmax = (double)__uint_as_float(wx[e]);
+                    dminA = (double)__uint_as_float(wnA[e]);
+                    dmaxA = (double)__uint_as_float(wxA[e]);
+                    dminB = (double)__uint_as_float(wnB[e]);
+                    dmaxB = (double)__uint_as_float(wxB[e]);
                 }
                 const int c = s * CPC + e;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const double2 qq = qpn[c * G + g];
-                    acc[g] = __fma_rn(qq.x, dmax, acc[g]);
-                    acc[g] = __fma_rn(qq.y, dmin, acc[g]);
+                    accA[g] = __fma_rn(qq.x, dmaxA, accA[g]);
+                    accA[g] = __fma_rn(qq.y, dminA, accA[g]);
+                    accB[g] = __fma_rn(qq.x, dmaxB, accB[g]);
+                    accB[g] = __fma_rn(qq.y, dminB, accB[g]);
                 }
             }
         }
-        double s = acc[0];
+        double sA = accA[0], sB = accB[0];
 #pragma unroll
-        for (int g = 1; g < G; ++g) s = acc[g] > s ? acc[g] : s;
-        s = s + 0.0;
-        const int pos = tl * 32 + lane;
-        const int j = j0 + pos;
-        keys[pos] = ord_key(s);
-        if (scores != nullptr && j < nb) scores[(size_t)pair * max_blk + j] = s;
+        for (int g = 1; g < G; ++g) {
+            sA = accA[g] > sA ? accA[g] : sA;
+            sB = accB[g] > sB ? accB[g] : sB;
+        }
+        sA = sA + 0.0;
+        sB = sB + 0.0;
+        const int posA = tl * 32 + lane, posB = (tl + kSelWarps) * 32 + lane;
+        keys[posA] = ord_key(sA);
+        if (scores != nullptr && j0 + posA < nb) scores[(size_t)pair * max_blk + j0 + posA] = sA;
+        if (two) {
+            keys[posB] = ord_key(sB);
+            if (scores != nullptr && j0 + posB < nb) scores[(size_t)pair * max_blk + j0 + posB] = sB;
+        }
     }
     __syncthreads();
 

@@ -101,7 +101,7 @@ struct WarpSmem {
     alignas(128) unsigned char buf[2][T::BLOCK_BYTES];
     alignas(16) float4 q4[G][kHeadDim / 4];  // q (fp32) in 16-byte chunks, chunk order below
     alignas(16) float p[G][kBlockTokens];    // softmax numerators of the current block
-    uint64_t bar[2];
+    uint64_t bar[2][2];  // [stage][K half / V half]
 };
 
 __device__ __forceinline__ int64_t warp_of_unit(int64_t x, int64_t U, int W) {
@@ -139,58 +139,88 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
     const int Ku = a.k + 1;
 
     if (lane == 0) {
-        mbar_init(&sm.bar[0], 1);
-        mbar_init(&sm.bar[1], 1);
+        mbar_init(&sm.bar[0][0], 1);
+        mbar_init(&sm.bar[0][1], 1);
+        mbar_init(&sm.bar[1][0], 1);
+        mbar_init(&sm.bar[1][1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
 
     // ---- producer: next valid unit -> stage (lane 0 issues the bulk copy) ----
+    // The unit descriptors of the warp's range are read 32 at a time into a
+    // lane-distributed window (lane l: unit wbase + l), so finding the next
+    // valid unit is a ballot, not a dependent global load per block.
     int64_t next_u = u0;
     int64_t bu0 = -1, bu1 = -1;  // unit held by stage 0 / 1 (-1: none)
-    auto issue = [&](int stage) {
-        const char* src = nullptr;
-        while (next_u < u1) {
-            int64_t p = next_u / Ku;
-            int r = (int)(next_u % Ku);
+    int64_t wbase = u0;
+    int wkind = 0;               // 0 invalid, 1 pool slot, 2 tail block
+    int64_t widx = 0;            // slot or pair index
+    auto refill = [&]() {
+        const int64_t u = wbase + lane;
+        wkind = 0;
+        if (u < u1) {
+            const int64_t p = u / Ku;
+            const int r = (int)(u % Ku);
             if (r < a.k) {
-                int32_t s = __ldg(a.slot + p * a.k + r);
-                if (s >= 0) {
-                    src = (const char*)a.pool + (int64_t)s * T::BLOCK_BYTES;
-                    break;
-                }
-            } else if (__ldg(a.tail_len + p / a.Hkv) > 0) {
-                src = (const char*)a.tail + p * (int64_t)T::BLOCK_BYTES;
-                break;
+                const int32_t sl = __ldg(a.slot + p * a.k + r);
+                wkind = sl >= 0 ? 1 : 0;
+                widx = sl;
+            } else {
+                wkind = __ldg(a.tail_len + p / a.Hkv) > 0 ? 2 : 0;
+                widx = p;
             }
-            ++next_u;
-        }
-        if (next_u < u1) {
-            if (lane == 0) {
-                // order this warp's earlier generic-proxy reads of the buffer
-                // before the async-proxy (TMA) write that refills it
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&sm.bar[stage], T::BLOCK_BYTES);
-                bulk_g2s(sm.buf[stage], src, T::BLOCK_BYTES, &sm.bar[stage]);
-            }
-            (stage ? bu1 : bu0) = next_u++;
-            // warm L2 with the following unit (one lane, no smem): the next bulk
-            // copy then sees L2 latency instead of DRAM latency
-            if (a.l2pf && lane == 0 && next_u < u1) {
-                const int64_t pn = next_u / Ku;
-                const int rn = (int)(next_u % Ku);
-                if (rn < a.k) {
-                    const int32_t sn = __ldg(a.slot + pn * a.k + rn);
-                    if (sn >= 0) prefetch_l2_bulk((const char*)a.pool + (int64_t)sn * T::BLOCK_BYTES, T::BLOCK_BYTES);
-                }
-            }
-        } else {
-            (stage ? bu1 : bu0) = -1;
         }
     };
-    issue(0);
-    issue(1);
-    uint32_t phases = 0u;  // bit s = mbarrier phase of stage s
+    refill();
+    // Each stage holds one unit as two 8 KiB (bf16) halves with their own
+    // mbarriers: the K half of the next unit is requested as soon as the
+    // current unit's logits are done, half a block earlier than a whole-block
+    // refill would allow (deeper pipeline at the same shared-memory budget).
+    constexpr uint32_t HALF = T::BLOCK_BYTES / 2;
+    const char* bsrc0 = nullptr;
+    const char* bsrc1 = nullptr;  // source of the unit held by stage 0 / 1
+    auto issue_half = [&](int stage, int half) {
+        const char* src = stage ? bsrc1 : bsrc0;
+        if (lane == 0 && src != nullptr) {
+            // order this warp's earlier generic-proxy reads of the buffer
+            // before the async-proxy (TMA) write that refills it
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&sm.bar[stage][half], HALF);
+            bulk_g2s(sm.buf[stage] + half * HALF, src + half * HALF, HALF, &sm.bar[stage][half]);
+        }
+    };
+    // next valid unit -> stage: records it and requests its K half
+    auto issue_k = [&](int stage) {
+        while (true) {
+            const unsigned m = __ballot_sync(0xffffffffu, wkind != 0 && wbase + lane >= next_u);
+            if (m) {
+                const int l = __ffs(m) - 1;
+                next_u = wbase + l;
+                const int kind = __shfl_sync(0xffffffffu, wkind, l);
+                const int64_t idx = __shfl_sync(0xffffffffu, widx, l);
+                const char* src = kind == 1 ? (const char*)a.pool + idx * T::BLOCK_BYTES
+                                            : (const char*)a.tail + idx * T::BLOCK_BYTES;
+                (stage ? bsrc1 : bsrc0) = src;
+                (stage ? bu1 : bu0) = next_u++;
+                issue_half(stage, 0);
+                return;
+            }
+            if (wbase + 32 >= u1) {
+                next_u = u1;
+                (stage ? bu1 : bu0) = -1;
+                (stage ? bsrc1 : bsrc0) = nullptr;
+                return;
+            }
+            wbase += 32;
+            refill();
+        }
+    };
+    issue_k(0);
+    issue_half(0, 1);
+    issue_k(1);
+    issue_half(1, 1);
+    uint32_t phases = 0u;  // bit 2*stage + half = mbarrier phase
     int stage = 0;
 
     const int64_t p_first = u0 / Ku, p_last = (u1 - 1) / Ku;
@@ -222,8 +252,8 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
             const int64_t cu = stage ? bu1 : bu0;
             if (cu < 0 || cu / Ku != p) break;
             const bool is_tail = (cu % Ku) == a.k;
-            mbar_wait(&sm.bar[stage], (phases >> stage) & 1u);
-            phases ^= 1u << stage;
+            mbar_wait(&sm.bar[stage][0], (phases >> (2 * stage)) & 1u);
+            phases ^= 1u << (2 * stage);
             const unsigned char* kb = sm.buf[stage];
             const unsigned char* vb = kb + kBlockTokens * kHeadDim * T::ES;
             // ---- logits: lane = token; 4 independent accumulators per head ----
@@ -283,6 +313,10 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
                 m[g] = mnew;
             }
             __syncwarp();
+            // K half consumed: request the K half of this stage's next unit now
+            issue_k(stage);
+            mbar_wait(&sm.bar[stage][1], (phases >> (2 * stage + 1)) & 1u);
+            phases ^= 1u << (2 * stage + 1);
             // ---- O += P V: lane owns dims 4*lane .. 4*lane+3 ----
             auto pv_token = [&](int t, const float (&pt)[G]) {
                 float v0, v1, v2, v3;
@@ -337,7 +371,7 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
                 }
             }
             __syncwarp();
-            issue(stage);  // refill the buffer just consumed
+            issue_half(stage, 1);  // V half of this stage's next unit
             stage ^= 1;
         }
 
@@ -469,7 +503,9 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
     // at least kMinUnitsPerWarp units (256 KiB in bf16) per warp: fewer, longer
     // ranges when the problem is small (C3: ~8 partials per pair to merge instead
     // of ~28); W <= U keeps every range non-empty
-    a.W = (int)std::max<int64_t>(1, std::min<int64_t>(attn_total_warps(dt), a.U / kMinUnitsPerWarp));
+    static const int min_units = getenv("SS_ATTN_MIN_UNITS") ? atoi(getenv("SS_ATTN_MIN_UNITS"))
+                                                              : kMinUnitsPerWarp;
+    a.W = (int)std::max<int64_t>(1, std::min<int64_t>(attn_total_warps(dt), a.U / std::max(1, min_units)));
     size_t part = (size_t)a.W * 2 * G * kAttnPartStride * 4;
     a.part = (float*)ws;
     a.tickets = (int32_t*)((char*)ws + part);

@@ -101,6 +101,7 @@ class RequestGroup:
         self.ev_cache = [torch.cuda.Event() for _ in range(c.layers)]
         self.ev_attn = [torch.cuda.Event() for _ in range(c.layers)]
         self.ev_gather = [torch.cuda.Event() for _ in range(c.layers)]
+        self.ev_sel = [torch.cuda.Event() for _ in range(c.layers)]
         # FlashH2D runs on the engine's shared high-priority stream (set below)
         self.h2d_stream = None
 
@@ -147,6 +148,7 @@ class DecodeEngine:
             h2d = torch.cuda.Stream(dev, priority=-1)
             for g in self.groups:
                 g.h2d_stream = h2d
+        self.cache_stream = torch.cuda.Stream(dev, priority=-1) if ng > 1 else None
         g0 = self.groups[0]
         # single-group aliases (tests, smoke)
         self.sel, self.slot, self.hit = g0.sel, g0.slot, g0.hit
@@ -204,32 +206,44 @@ class DecodeEngine:
                 e.record()
         timed("select", lambda: ops.ss_block_select(q, g.meta[l], g.n_blk, c.max_blk, c.topk, g.dims,
                                                     g.sel[l], g.ws_select, scores=scores))
-        if len(self.groups) > 1:
-            # pool order: groups of a layer call the cache in group order; the
-            # first group of step t waits for every group's layer-l attention of t-1
-            if gi > 0:
-                g.stream.wait_event(self.groups[gi - 1].ev_cache[l])
-            else:
+        multi = len(self.groups) > 1
+
+        def _cache():
+            timed("cache", lambda: ops.kv_cache_lookup_insert(
+                self.pools[l], g.sel[l], g.req_ids, l, c.layers, c.max_blk, c.topk, g.dims, stamp,
+                g.slot[l], g.hit[l], g.miss_keys[l], g.miss_slots[l], g.counts[l], g.ws_cache))
+
+        def _gather():
+            timed("gather", lambda: ops.flash_h2d_gather(self.host_ptr, self.host_blocks,
+                                                         g.miss_keys[l], g.miss_slots[l], g.counts[l],
+                                                         g.E, self.pool_kv[l], c.block_bytes))
+        if not multi:
+            _cache()
+            if gather:
+                _gather()
+        else:
+            # cache calls of all groups go through one high-priority stream in
+            # issue order (layer l: group 0, 1, ...): pool order for free, and the
+            # small cache kernels are dispatched ahead of queued select CTAs.  The
+            # first group of step t also waits for every group's layer-l attention
+            # of step t-1 (no eviction under a reader).
+            g.ev_sel[l].record(g.stream)
+            cs = self.cache_stream
+            cs.wait_event(g.ev_sel[l])
+            if gi == 0:
                 for other in self.groups[1:]:
-                    g.stream.wait_event(other.ev_attn[l])
-        timed("cache", lambda: ops.kv_cache_lookup_insert(
-            self.pools[l], g.sel[l], g.req_ids, l, c.layers, c.max_blk, c.topk, g.dims, stamp,
-            g.slot[l], g.hit[l], g.miss_keys[l], g.miss_slots[l], g.counts[l], g.ws_cache))
-        if len(self.groups) > 1:
-            g.ev_cache[l].record(g.stream)
-        if gather:
-            def _gather():
-                timed("gather", lambda: ops.flash_h2d_gather(self.host_ptr, self.host_blocks,
-                                                             g.miss_keys[l], g.miss_slots[l], g.counts[l],
-                                                             g.E, self.pool_kv[l], c.block_bytes))
-            if g.h2d_stream is not None:
+                    cs.wait_event(other.ev_attn[l])
+            with torch.cuda.stream(cs):
+                _cache()
+                g.ev_cache[l].record(cs)
+            if gather:
                 g.h2d_stream.wait_event(g.ev_cache[l])
                 with torch.cuda.stream(g.h2d_stream):
                     _gather()
                     g.ev_gather[l].record(g.h2d_stream)
                 g.stream.wait_event(g.ev_gather[l])
             else:
-                _gather()
+                g.stream.wait_event(g.ev_cache[l])
         timed("attn", lambda: ops.sparse_decode_attn(q, self.pool_kv[l], g.slot[l], c.topk,
                                                      g.tail_kv[l], g.tail_len, g.dims, self.scale,
                                                      g.out[l], g.ws_attn, counts=g.counts[l]))
@@ -257,6 +271,8 @@ class DecodeEngine:
         cur = torch.cuda.current_stream(self.device)
         for g in self.groups:
             g.stream.wait_stream(cur)
+        self.cache_stream.wait_stream(cur)
+        self.groups[0].h2d_stream.wait_stream(cur)
         # issue layer by layer, group by group: group A's FlashH2D (PCIe) overlaps
         # group B's select / attention (HBM) on the other stream
         for l in range(c.layers):

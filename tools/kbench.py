@@ -66,8 +66,10 @@ def bench_attn(c, iters):
     d = ops.dims(B, Hq, Hkv)
     ws = ops.alloc_workspace(2, d, 32, k)
     out = torch.empty(Hq, B, 128, dtype=torch.float32, device="cuda")
-    # flush between iterations: pool per-call bytes may fit in L2 (C3: 64 MB)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    # flush between iterations with a READ of 256 MB (clean L2; a memset would
+    # leave 126 MB of dirty lines whose write-back the timed kernel would pay)
+    flush = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+    sink = torch.empty((), dtype=torch.float32, device="cuda")
 
     def f():
         ops.sparse_decode_attn(q, pool, slot, k, tail, tl, d, 1 / math.sqrt(128), out, ws)
@@ -77,7 +79,7 @@ def bench_attn(c, iters):
         f()
     ts = []
     for _ in range(iters):
-        flush.zero_()
+        torch.sum(flush, dim=0, out=sink)
         s.record()
         f()
         e.record()
