@@ -282,9 +282,12 @@ def bench_ours(args):
     t_setup = time.time()
     eng, W = setup_engine(args, rank, world)
     c = eng.cfg
-    steps_total = args.warmup + args.steps
     e2e_steps = max(3, args.steps // 2)
-    qs = gen_queries(eng, args.warmup + e2e_steps + args.steps, W["rho"], seed=5000 + rank)
+    n_kt = max(3, min(args.steps, 8))                 # eager per-kernel timing pass
+    t_e2e = args.warmup
+    t_timed = t_e2e + e2e_steps
+    t_kt = t_timed + args.steps
+    qs = gen_queries(eng, t_kt + n_kt, W["rho"], seed=5000 + rank)
     gathered = None
     if world > 1:
         # one communicator per request group (their all-gathers run on different streams)
@@ -299,7 +302,13 @@ def bench_ours(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (the first step is cold: every selected block misses)
+    def allgather_hook():
+        if world == 1:
+            return None
+        from paper_2509_24626_b200.shard import gather_outputs
+        return lambda gi, g, l: gather_outputs(g.out[l], gathered[gi][l], group=pgs[gi])
+
+    # warm-up (eager, host stamps 1..W; the first step is cold: every block misses)
     cold_ms = None
     for t in range(args.warmup):
         s, e = torch.cuda.Event(True), torch.cuda.Event(True)
@@ -309,25 +318,42 @@ def bench_ours(args):
         torch.cuda.synchronize()
         if t == 0:
             cold_ms = s.elapsed_time(e)
-    # ---- e2e through the public API with host buffers (runs first, right after
-    # the warm-up, so it sees the colder -- more miss-heavy -- cache state) ----
-    # fresh drifting queries per step (continuing the same q process), staged in
-    # pinned host memory; each step copies its own q in and its outputs out.
-    q_host = qs[args.warmup:args.warmup + e2e_steps].cpu().pin_memory()
+
+    # steps from here on read q from one static buffer; with --graph (default)
+    # the whole step (all layers, groups and streams) is one captured CUDA graph
+    # and the LRU stamps come from device clocks in the pools
+    q_static = torch.empty_like(qs[0])
+    graph = None
+    if args.graph:
+        eng.use_device_clock(start=args.warmup)
+        graph = eng.capture_graph(q_static, post_attn=allgather_hook())
+
+    def do_step(q_src, t):
+        q_static.copy_(q_src, non_blocking=True)
+        if graph is not None:
+            graph.replay()
+        else:
+            run_step(eng, q_static, stamp=t + 1, pgs=pgs, world=world, gathered=gathered)
+
+    def counts_sum(acc):
+        for g in eng.groups:
+            acc += g.counts.to(torch.int64).sum(0)
+
+    # ---- e2e through the public API with host buffers (first, right after the
+    # warm-up, so it sees the colder -- more miss-heavy -- cache state): every
+    # step copies its q in from pinned host memory and its outputs out ----
+    q_host = qs[t_e2e:t_e2e + e2e_steps].cpu().pin_memory()
     outs = gathered if world > 1 else eng.outputs()
     out_host = [torch.empty(o.shape, dtype=torch.float32, pin_memory=True) for o in outs]
-    q_dev = torch.empty_like(qs[0])
     barrier()
     e_s, e_e = torch.cuda.Event(True), torch.cuda.Event(True)
     e2e_cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
     e_s.record()
     for i in range(e2e_steps):
-        q_dev.copy_(q_host[i], non_blocking=True)
-        run_step(eng, q_dev, stamp=args.warmup + 1 + i, pgs=pgs, world=world, gathered=gathered)
+        do_step(q_host[i], t_e2e + i)
         for oh, o in zip(out_host, outs):
             oh.copy_(o, non_blocking=True)
-        for g in eng.groups:
-            e2e_cnt += g.counts.to(torch.int64).sum(0)
+        counts_sum(e2e_cnt)
     e_e.record()
     barrier()
     e_ms = e_s.elapsed_time(e_e)
@@ -336,80 +362,92 @@ def bench_ours(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e_ms = float(tt.item())
     e2e = {"value": round(c.batch * e2e_steps / (e_ms * 1e-3), 2), "unit": "tokens/s",
-           "h2d_bytes_per_step": int(q_host.numel() * q_host.element_size()),
+           "h2d_bytes_per_step": int(q_host[0].numel() * q_host.element_size()),
            "d2h_bytes_per_step": int(sum(o.numel() * o.element_size() for o in out_host)),
            "steps": e2e_steps,
            "hit_rate": round(float(e2e_cnt[0]) / max(1.0, float(e2e_cnt[0] + e2e_cnt[1])), 4),
            "misses_per_step": float(e2e_cnt[1]) / e2e_steps}
 
-    # timed region
-    timers = StepTimers()
+    # ---- timed region (value): inputs resident in HBM ----
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
     barrier()
     start, end = torch.cuda.Event(True), torch.cuda.Event(True)
-    hits = torch.zeros(4, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
     start.record()
-    t0 = args.warmup + e2e_steps
-    for t in range(t0, t0 + args.steps):
-        run_step(eng, qs[t], stamp=t + 1, timers=timers, pgs=pgs, world=world, gathered=gathered)
-        for g in eng.groups:
-            hits += g.counts.to(torch.int64).sum(0)
+    for t in range(t_timed, t_timed + args.steps):
+        do_step(qs[t], t)
+        counts_sum(cnt)
     end.record()
     barrier()
     clocks = sampler.stop()
     ms = start.elapsed_time(end)
-    if args.timeline and rank == 0:
-        ops_per_step = len(timers.trace) // args.steps
-        with open(args.timeline, "w") as f:
-            json.dump(timers.timeline(start, ops_per_step), f)
     if world > 1:
         tt = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms = float(tt.item())
     ms_step = ms / args.steps
-    tot = timers.totals_ms()
-    nlaunch = timers.counts()
-    hc = hits.cpu().tolist()
-    n_hits, n_miss, n_evict, n_err = hc
+    n_hits, n_miss, n_evict, n_err = cnt.cpu().tolist()
     lookups = n_hits + n_miss
     hit_rate = n_hits / lookups if lookups else 0.0
-    tokens = c.batch * args.steps                       # one token per request per step (all ranks: x world / world)
-    tokens_all = tokens                                 # batch already counts every rank's requests
-    value = tokens_all / (ms * 1e-3)
+    value = c.batch * args.steps / (ms * 1e-3)        # batch counts every rank's requests
+
+    # ---- per-kernel timing pass: eager launches with CUDA events recorded on
+    # each kernel's launching stream (the graph hides the individual kernels) ----
+    timers = StepTimers()
+    kcnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    barrier()
+    k_s = torch.cuda.Event(True)
+    k_s.record()
+    for t in range(t_kt, t_kt + n_kt):
+        q_static.copy_(qs[t], non_blocking=True)
+        if graph is not None:
+            eng.advance_clock()          # device-clock stamps (the host stamp is ignored)
+        run_step(eng, q_static, stamp=t + 1, timers=timers, pgs=pgs, world=world, gathered=gathered)
+        counts_sum(kcnt)
+    barrier()
+    if args.timeline and rank == 0:
+        with open(args.timeline, "w") as f:
+            json.dump(timers.timeline(k_s, len(timers.trace) // n_kt), f)
+    tot = timers.totals_ms()
+    nlaunch = timers.counts()
+    k_hits, k_miss = [int(x) for x in kcnt.cpu().tolist()[:2]]
 
     # ---- roofline of each kernel (algorithmic bytes / measured time) ----
     hbm_peak, peak_src = _peaks()
-    pairs = c.pairs
-    meta_bytes = pairs * W["n_blk"] * 2 * 128 * 2 * c.layers * args.steps       # per timed region
-    q_bytes = c.batch * c.num_q_heads * 128 * 2 * c.layers * args.steps
-    attn_units = lookups                                  # selected blocks attended (tail_len = 0)
-    attn_bytes = attn_units * c.block_bytes + c.num_q_heads * c.batch * 128 * 4 * c.layers * args.steps
-    miss_bytes = n_miss * c.block_bytes
-    sel_gbs = (meta_bytes + q_bytes) / (tot["select"] * 1e-3) / 1e9
+    n_sel = max(1, nlaunch["select"])
+    sel_bytes = (c.pairs * W["n_blk"] * 2 * 128 * 2 + c.batch * c.num_q_heads * 128 * 2) * c.layers * n_kt
+    attn_bytes = (k_hits + k_miss) * c.block_bytes + c.num_q_heads * c.batch * 128 * 4 * c.layers * n_kt
+    miss_bytes_kt = k_miss * c.block_bytes
+    sel_gbs = sel_bytes / (tot["select"] * 1e-3) / 1e9
     attn_gbs = attn_bytes / (tot["attn"] * 1e-3) / 1e9
-    h2d_gbs = miss_bytes / (tot["gather"] * 1e-3) / 1e9 if tot["gather"] > 0 else 0.0
+    h2d_gbs = miss_bytes_kt / (tot["gather"] * 1e-3) / 1e9 if tot["gather"] > 0 else 0.0
     kernels = {
         "ss_block_select": {"bound": "hbm", "achieved": round(sel_gbs, 1), "peak": hbm_peak,
                              "unit": "GB/s", "frac": round(sel_gbs / hbm_peak, 4),
-                             "ms_per_step": round(tot["select"] / args.steps, 3),
-                             "bytes_per_launch": int((meta_bytes + q_bytes) / nlaunch["select"])},
+                             "us_per_launch": round(tot["select"] * 1e3 / n_sel, 2),
+                             "bytes_per_launch": int(sel_bytes / n_sel)},
         "sparse_decode_attn": {"bound": "hbm", "achieved": round(attn_gbs, 1), "peak": hbm_peak,
                                 "unit": "GB/s", "frac": round(attn_gbs / hbm_peak, 4),
-                                "ms_per_step": round(tot["attn"] / args.steps, 3),
-                                "bytes_per_launch": int(attn_bytes / nlaunch["attn"])},
+                                "us_per_launch": round(tot["attn"] * 1e3 / max(1, nlaunch["attn"]), 2),
+                                "bytes_per_launch": int(attn_bytes / max(1, nlaunch["attn"]))},
         "flash_h2d_gather": {"bound": "host-link", "achieved": round(h2d_gbs, 2),
                               "peak": round(h2d_peak, 2), "unit": "GB/s",
                               "frac": round(h2d_gbs / h2d_peak, 4) if h2d_peak else None,
-                              "ms_per_step": round(tot["gather"] / args.steps, 3),
-                              "bytes_per_launch": int(miss_bytes / max(1, nlaunch["gather"]))},
-        "kv_cache_lookup_insert": {"bound": "latency", "ms_per_step": round(tot["cache"] / args.steps, 3)},
+                              "us_per_launch": round(tot["gather"] * 1e3 / max(1, nlaunch["gather"]), 2),
+                              "bytes_per_launch": int(miss_bytes_kt / max(1, nlaunch["gather"]))},
+        "kv_cache_lookup_insert": {"bound": "latency",
+                                   "us_per_launch": round(tot["cache"] * 1e3 / max(1, nlaunch["cache"]), 2)},
+        "timing_pass": {"steps": n_kt, "eager": True, "request_groups": len(eng.groups),
+                        "note": "events on each kernel's launching stream; kernels of different request "
+                                "groups overlap, so a launch's time includes co-running work"},
     }
     if world > 1:
-        kernels["nccl_all_gather"] = {"ms_per_step": round(tot["allgather"] / args.steps, 3)}
-    dom = max(("ss_block_select", "sparse_decode_attn", "flash_h2d_gather"),
-              key=lambda k: kernels[k]["ms_per_step"])
+        kernels["nccl_all_gather"] = {"us_per_launch": round(tot["allgather"] * 1e3 / max(1, nlaunch["allgather"]), 2)}
+    share = {k: tot[n] for k, n in (("ss_block_select", "select"), ("sparse_decode_attn", "attn"),
+                                    ("flash_h2d_gather", "gather"))}
+    dom = max(share, key=share.get)
     dk = kernels[dom]
     traffic = None
     prof_t = os.path.join(ROOT, "profiles", "traffic.json")
@@ -438,17 +476,18 @@ def bench_ours(args):
                        "topk_blocks": c.topk, "hbm_cache_slots_per_layer": c.slots_per_layer,
                        "host_pool_blocks": eng.host_blocks, "host_kv": "pinned DRAM, zero-copy (UVA)",
                        "parallelism": f"kv-heads/{world} per GPU" if world > 1 else "1 GPU",
-                       "request_groups": len(eng.groups),
+                       "request_groups": len(eng.groups), "cuda_graph": graph is not None,
                        "l2": "no flush needed: inputs larger than L2 (32 GiB metadata streamed per step)",
                        "scope": "attention path only (no QKV/O projections, no FFN)"},
             "hit_rate": round(hit_rate, 4), "misses_per_step": n_miss / args.steps,
-            "h2d_bytes_per_step": miss_bytes / args.steps,
+            "h2d_bytes_per_step": n_miss * c.block_bytes / args.steps,
             "flash_h2d": {"achieved_gbs": kernels["flash_h2d_gather"]["achieved"],
                           "link_peak_gbs": round(h2d_peak, 2), "link_theoretical_gbs": 63.0,
-                          "frac": kernels["flash_h2d_gather"]["frac"]},
+                          "frac": kernels["flash_h2d_gather"]["frac"],
+                          "h2d_gbs_over_step": round(n_miss * c.block_bytes / (ms * 1e-3) / 1e9, 2)},
             "roofline": roofline, "kernels": kernels,
             "cold_step_ms": round(cold_ms, 2) if cold_ms else None,
-            "e2e": e2e, "gpu_launches": int(args.steps * c.layers * 10 * len(eng.groups)),
+            "e2e": e2e, "gpu_launches": int(args.steps * c.layers * 6 * len(eng.groups)),
             "cpu_baseline": cpu, "clocks": clocks, "setup_s": round(setup_s, 1),
             "errors_in_timed_region": n_err,
         }
@@ -511,7 +550,9 @@ def main():
     ap.add_argument("--host-runs", type=int, default=251,
                     help="physical host KV pool = host_runs x max_blk blocks (251 -> 15.7 GiB)")
     ap.add_argument("--cpu-req", type=int, default=1)
-    ap.add_argument("--timeline", default=None, help="write the first timed step's op timeline (json)")
+    ap.add_argument("--timeline", default=None, help="write one step's op timeline (json, timing pass)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch kernels eagerly instead of replaying a captured CUDA graph per step")
     ap.add_argument("--groups", type=int, default=2,
                     help="request groups pipelined on separate streams (PCIe of one overlaps HBM work of another)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -149,9 +149,10 @@ typedef struct {
     int32_t* order_pos;  /* inverse permutation of order.      Initially 0..S-1. */
     int32_t num_slots;
     /* Optional device int64 "clock" (NULL = use the `stamp` argument).  When
-     * set, the call's stamp is *clock + 1 (the `stamp` argument is ignored)
-     * and *clock is advanced to it on success (left unchanged on error), so a
-     * captured CUDA graph can replay decode steps without host-side scalars. */
+     * set, the call's stamp is *clock, read on the device (the `stamp`
+     * argument is ignored); the caller advances it once per decode step (all
+     * calls of one step share it), so a captured CUDA graph can replay decode
+     * steps without host-side scalars. */
     int64_t* clock;
 } ss_cache_pool;
 

@@ -22,7 +22,7 @@
 //                     stamp == t per slot chunk; hits correct both counts
 //                     through order_pos.  The LAST CTA (atomic ticket) scans
 //                     the per-CTA counts, checks capacity, writes counts/status
-//                     and publishes the stamp (advances the device clock).
+//                     and publishes the stamp.
 //   K2 victims      : first M eligible order entries -> victim list (evict old
 //                     keys, mark victims); the rest -> new order prefix
 //   K3 assign+place : entry CTAs assign the i-th miss the i-th victim
@@ -118,11 +118,11 @@ __device__ __forceinline__ int64_t cache_key(const CacheArgs& a, int64_t e, int3
     return (((int64_t)a.req_ids[b] * a.num_layers + a.layer) * a.Hkv + h) * a.max_blk + j;
 }
 
-// The call's stamp: the host argument, or *clock + 1 with a device clock.
-// K1 reads it from the clock; its last CTA publishes it in ctrl64[0] (and
-// advances *clock); K2/K3 read ctrl64[0].
+// The call's stamp: the host argument, or *clock (read on the device) when
+// the pool has a device clock.  K1 reads it; its last CTA publishes it in
+// ctrl64[0] for K2/K3.  The caller advances the clock between decode steps.
 __device__ __forceinline__ int64_t stamp_pre_plan(const CacheArgs& a) {
-    return a.pool.clock ? *a.pool.clock + 1 : a.stamp;
+    return a.pool.clock ? *a.pool.clock : a.stamp;
 }
 __device__ __forceinline__ int64_t stamp_post_plan(const CacheArgs& a) {
     return a.pool.clock ? a.ws.ctrl64[0] : a.stamp;
@@ -164,9 +164,7 @@ __device__ void cache_plan(const CacheArgs& a, int* sw) {
         a.counts[1] = status == 1 ? 0 : M;
         a.counts[2] = 0;
         a.counts[3] = status;
-        const int64_t t = stamp_pre_plan(a);
-        a.ws.ctrl64[0] = t;
-        if (a.pool.clock && status == 0) *a.pool.clock = t;
+        a.ws.ctrl64[0] = stamp_pre_plan(a);
     }
 }
 

@@ -149,6 +149,7 @@ class DecodeEngine:
             for g in self.groups:
                 g.h2d_stream = h2d
         self.cache_stream = torch.cuda.Stream(dev, priority=-1) if ng > 1 else None
+        self._capturing = False
         g0 = self.groups[0]
         # single-group aliases (tests, smoke)
         self.sel, self.slot, self.hit = g0.sel, g0.slot, g0.hit
@@ -230,7 +231,9 @@ class DecodeEngine:
             g.ev_sel[l].record(g.stream)
             cs = self.cache_stream
             cs.wait_event(g.ev_sel[l])
-            if gi == 0:
+            if gi == 0 and not self._capturing:
+                # (inside a captured graph, successive replays are serialised,
+                # which already orders step t+1 after all of step t)
                 for other in self.groups[1:]:
                     cs.wait_event(other.ev_attn[l])
             with torch.cuda.stream(cs):
@@ -286,3 +289,43 @@ class DecodeEngine:
 
     def outputs(self) -> List[torch.Tensor]:
         return [g.out for g in self.groups]
+
+    def capture_graph(self, q_static: torch.Tensor, post_attn=None) -> "torch.cuda.CUDAGraph":
+        """Capture one whole decode step (all layers, all request groups and
+        streams) into a CUDA graph reading q from `q_static` [L][B][Hq][d].
+        Requires device clocks on the pools (`use_device_clock()`), so each
+        replay advances the LRU stamps without host-side scalars.  Replaying
+        the graph replaces ~10 host launches per layer and group with one."""
+        assert getattr(self, "clock", None) is not None, "call use_device_clock() first"
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        self._capturing = True
+        try:
+            with torch.cuda.graph(g, stream=side):
+                self.clock.add_(1)      # one new LRU stamp per replayed step
+                self.step(q_static, stamp=0, post_attn=post_attn)
+        finally:
+            self._capturing = False
+        torch.cuda.synchronize(self.device)
+        # the step events were recorded inside the capture; fresh ones keep
+        # later eager steps from waiting on graph-internal records
+        for grp in self.groups:
+            for name in ("ev_cache", "ev_attn", "ev_gather", "ev_sel"):
+                setattr(grp, name, [torch.cuda.Event() for _ in range(self.cfg.layers)])
+        return g
+
+    def use_device_clock(self, start: int) -> None:
+        """Switch every pool to one shared device-side stamp counter holding
+        `start` (the host `stamp` argument is then ignored).  A captured step
+        increments it once per replay; eager steps in this mode must call
+        `advance_clock()` before each step."""
+        if getattr(self, "clock", None) is None:
+            self.clock = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.clock.fill_(start)
+        for p in self.pools:
+            p.clock = self.clock
+
+    def advance_clock(self) -> None:
+        self.clock.add_(1)

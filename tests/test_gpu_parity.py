@@ -350,35 +350,35 @@ def test_attention_skipped_on_error_status(ops):
 
 
 def test_cache_device_clock_mode(ops):
-    # pool.clock set: stamps come from the device (call index), the host stamp is
-    # ignored, and a capacity error leaves the clock (and pool) unchanged.
+    # pool.clock set: the stamp is read on the device (*clock) and the host stamp
+    # argument is ignored; several calls may share one stamp (request groups).
     rng = synth.rng_for(1000, 4)
     B, Hkv, k, max_blk, S = 2, 2, 16, 128, 80
     fwd_len = B * Hkv * max_blk
     fwd = torch.full((fwd_len,), -1, dtype=torch.int32, device="cuda")
     gp = ops.CachePool(S, fwd, clock=True)
     op = oracle.Pool(S, fwd_len)
-    d = ops.dims(B, Hkv, Hkv)
+    d = ops.dims(1, Hkv, Hkv)
     ws = ops.alloc_workspace(1, d, max_blk, k, S)
-    E = B * Hkv * k
-    slot = torch.empty(B, Hkv, k, dtype=torch.int32, device="cuda")
-    hit = torch.empty(B, Hkv, k, dtype=torch.uint8, device="cuda")
+    E = Hkv * k
+    slot = torch.empty(1, Hkv, k, dtype=torch.int32, device="cuda")
+    hit = torch.empty(1, Hkv, k, dtype=torch.uint8, device="cuda")
     mk = torch.empty(E, dtype=torch.int64, device="cuda")
     ms = torch.empty(E, dtype=torch.int32, device="cuda")
     counts = torch.empty(4, dtype=torch.int32, device="cuda")
-    req = np.arange(B, dtype=np.int32)
-    clock = 0
-    prev = None
+    prev = [None, None]
     for t in range(30):
-        sel = _random_sel(rng, B, Hkv, k, max_blk, prev, keep=0.7)
-        prev = sel
-        r = oracle.lru(op, sel, req, 0, 1, max_blk, stamp=clock + 1)
-        ops.kv_cache_lookup_insert(gp, to_torch(sel), to_torch(req), 0, 1, max_blk, k, d, 999999,
-                                   slot, hit, mk, ms, counts, ws)
-        torch.cuda.synchronize()
-        np.testing.assert_array_equal(counts.cpu().numpy(), r["counts"])
-        if r["counts"][3] == 0:
-            clock += 1
-            np.testing.assert_array_equal(slot.cpu().numpy(), r["slot"])
-        assert int(gp.clock.item()) == clock
-        _cmp_pool(gp, op, S)
+        gp.clock.fill_(t + 1)
+        for b in range(B):          # two calls per step (one per request), same stamp
+            sel = _random_sel(rng, 1, Hkv, k, max_blk, prev[b], keep=0.7)
+            prev[b] = sel
+            req = np.array([b], np.int32)
+            r = oracle.lru(op, sel, req, 0, 1, max_blk, stamp=t + 1)
+            ops.kv_cache_lookup_insert(gp, to_torch(sel), to_torch(req), 0, 1, max_blk, k, d, 999999,
+                                       slot, hit, mk, ms, counts, ws)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(counts.cpu().numpy(), r["counts"])
+            if r["counts"][3] == 0:
+                np.testing.assert_array_equal(slot.cpu().numpy(), r["slot"])
+            _cmp_pool(gp, op, S)
+        assert int(gp.clock.item()) == t + 1

@@ -132,9 +132,12 @@ def test_f32_pipeline():
                   steps=8, rho=0.9, seed=3)
 
 
-def test_request_groups_pipeline_two_streams():
+@pytest.mark.parametrize("graph_after", [None, 4])
+def test_request_groups_pipeline_two_streams(graph_after):
     """groups=2: the two request groups run on separate streams; per layer the
-    oracle makes the same two cache calls (group order, same stamp)."""
+    oracle makes the same two cache calls (group order, same stamp).  With
+    graph_after=4 the steps from 4 on are replays of one captured CUDA graph
+    whose LRU stamps come from the pools' device clocks."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     from paper_2509_24626_b200.engine import DecodeEngine, EngineConfig
@@ -172,8 +175,18 @@ def test_request_groups_pipeline_two_streams():
     host_u8 = host_np.view(np.uint8).reshape(hb, -1)
     nbk = np.array(n_blk, np.int32)
     tl = np.array(tails, np.int32)
+    graph = None
+    q_static = None
     for t in range(steps):
-        eng.step(to_torch(qs[t]), stamp=t + 1)
+        if graph_after is not None and t == graph_after:
+            eng.use_device_clock(start=t)
+            q_static = torch.empty_like(to_torch(qs[0]))
+            graph = eng.capture_graph(q_static)
+        if graph is not None:
+            q_static.copy_(to_torch(qs[t]))
+            graph.replay()
+        else:
+            eng.step(to_torch(qs[t]), stamp=t + 1)
         torch.cuda.synchronize()
         for l in range(L):
             for g in eng.groups:
