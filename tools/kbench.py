@@ -126,7 +126,7 @@ def main():
         print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}))
 
 
-if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] == "overlap"):
+if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] in ("overlap", "meta")):
     main()
 
 
@@ -182,3 +182,20 @@ def bench_overlap(c, iters=10, nmiss=1250, host_gib=None):
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "overlap":
     print(json.dumps({k: round(v, 2) for k, v in bench_overlap(CFG["C2"]).items()}))
+
+
+def bench_meta(iters=10):
+    """S0 block_meta_update over 1M blocks (bulk build, C2 physical pool size)."""
+    n = 1 << 20
+    keys = torch.randn(n * 2 * 32 * 128 // 16, 16, device="cuda").to(torch.bfloat16).view(-1)
+    meta = torch.empty(n * 2 * 128, dtype=torch.bfloat16, device="cuda")
+    def f():
+        ops.block_meta_update(keys, meta, n, key_stride=2 * 32 * 128)
+    ms = timeit(f, iters)
+    byts = n * (32 * 128 * 2 + 2 * 128 * 2)        # K half read + meta written
+    return {"kernel": "meta_update", "blocks": n, "us": ms * 1e3, "GBps": byts / ms / 1e6,
+            "frac": byts / ms / 1e6 / PEAK}
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "meta":
+    print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in bench_meta().items()}))
