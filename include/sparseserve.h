@@ -196,9 +196,92 @@ ss_status sparse_decode_attn(const void* q, const void* pool_kv, const int32_t* 
                              ss_dtype dt, float softmax_scale, const int32_t* counts,
                              float* out, void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT-1: decode KV append + save path (PAPER.md:151-153 §3.2.2, :125).
+ * Per decode step: kv_append for every layer (advance = 1 on the first layer
+ * only, so every layer writes the same row and attends the new token), then
+ * for the requests whose tail just filled: kv_seal_blocks per layer (metadata
+ * of the new block + a contiguous device staging copy), flash_d2h_save per
+ * layer (FlashD2H), and kv_commit once.
+ * ------------------------------------------------------------------------- */
+
+/* kv_append -- "the resulting KV tensor is then saved into the free slots in
+ * the corresponding KV blocks in HBM".
+ *   new_kv    device [B][Hkv][2][d] dtype dt: this step's K and V rows.
+ *   tail_kv   device [B][Hkv][2][32][d]: row tail_len[b] - 1 of each (b, h)
+ *             tail receives the new K / V row.
+ *   tail_len  device int32 [B]; if advance != 0 it is first incremented (the
+ *             new token is counted), then used.  Precondition: the resulting
+ *             tail_len is in 1..32 (rows outside are not written). */
+ss_status kv_append(const void* new_kv, void* tail_kv, int32_t* tail_len, int32_t advance,
+                    ss_dims dims, ss_dtype dt, void* stream);
+
+/* kv_seal_blocks -- "Once a KV block reaches its capacity, its associated
+ * metadata is created".  For the n_fill requests fill_req
+ * (device int32, unique, each with a full 32-token tail): the tail of every KV
+ * head is copied to staging[i][h] (device [n_fill][Hkv][2][32][d], list order)
+ * and its per-channel min/max is written to meta (tiled layout) as block
+ * n_blk[b] of (b, h).  Counters are not changed (see kv_commit).
+ *   ws   device, ss_workspace_size(SS_WS_SEAL, ...) bytes, no initialisation. */
+ss_status kv_seal_blocks(const int32_t* fill_req, int32_t n_fill, const void* tail_kv,
+                         const int32_t* n_blk, int32_t max_blk, void* meta, void* staging,
+                         void* ws, size_t ws_bytes, ss_dims dims, ss_dtype dt, void* stream);
+
+/* kv_commit -- n_blk[b] += 1 and tail_len[b] = 0 for b in fill_req (device). */
+ss_status kv_commit(const int32_t* fill_req, int32_t n_fill, int32_t* n_blk, int32_t* tail_len,
+                    void* stream);
+
+/* FlashD2H ("(1) the contiguous KV tensor is first copied
+ * into a DRAM buffer with a single memcpy, and (2) once the transfer
+ * completes, CPU threads redistribute the buffered data into the corresponding
+ * DRAM KV blocks").  An engine owns a pool of CPU threads (created/destroyed
+ * explicitly by the caller; the only library object with state).
+ * flash_d2h_save enqueues on `stream`: one cudaMemcpyAsync of n_blocks x
+ * block_bytes from device `staging` into pinned `host_buf`, then a host
+ * function that scatters block i to host_kv + (keys[i] % host_blocks) *
+ * block_bytes on the engine's threads and returns when all are written, so
+ * later work on `stream` (or waiting on an event after it) sees them.
+ *   keys      HOST int64 [n_blocks], copied at call time.
+ *   host_buf  pinned, >= n_blocks * block_bytes, untouched until the stream
+ *             passes the call.  host_kv: host memory (pinned for FlashH2D). */
+typedef struct ss_d2h_engine ss_d2h_engine;
+ss_status ss_d2h_create(int32_t num_threads, ss_d2h_engine** out);
+ss_status ss_d2h_destroy(ss_d2h_engine* engine);
+ss_status flash_d2h_save(ss_d2h_engine* engine, const void* staging, void* host_buf,
+                         int64_t n_blocks, const int64_t* keys, void* host_kv, int64_t host_blocks,
+                         int64_t block_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * NEXT-2: decoding working set + working-set-aware admission (PAPER.md:199-207
+ * §3.3, Algorithm 1).
+ * ------------------------------------------------------------------------- */
+
+/* ws_track -- "tracks the KV blocks selected over the past w decoding steps
+ * (with w = 12 by default) and regards their union as the decoding working
+ * set".  Call once per layer per step with that layer's state,
+ * after ss_block_select.  For every (b, h): ws_count[b] += |U_t| - |U_{t-1}|
+ * where U_t = union of sel over steps t-w+1..t, so after all layers of step t
+ * ws_count[b] = sum over layers and heads of |U_t| (blocks; x block bytes =
+ * the request's working set).
+ *   sel       device int32 [B][Hkv][k] (-1 = none), this layer, step t.
+ *   last_sel  device int32 [B][Hkv][max_blk], this layer: step a block was last
+ *             selected; initialise to <= -w (e.g. INT32_MIN / 2).
+ *   ring      device int32 [w][B][Hkv][k], this layer: initialise to -1.
+ *   ws_count  device int32 [B], shared by the layers; initialise to 0.
+ *   t         step index, strictly increasing by 1 per step, 0 <= t < 2^31.  */
+ss_status ws_track(const int32_t* sel, int32_t k, ss_dims dims, int32_t max_blk, int64_t t,
+                   int32_t w, int32_t* last_sel, int32_t* ring, int32_t* ws_count, void* stream);
+
+/* ss_admit -- Algorithm 1 lines 6-14: for the candidate batch in order, admit a
+ * request if M_used + M_req <= M_avl (M_used += M_req), else mark it for reset.
+ * Host arrays: ws_bytes [n] (M_req), admit_out [n] (1 admitted / 0 reset).
+ * Returns the number admitted (or -1 on invalid arguments). */
+int32_t ss_admit(const int64_t* ws_bytes, int32_t n, int64_t m_avl, uint8_t* admit_out);
+
 #define SS_WS_SELECT 0
 #define SS_WS_CACHE 1
 #define SS_WS_ATTN 2
+#define SS_WS_SEAL 3
 
 /* Workspace bytes for call `which` (SS_WS_*); num_slots is used by SS_WS_CACHE. */
 size_t ss_workspace_size(int32_t which, ss_dims dims, int32_t max_blk, int32_t k,

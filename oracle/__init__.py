@@ -50,6 +50,9 @@ def lib():
         L.or_lru.restype = ctypes.c_int
         L.or_gather.argtypes = [P, I64, P, P, ctypes.c_int32, P, I64]
         L.or_attention.argtypes = [P, P, P, I32, P, P, I32, I32, I32, I32, I32, D, P]
+        L.or_kv_append.argtypes = [P, P, P, I32, I32, I32, I32, I32]
+        L.or_kv_seal.argtypes = [P, I32, P, P, P, I32, P, P, I32, I32, I32]
+        L.or_d2h_scatter.argtypes = [P, I64, P, P, I64, I64]
         _lib = L
     return _lib
 
@@ -193,3 +196,36 @@ def decode_layer(q, meta, n_blk, k, pool: Pool, req_ids, layer, num_layers, max_
         pool_view = pool.kv.view(q.dtype).reshape(pool.num_slots, 2, 32, d)
         out = attention(q, pool_view, r["slot"], tail, tail_len, scale)
     return dict(scores=scores, sel=sel, out=out, **r)
+
+
+# --------------------------------------------------------------------------
+# NEXT-1: decode KV append + save path
+# --------------------------------------------------------------------------
+def kv_append(new_kv: np.ndarray, tail: np.ndarray, tail_len: np.ndarray, advance: bool) -> None:
+    """new_kv [B][Hkv][2][d]; tail [B][Hkv][2][32][d] (mutated); tail_len int32 [B] (mutated)."""
+    assert new_kv.dtype == tail.dtype and tail.flags["C_CONTIGUOUS"]
+    assert tail_len.dtype == np.int32 and tail_len.flags["C_CONTIGUOUS"]
+    new_kv = np.ascontiguousarray(new_kv)
+    B, Hkv, _, d = new_kv.shape
+    lib().or_kv_append(_p(new_kv), _p(tail), _p(tail_len), int(bool(advance)), B, Hkv, d, _dt(new_kv))
+
+
+def kv_seal(fill_req, tail: np.ndarray, tail_len: np.ndarray, n_blk: np.ndarray, meta: np.ndarray) -> np.ndarray:
+    """Seal the full tails of fill_req: metadata into meta [B][Hkv][max_blk][2][d]
+    (mutated), counters committed; returns the staging blocks [n][Hkv][2][32][d]."""
+    fill = np.ascontiguousarray(np.asarray(fill_req, dtype=np.int32))
+    B, Hkv, _, _, d = tail.shape
+    max_blk = meta.shape[2]
+    staging = np.empty((fill.shape[0], Hkv, 2, 32, d), dtype=tail.dtype)
+    assert meta.flags["C_CONTIGUOUS"] and n_blk.dtype == np.int32 and tail_len.dtype == np.int32
+    lib().or_kv_seal(_p(fill), int(fill.shape[0]), _p(np.ascontiguousarray(tail)), _p(tail_len),
+                     _p(n_blk), max_blk, _p(meta), _p(staging), Hkv, d, _dt(tail))
+    return staging
+
+
+def d2h_scatter(staging_u8: np.ndarray, keys, host_kv_u8: np.ndarray, host_blocks: int) -> None:
+    """staging_u8 [n][block_bytes]; host_kv_u8 [host_blocks][block_bytes] (mutated)."""
+    keys = np.ascontiguousarray(np.asarray(keys, dtype=np.int64))
+    staging_u8 = np.ascontiguousarray(staging_u8)
+    bb = staging_u8.shape[1]
+    lib().or_d2h_scatter(_p(staging_u8), int(keys.shape[0]), _p(keys), _p(host_kv_u8), host_blocks, bb)

@@ -309,3 +309,58 @@ void or_attention(const void* q, const void* pool, const int32_t* slot, int k,
     free(vsrc);
     free(voff);
 }
+
+/* ------------------------------------------------------------------------
+ * NEXT-1  decode KV append and save path.
+ * or_kv_append: "the resulting KV tensor is then saved into the
+ * free slots in the corresponding KV blocks in HBM": if advance, tail_len[b]
+ * += 1; then row tail_len[b]-1 of tail[b][h][0|1] <- new_kv[b][h][0|1].
+ * new_kv: [B][Hkv][2][d]; tail: [B][Hkv][2][32][d] (storage dtype).
+ * ---------------------------------------------------------------------- */
+void or_kv_append(const void* new_kv, void* tail, int32_t* tail_len, int advance, int B, int Hkv,
+                  int d, int dt) {
+    int64_t es = esize(dt);
+    for (int b = 0; b < B; ++b) {
+        if (advance) tail_len[b] += 1;
+        int row = tail_len[b] - 1;
+        if (row < 0 || row >= OR_BLOCK_TOKENS) continue;
+        for (int h = 0; h < Hkv; ++h)
+            for (int half = 0; half < 2; ++half)
+                memcpy((char*)tail + (((((int64_t)b * Hkv + h) * 2 + half) * OR_BLOCK_TOKENS + row) * d) * es,
+                       (const char*)new_kv + ((((int64_t)b * Hkv + h) * 2 + half) * d) * es,
+                       (size_t)(d * es));
+    }
+}
+
+/* or_kv_seal: "Once a KV block reaches its capacity, its
+ * associated metadata is created": for each listed request b (in list order)
+ * and head h: staging[i][h] <- tail[b][h]; meta[b][h][n_blk[b]] <- per-channel
+ * min/max of its 32 keys (or_block_meta); then (commit) n_blk[b] += 1,
+ * tail_len[b] = 0.  meta: logical layout [B][Hkv][max_blk][2][d]. */
+void or_kv_seal(const int32_t* fill_req, int n_fill, const void* tail, int32_t* tail_len,
+                int32_t* n_blk, int max_blk, void* meta, void* staging, int Hkv, int d, int dt) {
+    int64_t es = esize(dt);
+    int64_t blk = (int64_t)2 * OR_BLOCK_TOKENS * d;  /* elements per [2][32][d] block */
+    for (int i = 0; i < n_fill; ++i) {
+        int b = fill_req[i];
+        for (int h = 0; h < Hkv; ++h) {
+            const char* src = (const char*)tail + ((int64_t)b * Hkv + h) * blk * es;
+            memcpy((char*)staging + ((int64_t)i * Hkv + h) * blk * es, src, (size_t)(blk * es));
+            void* m = (char*)meta + ((((int64_t)b * Hkv + h) * max_blk + n_blk[b]) * 2 * d) * es;
+            or_block_meta(src, blk, 1, dt, d, m);
+        }
+    }
+    for (int i = 0; i < n_fill; ++i) {
+        n_blk[fill_req[i]] += 1;
+        tail_len[fill_req[i]] = 0;
+    }
+}
+
+/* or_d2h_scatter: "CPU threads redistribute the buffered data
+ * into the corresponding DRAM KV blocks": block i -> host_kv[keys[i] % hb]. */
+void or_d2h_scatter(const void* staging, int64_t n, const int64_t* keys, void* host_kv,
+                    int64_t host_blocks, int64_t block_bytes) {
+    for (int64_t i = 0; i < n; ++i)
+        memcpy((char*)host_kv + (keys[i] % host_blocks) * block_bytes,
+               (const char*)staging + i * block_bytes, (size_t)block_bytes);
+}

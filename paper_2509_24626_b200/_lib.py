@@ -14,11 +14,12 @@ LIB_PATH = os.path.join(PKG, "libsparseserve.so")
 
 SS_OK, SS_ERR_INVALID_ARG, SS_ERR_UNSUPPORTED, SS_ERR_CAPACITY, SS_ERR_CUDA = range(5)
 SS_BF16, SS_F32 = 0, 1
-SS_WS_SELECT, SS_WS_CACHE, SS_WS_ATTN = 0, 1, 2
+SS_WS_SELECT, SS_WS_CACHE, SS_WS_ATTN, SS_WS_SEAL = 0, 1, 2, 3
 
 EXPORTS = ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert", "flash_h2d_gather",
            "sparse_decode_attn", "ss_workspace_size", "ss_host_device_pointer",
-           "ss_status_string", "ss_version")
+           "ss_status_string", "ss_version", "kv_append", "kv_seal_blocks", "kv_commit",
+           "ss_d2h_create", "ss_d2h_destroy", "flash_d2h_save", "ws_track", "ss_admit")
 
 
 class SSDims(ctypes.Structure):
@@ -63,8 +64,20 @@ def load() -> ctypes.CDLL:
     L.ss_status_string.argtypes = [I32]
     L.ss_status_string.restype = ctypes.c_char_p
     L.ss_version.restype = ctypes.c_char_p
+    L.kv_append.argtypes = [P, P, P, I32, SSDims, I32, P]
+    L.kv_seal_blocks.argtypes = [P, I32, P, P, I32, P, P, P, SZ, SSDims, I32, P]
+    L.kv_commit.argtypes = [P, I32, P, P, P]
+    L.ss_d2h_create.argtypes = [I32, ctypes.POINTER(ctypes.c_void_p)]
+    L.ss_d2h_destroy.argtypes = [P]
+    L.flash_d2h_save.argtypes = [P, P, P, I64, P, P, I64, I64, P]
+    L.ws_track.argtypes = [P, I32, SSDims, I32, I64, I32, P, P, P, P]
+    L.ws_track.restype = I32
+    L.ss_admit.argtypes = [P, I32, I64, P]
+    L.ss_admit.restype = I32
     for name in ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert",
-                 "flash_h2d_gather", "sparse_decode_attn", "ss_host_device_pointer"):
+                 "flash_h2d_gather", "sparse_decode_attn", "ss_host_device_pointer", "kv_append",
+                 "kv_seal_blocks", "kv_commit", "ss_d2h_create", "ss_d2h_destroy",
+                 "flash_d2h_save"):
         getattr(L, name).restype = I32
     _lib = L
     return L

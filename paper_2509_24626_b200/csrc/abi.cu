@@ -25,6 +25,16 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
                              ss_dtype dt, float scale, const int32_t* counts, float* out, void* ws,
                              cudaStream_t stream);
 size_t attn_ws_bytes(const ss_dims& d, int k, ss_dtype dt);
+ss_status launch_kv_append(const void* new_kv, void* tail_kv, int32_t* tail_len, int advance,
+                           const ss_dims& d, ss_dtype dt, cudaStream_t stream);
+ss_status launch_kv_seal(const int32_t* fill_req, int n_fill, const void* tail_kv,
+                         const int32_t* n_blk, int max_blk, void* meta, void* staging, void* ws,
+                         const ss_dims& d, ss_dtype dt, cudaStream_t stream);
+ss_status launch_kv_commit(const int32_t* fill_req, int n_fill, int32_t* n_blk, int32_t* tail_len,
+                           cudaStream_t stream);
+ss_status launch_ws_track(const int32_t* sel, int k, const ss_dims& d, int max_blk, int64_t t,
+                          int w, int32_t* last_sel, int32_t* ring, int32_t* ws_count,
+                          cudaStream_t stream);
 }  // namespace ss
 
 namespace {
@@ -118,6 +128,62 @@ ss_status sparse_decode_attn(const void* q, const void* pool_kv, const int32_t* 
                                   counts, out, ws, (cudaStream_t)stream);
 }
 
+ss_status kv_append(const void* new_kv, void* tail_kv, int32_t* tail_len, int32_t advance,
+                    ss_dims dims, ss_dtype dt, void* stream) {
+    if (!new_kv || !tail_kv || !tail_len || !dt_ok(dt) || !dims_ok(dims)) return SS_ERR_INVALID_ARG;
+    if (!aligned16(new_kv) || !aligned16(tail_kv)) return SS_ERR_INVALID_ARG;
+    ss_status st = dims_supported(dims);
+    if (st != SS_OK) return st;
+    return ss::launch_kv_append(new_kv, tail_kv, tail_len, advance, dims, dt, (cudaStream_t)stream);
+}
+
+ss_status kv_seal_blocks(const int32_t* fill_req, int32_t n_fill, const void* tail_kv,
+                         const int32_t* n_blk, int32_t max_blk, void* meta, void* staging,
+                         void* ws, size_t ws_bytes, ss_dims dims, ss_dtype dt, void* stream) {
+    if (n_fill < 0 || !dt_ok(dt) || !dims_ok(dims)) return SS_ERR_INVALID_ARG;
+    if (n_fill == 0) return SS_OK;
+    if (!fill_req || !tail_kv || !n_blk || !meta || !staging || !ws) return SS_ERR_INVALID_ARG;
+    if (max_blk < 32 || (max_blk % 32) || n_fill > dims.batch) return SS_ERR_INVALID_ARG;
+    if (!aligned16(tail_kv) || !aligned16(staging)) return SS_ERR_INVALID_ARG;
+    ss_status st = dims_supported(dims);
+    if (st != SS_OK) return st;
+    if (ws_bytes < (size_t)n_fill * dims.num_kv_heads * 8) return SS_ERR_INVALID_ARG;
+    return ss::launch_kv_seal(fill_req, n_fill, tail_kv, n_blk, max_blk, meta, staging, ws, dims,
+                              dt, (cudaStream_t)stream);
+}
+
+ss_status kv_commit(const int32_t* fill_req, int32_t n_fill, int32_t* n_blk, int32_t* tail_len,
+                    void* stream) {
+    if (n_fill < 0) return SS_ERR_INVALID_ARG;
+    if (n_fill == 0) return SS_OK;
+    if (!fill_req || !n_blk || !tail_len) return SS_ERR_INVALID_ARG;
+    return ss::launch_kv_commit(fill_req, n_fill, n_blk, tail_len, (cudaStream_t)stream);
+}
+
+ss_status ws_track(const int32_t* sel, int32_t k, ss_dims dims, int32_t max_blk, int64_t t,
+                   int32_t w, int32_t* last_sel, int32_t* ring, int32_t* ws_count, void* stream) {
+    if (!sel || !last_sel || !ring || !ws_count || !dims_ok(dims)) return SS_ERR_INVALID_ARG;
+    if (k < 1 || w < 1 || max_blk < 1 || t < 0 || t >= ((int64_t)1 << 31)) return SS_ERR_INVALID_ARG;
+    return ss::launch_ws_track(sel, k, dims, max_blk, t, w, last_sel, ring, ws_count,
+                               (cudaStream_t)stream);
+}
+
+int32_t ss_admit(const int64_t* ws_bytes, int32_t n, int64_t m_avl, uint8_t* admit_out) {
+    if (n < 0 || (n > 0 && (!ws_bytes || !admit_out))) return -1;
+    int64_t used = 0;
+    int32_t admitted = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        if (used + ws_bytes[i] <= m_avl) {
+            admit_out[i] = 1;
+            used += ws_bytes[i];
+            ++admitted;
+        } else {
+            admit_out[i] = 0;
+        }
+    }
+    return admitted;
+}
+
 size_t ss_workspace_size(int32_t which, ss_dims dims, int32_t max_blk, int32_t k,
                          int32_t num_slots) {
     if (!dims_ok(dims) || k < 1) return 0;
@@ -126,6 +192,8 @@ size_t ss_workspace_size(int32_t which, ss_dims dims, int32_t max_blk, int32_t k
             return ss::select_ws_bytes(dims, max_blk, k);
         case SS_WS_CACHE:
             return ss::cache_ws_bytes(dims, k, num_slots);
+        case SS_WS_SEAL:
+            return ((size_t)dims.batch * dims.num_kv_heads * 8 + 255) & ~(size_t)255;
         case SS_WS_ATTN:
             // sized for the larger (bf16 / f32 use different warp counts)
             {

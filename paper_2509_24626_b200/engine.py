@@ -329,3 +329,61 @@ class DecodeEngine:
 
     def advance_clock(self) -> None:
         self.clock.add_(1)
+
+    # ------------------------------------------------------- NEXT-1 save path
+    def enable_save_path(self, tail_len_host: List[int], n_blk_host: List[int],
+                         d2h_threads: int = 8) -> None:
+        """Decode KV append + save: per-layer device staging for
+        sealed blocks, a pinned DRAM landing buffer, the FlashD2H CPU-thread pool
+        and a side stream.  The host mirrors of tail_len / n_blk decide (without
+        a device sync) which requests' tails fill at each step."""
+        c, dev = self.cfg, self.device
+        self.staging = torch.empty(c.layers, c.batch * c.num_kv_heads * c.block_elems, dtype=c.dtype,
+                                   device=dev)
+        self.host_stage = torch.empty(c.layers, c.batch * c.num_kv_heads * c.block_elems, dtype=c.dtype,
+                                      pin_memory=True)
+        self.seal_ws = ops.alloc_workspace(3, self.dims, c.max_blk, c.topk, device=dev)
+        self.fill_req = torch.empty(c.batch, dtype=torch.int32, device=dev)
+        self.d2h = ops.D2HEngine(d2h_threads)
+        self.d2h_stream = torch.cuda.Stream(dev)
+        self.ev_save = torch.cuda.Event()
+        self.tail_len_host = list(tail_len_host)
+        self.n_blk_host = list(n_blk_host)
+        self.req_ids_host = self.req_ids.tolist()
+
+    def append_kv(self, new_kv_all: torch.Tensor) -> None:
+        """Append this step's token: new_kv_all [L][B][Hkv][2][d] (device).  Layer 0
+        counts the token in tail_len; every layer writes the same tail row."""
+        for l in range(self.cfg.layers):
+            ops.kv_append(new_kv_all[l], self.tail_kv[l], self.tail_len, advance=(l == 0), d=self.dims)
+        self.tail_len_host = [t + 1 for t in self.tail_len_host]
+
+    def seal_full_blocks(self) -> List[int]:
+        """After the step's attention: for the requests whose tail is full, build
+        the metadata of the new block, save it to DRAM with FlashD2H on the side
+        stream, and commit (n_blk += 1, tail_len = 0).  The current stream waits
+        for the save, so the next step (which may select and miss the new block)
+        finds it in DRAM.  Returns the sealed request indices."""
+        c = self.cfg
+        fill = [b for b in range(c.batch) if self.tail_len_host[b] == BLOCK_TOKENS]
+        if not fill:
+            return []
+        n = len(fill)
+        cur = torch.cuda.current_stream(self.device)
+        self.fill_req[:n].copy_(torch.tensor(fill, dtype=torch.int32), non_blocking=False)
+        self.d2h_stream.wait_stream(cur)
+        with torch.cuda.stream(self.d2h_stream):
+            for l in range(c.layers):
+                ops.kv_seal_blocks(self.fill_req, n, self.tail_kv[l], self.n_blk, c.max_blk, self.meta[l],
+                                   self.staging[l], self.seal_ws, self.dims)
+                keys = [self.key0(self.req_ids_host[b], l, h) + self.n_blk_host[b]
+                        for b in fill for h in range(c.num_kv_heads)]
+                ops.flash_d2h_save(self.d2h, self.staging[l], self.host_stage[l], n * c.num_kv_heads,
+                                   keys, self.host_kv, self.host_blocks, c.block_bytes)
+            ops.kv_commit(self.fill_req, n, self.n_blk, self.tail_len)
+            self.ev_save.record(self.d2h_stream)
+        cur.wait_event(self.ev_save)
+        for b in fill:
+            self.n_blk_host[b] += 1
+            self.tail_len_host[b] = 0
+        return fill

@@ -149,3 +149,102 @@ def sparse_decode_attn(q: torch.Tensor, pool_kv: torch.Tensor, slot: torch.Tenso
                                          _ptr(tail_len), d, _dt(q), float(scale), _ptr(counts),
                                          _ptr(out), _ptr(ws), ws.numel(), _stream(stream)),
           "sparse_decode_attn")
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1: decode KV append + save path (FlashD2H)
+# ---------------------------------------------------------------------------
+def kv_append(new_kv: torch.Tensor, tail_kv: torch.Tensor, tail_len: torch.Tensor, advance: bool,
+              d: SSDims, stream=None) -> None:
+    """Write this step's K/V rows [B][Hkv][2][d] into row tail_len-1 of the tails
+    (tail_len incremented first when `advance`)."""
+    assert tail_len.dtype == torch.int32
+    check(_lib.load().kv_append(_ptr(new_kv), _ptr(tail_kv), _ptr(tail_len), int(bool(advance)), d,
+                                _dt(new_kv), _stream(stream)), "kv_append")
+
+
+def kv_seal_blocks(fill_req: torch.Tensor, n_fill: int, tail_kv: torch.Tensor, n_blk: torch.Tensor,
+                   max_blk: int, meta: torch.Tensor, staging: torch.Tensor, ws: torch.Tensor,
+                   d: SSDims, stream=None) -> None:
+    """Metadata + contiguous staging copy of the full tails of fill_req[:n_fill]."""
+    assert fill_req.dtype == torch.int32 and n_blk.dtype == torch.int32
+    check(_lib.load().kv_seal_blocks(_ptr(fill_req), n_fill, _ptr(tail_kv), _ptr(n_blk), max_blk,
+                                     _ptr(meta), _ptr(staging), _ptr(ws), ws.numel(), d,
+                                     _dt(tail_kv), _stream(stream)), "kv_seal_blocks")
+
+
+def kv_commit(fill_req: torch.Tensor, n_fill: int, n_blk: torch.Tensor, tail_len: torch.Tensor,
+              stream=None) -> None:
+    check(_lib.load().kv_commit(_ptr(fill_req), n_fill, _ptr(n_blk), _ptr(tail_len),
+                                _stream(stream)), "kv_commit")
+
+
+class D2HEngine:
+    """FlashD2H CPU-thread pool (owned here, freed on close/garbage collection)."""
+
+    def __init__(self, num_threads: int = 8):
+        import ctypes
+        h = ctypes.c_void_p()
+        check(_lib.load().ss_d2h_create(num_threads, ctypes.byref(h)), "ss_d2h_create")
+        self.handle = h.value
+
+    def close(self) -> None:
+        if self.handle:
+            _lib.load().ss_d2h_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def flash_d2h_save(engine: D2HEngine, staging: torch.Tensor, host_buf: torch.Tensor, n_blocks: int,
+                   keys_host, host_kv: torch.Tensor, host_blocks: int, block_bytes: int,
+                   stream=None) -> None:
+    """One D2H copy of n_blocks staged blocks into pinned host_buf, then CPU-thread
+    scatter to host_kv[key % host_blocks] (keys: host int64 sequence)."""
+    import ctypes
+    import numpy as np
+    keys = np.ascontiguousarray(np.asarray(keys_host, dtype=np.int64))
+    assert keys.shape[0] >= n_blocks
+    check(_lib.load().flash_d2h_save(engine.handle, _ptr(staging), host_buf.data_ptr(), n_blocks,
+                                     keys.ctypes.data_as(ctypes.c_void_p), host_kv.data_ptr(),
+                                     host_blocks, block_bytes, _stream(stream)), "flash_d2h_save")
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: decoding working set (w-step union of selections) + Algorithm 1
+# ---------------------------------------------------------------------------
+class WorkingSetState:
+    """Per-layer last-selected steps and selection rings + per-request counts."""
+
+    def __init__(self, layers: int, batch: int, num_kv_heads: int, max_blk: int, k: int, w: int = 12,
+                 device=None):
+        device = device or "cuda"
+        self.w = w
+        self.last_sel = torch.full((layers, batch, num_kv_heads, max_blk), -(1 << 30),
+                                   dtype=torch.int32, device=device)
+        self.ring = torch.full((layers, w, batch, num_kv_heads, k), -1, dtype=torch.int32, device=device)
+        self.ws_count = torch.zeros(batch, dtype=torch.int32, device=device)
+
+
+def ws_track(state: WorkingSetState, layer: int, sel: torch.Tensor, k: int, d: SSDims, max_blk: int,
+             t: int, stream=None) -> None:
+    check(_lib.load().ws_track(_ptr(sel), k, d, max_blk, int(t), state.w, _ptr(state.last_sel[layer]),
+                               _ptr(state.ring[layer]), _ptr(state.ws_count), _stream(stream)),
+          "ws_track")
+
+
+def ss_admit(ws_bytes, m_avl: int):
+    """Algorithm 1 admission over candidates in order; returns a bool list."""
+    import ctypes
+    import numpy as np
+    ws = np.ascontiguousarray(np.asarray(ws_bytes, dtype=np.int64))
+    out = np.zeros(ws.shape[0], dtype=np.uint8)
+    n = _lib.load().ss_admit(ws.ctypes.data_as(ctypes.c_void_p), int(ws.shape[0]), int(m_avl),
+                             out.ctypes.data_as(ctypes.c_void_p))
+    if n < 0:
+        raise _lib.SparseServeError("ss_admit: invalid arguments")
+    return [bool(x) for x in out]

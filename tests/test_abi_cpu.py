@@ -81,3 +81,21 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "nope.so"))
     with pytest.raises(ImportError):
         _lib.load()
+
+
+def test_ss_admit_matches_algorithm1(lib):
+    # PAPER.md:159-183 Algorithm 1 lines 6-14, restated in Python as the check
+    from paper_2509_24626_b200 import ops
+    import random
+    rnd = random.Random(5)
+    for _ in range(50):
+        ws = [rnd.randint(0, 100) for _ in range(rnd.randint(0, 20))]
+        m_avl = rnd.randint(0, 400)
+        used, exp = 0, []
+        for m in ws:
+            if used + m <= m_avl:
+                exp.append(True)
+                used += m
+            else:
+                exp.append(False)
+        assert ops.ss_admit(ws, m_avl) == exp

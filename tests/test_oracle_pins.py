@@ -364,3 +364,47 @@ def test_block_geometry_golden():
     assert fx["block_tokens"] * fx["head_dim"] * 2 * 2 == fx["bytes_per_head_block_kv_2byte"]
     assert synth.BLOCK_TOKENS == fx["block_tokens"] and synth.HEAD_DIM == fx["head_dim"]
     assert fx["token_budget"] // fx["block_tokens"] == synth.C2.topk
+
+
+# ----------------------------------------------------------------------------
+# NEXT-1: append / seal / FlashD2H scatter
+# ----------------------------------------------------------------------------
+def test_kv_append_and_seal_match_numpy():
+    rng = synth.rng_for(900, 20)
+    B, Hkv, max_blk = 3, 2, 64
+    tail = np.zeros((B, Hkv, 2, 32, D), np.uint16)
+    tail_len = np.array([0, 29, 5], np.int32)
+    n_blk = np.array([3, 7, 0], np.int32)
+    meta = np.zeros((B, Hkv, max_blk, 2, D), np.uint16)
+    ref_tail = tail.copy()
+    ref_len = tail_len.copy()
+    for step in range(3):
+        new = synth.encode(rng.standard_normal((B, Hkv, 2, D)), synth.DT_BF16)
+        oracle.kv_append(new, tail, tail_len, advance=True)
+        for b in range(B):                      # numpy slicing: the definition of "append"
+            ref_len[b] += 1
+            ref_tail[b, :, :, ref_len[b] - 1] = new[b]
+        np.testing.assert_array_equal(tail, ref_tail)
+        np.testing.assert_array_equal(tail_len, ref_len)
+        # a second layer writes the same row without advancing
+        oracle.kv_append(new, tail, tail_len, advance=False)
+        np.testing.assert_array_equal(tail, ref_tail)
+    assert tail_len[1] == 32
+    full = tail[1].copy()
+    staging = oracle.kv_seal([1], tail, tail_len, n_blk, meta)
+    np.testing.assert_array_equal(staging[0], full)
+    vals = _val(full[:, 0])                       # [Hkv][32][d] keys
+    np.testing.assert_array_equal(_val(meta[1, :, 7, 0]), vals.min(axis=1))
+    np.testing.assert_array_equal(_val(meta[1, :, 7, 1]), vals.max(axis=1))
+    assert n_blk.tolist() == [3, 8, 0] and tail_len[1] == 0
+
+
+def test_d2h_scatter_matches_numpy():
+    rng = np.random.default_rng(3)
+    st = rng.integers(0, 256, size=(5, 64), dtype=np.uint8)
+    host = rng.integers(0, 256, size=(11, 64), dtype=np.uint8)
+    keys = np.array([3, 14, 9, 0, 21], np.int64)
+    exp = host.copy()
+    exp[keys % 11] = st
+    oracle.d2h_scatter(st, keys, host, 11)
+    np.testing.assert_array_equal(host, exp)

@@ -126,7 +126,7 @@ def main():
         print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}))
 
 
-if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] in ("overlap", "meta")):
+if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] in ("overlap", "meta", "d2h")):
     main()
 
 
@@ -199,3 +199,44 @@ def bench_meta(iters=10):
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "meta":
     print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in bench_meta().items()}))
+
+
+def bench_d2h(n=2048, threads=8, iters=5):
+    """FlashD2H (one D2H memcpy + CPU-thread scatter) vs one cudaMemcpy per 16 KiB
+    block (Fig. 4b analog)."""
+    bb = 16384
+    hb = (4 << 30) // bb
+    host = torch.empty(hb * bb, dtype=torch.uint8, pin_memory=True)
+    hview = host.view(hb, bb)
+    stage_dev = torch.randint(0, 255, (n, bb), dtype=torch.uint8, device="cuda")
+    landing = torch.empty(n * bb, dtype=torch.uint8, pin_memory=True)
+    keys = torch.randperm(hb)[:n].tolist()
+    eng = ops.D2HEngine(threads)
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    res = {}
+    for _ in range(2):
+        ops.flash_d2h_save(eng, stage_dev, landing, n, keys, host, hb, bb)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(iters):
+        ops.flash_d2h_save(eng, stage_dev, landing, n, keys, host, hb, bb)
+    e.record()
+    torch.cuda.synchronize()
+    res["flash_d2h_GBps"] = iters * n * bb / (s.elapsed_time(e) * 1e-3) / 1e9
+    ok = all(torch.equal(hview[keys[i]], stage_dev[i].cpu()) for i in range(0, n, max(1, n // 64)))
+    s.record()
+    for i in range(n):
+        hview[keys[i]].copy_(stage_dev[i], non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    res["per_block_memcpy_GBps"] = n * bb / (s.elapsed_time(e) * 1e-3) / 1e9
+    res["blocks"] = n
+    res["threads"] = threads
+    res["byte_exact"] = bool(ok)
+    eng.close()
+    return res
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "d2h":
+    for th in (1, 4, 8, 16):
+        print(json.dumps({k: (round(v, 2) if isinstance(v, float) else v) for k, v in bench_d2h(threads=th).items()}))
