@@ -278,10 +278,32 @@ ss_status ws_track(const int32_t* sel, int32_t k, ss_dims dims, int32_t max_blk,
  * Returns the number admitted (or -1 on invalid arguments). */
 int32_t ss_admit(const int64_t* ws_bytes, int32_t n, int64_t m_avl, uint8_t* admit_out);
 
+/* ---------------------------------------------------------------------------
+ * NEXT-4: layer-segmented prefill, storage side (§3.4: "The KV
+ * blocks of all finished layers can be immediately evicted after being saved
+ * to DRAM"; (N,H,D) -> (H,N,D) blocks).
+ * prefill_layer_save -- one prefill layer of one request (batch slot b, request
+ * id req): k_nhd / v_nhd device [n_tok][Hkv][d] ((N,H,D) projection output).
+ * Full blocks j < n_tok/32 of every head are re-laid out into staging (device
+ * [Hkv][n_tok/32][2][32][d]), their metadata written (tiled meta, index
+ * (b*Hkv+h)*max_blk + j) and saved to their DRAM home host_kv + (key %
+ * host_blocks) * block_bytes, key = ((req*L + layer)*Hkv + h)*max_blk + j, with
+ * one DMA copy per head (requires host_blocks % max_blk == 0: a head's blocks are
+ * contiguous there); the remaining n_tok % 32 tokens become the tail (rows of
+ * tail_kv[b][h]); n_blk[b] = n_tok/32, tail_len[b] = n_tok % 32.
+ *   ws  device, ss_workspace_size(SS_WS_PREFILL, dims, max_blk, ...) bytes.
+ * host_kv: pinned host memory (HOST address). n_tok <= 32 * max_blk. */
+ss_status prefill_layer_save(const void* k_nhd, const void* v_nhd, int32_t n_tok, int32_t b,
+                             int32_t req, int32_t layer, int32_t num_layers, int32_t max_blk,
+                             ss_dims dims, ss_dtype dt, void* staging, void* meta, void* tail_kv,
+                             int32_t* n_blk, int32_t* tail_len, void* host_kv, int64_t host_blocks,
+                             void* ws, size_t ws_bytes, void* stream);
+
 #define SS_WS_SELECT 0
 #define SS_WS_CACHE 1
 #define SS_WS_ATTN 2
 #define SS_WS_SEAL 3
+#define SS_WS_PREFILL 4
 
 /* Workspace bytes for call `which` (SS_WS_*); num_slots is used by SS_WS_CACHE. */
 size_t ss_workspace_size(int32_t which, ss_dims dims, int32_t max_blk, int32_t k,

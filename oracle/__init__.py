@@ -53,6 +53,8 @@ def lib():
         L.or_kv_append.argtypes = [P, P, P, I32, I32, I32, I32, I32]
         L.or_kv_seal.argtypes = [P, I32, P, P, P, I32, P, P, I32, I32, I32]
         L.or_d2h_scatter.argtypes = [P, I64, P, P, I64, I64]
+        L.or_prefill_save.argtypes = [P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P,
+                                      P, I64]
         _lib = L
     return _lib
 
@@ -229,3 +231,22 @@ def d2h_scatter(staging_u8: np.ndarray, keys, host_kv_u8: np.ndarray, host_block
     staging_u8 = np.ascontiguousarray(staging_u8)
     bb = staging_u8.shape[1]
     lib().or_d2h_scatter(_p(staging_u8), int(keys.shape[0]), _p(keys), _p(host_kv_u8), host_blocks, bb)
+
+
+# --------------------------------------------------------------------------
+# NEXT-4: layer-segmented prefill, storage side
+# --------------------------------------------------------------------------
+def prefill_save(k_nhd: np.ndarray, v_nhd: np.ndarray, b: int, req: int, layer: int, num_layers: int,
+                 meta: np.ndarray, tail: np.ndarray, n_blk: np.ndarray, tail_len: np.ndarray,
+                 host_kv_u8: np.ndarray, host_blocks: int) -> None:
+    """k/v [n][Hkv][d]; meta [B][Hkv][max_blk][2][d], tail [B][Hkv][2][32][d], n_blk/tail_len
+    int32 [B] and host_kv_u8 [host_blocks][block_bytes] are mutated."""
+    k_nhd = np.ascontiguousarray(k_nhd)
+    v_nhd = np.ascontiguousarray(v_nhd)
+    n, Hkv, d = k_nhd.shape
+    max_blk = meta.shape[2]
+    for a in (meta, tail, n_blk, tail_len, host_kv_u8):
+        assert a.flags["C_CONTIGUOUS"]
+    lib().or_prefill_save(_p(k_nhd), _p(v_nhd), n, b, req, layer, num_layers, max_blk, Hkv, d,
+                          _dt(k_nhd), _p(meta), _p(tail), _p(n_blk), _p(tail_len), _p(host_kv_u8),
+                          int(host_blocks))

@@ -364,3 +364,45 @@ void or_d2h_scatter(const void* staging, int64_t n, const int64_t* keys, void* h
         memcpy((char*)host_kv + (keys[i] % host_blocks) * block_bytes,
                (const char*)staging + i * block_bytes, (size_t)block_bytes);
 }
+
+/* ------------------------------------------------------------------------
+ * NEXT-4  layer-segmented prefill, storage side (§3.4;
+ * (N,H,D) -> (H,N,D) blocks): one layer of one request.
+ *   k, v: [n_tok][Hkv][d] (N,H,D).  For head h and full block j < n_tok/32:
+ *   block[h][j] = {K rows 32j..32j+31 of head h, V rows ...} ([2][32][d]);
+ *   meta[b][h][j] = or_block_meta(block); host_kv[key % hb] = block with
+ *   key = ((req*L + layer)*Hkv + h)*max_blk + j; the n_tok % 32 remaining rows
+ *   go to tail[b][h][0|1][0..rem); n_blk[b] = n_tok/32, tail_len[b] = rem.
+ *   meta: logical [B][Hkv][max_blk][2][d]; tail: [B][Hkv][2][32][d].
+ * ---------------------------------------------------------------------- */
+void or_prefill_save(const void* k, const void* v, int n_tok, int b, int req, int layer, int L,
+                     int max_blk, int Hkv, int d, int dt, void* meta, void* tail, int32_t* n_blk,
+                     int32_t* tail_len, void* host_kv, int64_t host_blocks) {
+    int64_t es = esize(dt);
+    int64_t row = (int64_t)d * es;
+    int64_t bb = 2 * OR_BLOCK_TOKENS * row;
+    int nb = n_tok / OR_BLOCK_TOKENS, rem = n_tok % OR_BLOCK_TOKENS;
+    char* blk = (char*)malloc((size_t)bb);
+    for (int h = 0; h < Hkv; ++h) {
+        for (int j = 0; j < nb; ++j) {
+            for (int t = 0; t < OR_BLOCK_TOKENS; ++t) {
+                int64_t tok = (int64_t)j * OR_BLOCK_TOKENS + t;
+                memcpy(blk + t * row, (const char*)k + (tok * Hkv + h) * row, (size_t)row);
+                memcpy(blk + (OR_BLOCK_TOKENS + t) * row, (const char*)v + (tok * Hkv + h) * row, (size_t)row);
+            }
+            or_block_meta(blk, 2 * OR_BLOCK_TOKENS * d, 1, dt, d,
+                          (char*)meta + ((((int64_t)b * Hkv + h) * max_blk + j) * 2 * d) * es);
+            int64_t key = (((int64_t)req * L + layer) * Hkv + h) * max_blk + j;
+            memcpy((char*)host_kv + (key % host_blocks) * bb, blk, (size_t)bb);
+        }
+        for (int t = 0; t < rem; ++t) {
+            int64_t tok = (int64_t)nb * OR_BLOCK_TOKENS + t;
+            char* tb = (char*)tail + ((int64_t)b * Hkv + h) * bb;
+            memcpy(tb + t * row, (const char*)k + (tok * Hkv + h) * row, (size_t)row);
+            memcpy(tb + (OR_BLOCK_TOKENS + t) * row, (const char*)v + (tok * Hkv + h) * row, (size_t)row);
+        }
+    }
+    n_blk[b] = nb;
+    tail_len[b] = rem;
+    free(blk);
+}

@@ -14,12 +14,12 @@ LIB_PATH = os.path.join(PKG, "libsparseserve.so")
 
 SS_OK, SS_ERR_INVALID_ARG, SS_ERR_UNSUPPORTED, SS_ERR_CAPACITY, SS_ERR_CUDA = range(5)
 SS_BF16, SS_F32 = 0, 1
-SS_WS_SELECT, SS_WS_CACHE, SS_WS_ATTN, SS_WS_SEAL = 0, 1, 2, 3
+SS_WS_SELECT, SS_WS_CACHE, SS_WS_ATTN, SS_WS_SEAL, SS_WS_PREFILL = 0, 1, 2, 3, 4
 
 EXPORTS = ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert", "flash_h2d_gather",
            "sparse_decode_attn", "ss_workspace_size", "ss_host_device_pointer",
            "ss_status_string", "ss_version", "kv_append", "kv_seal_blocks", "kv_commit",
-           "ss_d2h_create", "ss_d2h_destroy", "flash_d2h_save", "ws_track", "ss_admit")
+           "ss_d2h_create", "ss_d2h_destroy", "flash_d2h_save", "ws_track", "ss_admit", "prefill_layer_save")
 
 
 class SSDims(ctypes.Structure):
@@ -73,6 +73,9 @@ def load() -> ctypes.CDLL:
     L.ws_track.argtypes = [P, I32, SSDims, I32, I64, I32, P, P, P, P]
     L.ws_track.restype = I32
     L.ss_admit.argtypes = [P, I32, I64, P]
+    L.prefill_layer_save.argtypes = [P, P, I32, I32, I32, I32, I32, I32, SSDims, I32, P, P, P, P, P,
+                                     P, I64, P, SZ, P]
+    L.prefill_layer_save.restype = I32
     L.ss_admit.restype = I32
     for name in ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert",
                  "flash_h2d_gather", "sparse_decode_attn", "ss_host_device_pointer", "kv_append",

@@ -32,6 +32,11 @@ ss_status launch_kv_seal(const int32_t* fill_req, int n_fill, const void* tail_k
                          const ss_dims& d, ss_dtype dt, cudaStream_t stream);
 ss_status launch_kv_commit(const int32_t* fill_req, int n_fill, int32_t* n_blk, int32_t* tail_len,
                            cudaStream_t stream);
+ss_status launch_prefill_layer_save(const void* k_nhd, const void* v_nhd, int n_tok, int b, int req,
+                                    int layer, int num_layers, int max_blk, const ss_dims& d,
+                                    ss_dtype dt, void* staging, void* meta, void* tail_kv,
+                                    int32_t* n_blk, int32_t* tail_len, void* host_kv,
+                                    int64_t host_blocks, void* ws, cudaStream_t stream);
 ss_status launch_ws_track(const int32_t* sel, int k, const ss_dims& d, int max_blk, int64_t t,
                           int w, int32_t* last_sel, int32_t* ring, int32_t* ws_count,
                           cudaStream_t stream);
@@ -168,6 +173,28 @@ ss_status ws_track(const int32_t* sel, int32_t k, ss_dims dims, int32_t max_blk,
                                (cudaStream_t)stream);
 }
 
+ss_status prefill_layer_save(const void* k_nhd, const void* v_nhd, int32_t n_tok, int32_t b,
+                             int32_t req, int32_t layer, int32_t num_layers, int32_t max_blk,
+                             ss_dims dims, ss_dtype dt, void* staging, void* meta, void* tail_kv,
+                             int32_t* n_blk, int32_t* tail_len, void* host_kv, int64_t host_blocks,
+                             void* ws, size_t ws_bytes, void* stream) {
+    if (!k_nhd || !v_nhd || !staging || !meta || !tail_kv || !n_blk || !tail_len || !host_kv || !ws)
+        return SS_ERR_INVALID_ARG;
+    if (!dt_ok(dt) || !dims_ok(dims) || n_tok < 0 || b < 0 || b >= dims.batch || req < 0)
+        return SS_ERR_INVALID_ARG;
+    if (max_blk < 32 || (max_blk % 32) || (int64_t)n_tok > 32LL * max_blk) return SS_ERR_INVALID_ARG;
+    if (layer < 0 || layer >= num_layers || host_blocks < max_blk || (host_blocks % max_blk))
+        return SS_ERR_INVALID_ARG;
+    if (!aligned16(k_nhd) || !aligned16(v_nhd) || !aligned16(staging) || !aligned16(tail_kv))
+        return SS_ERR_INVALID_ARG;
+    ss_status st = dims_supported(dims);
+    if (st != SS_OK) return st;
+    if (ws_bytes < (size_t)dims.num_kv_heads * max_blk * 8) return SS_ERR_INVALID_ARG;
+    return ss::launch_prefill_layer_save(k_nhd, v_nhd, n_tok, b, req, layer, num_layers, max_blk, dims,
+                                         dt, staging, meta, tail_kv, n_blk, tail_len, host_kv,
+                                         host_blocks, ws, (cudaStream_t)stream);
+}
+
 int32_t ss_admit(const int64_t* ws_bytes, int32_t n, int64_t m_avl, uint8_t* admit_out) {
     if (n < 0 || (n > 0 && (!ws_bytes || !admit_out))) return -1;
     int64_t used = 0;
@@ -194,6 +221,8 @@ size_t ss_workspace_size(int32_t which, ss_dims dims, int32_t max_blk, int32_t k
             return ss::cache_ws_bytes(dims, k, num_slots);
         case SS_WS_SEAL:
             return ((size_t)dims.batch * dims.num_kv_heads * 8 + 255) & ~(size_t)255;
+        case SS_WS_PREFILL:
+            return ((size_t)dims.num_kv_heads * max_blk * 8 + 255) & ~(size_t)255;
         case SS_WS_ATTN:
             // sized for the larger (bf16 / f32 use different warp counts)
             {

@@ -270,3 +270,79 @@ ss_status flash_d2h_save(ss_d2h_engine* eng, const void* staging, void* host_buf
 }
 
 }  // extern "C"
+
+// ---- NEXT-4: layer-segmented prefill, storage side ------------------------------
+// (§3.4: "The KV blocks of all finished layers can be
+// immediately evicted after being saved to DRAM"; P:129/137 (N,H,D) -> (H,N,D)).
+// One prefill layer of one request: the projection output K, V [n][Hkv][d]
+// ((N,H,D) layout) is re-laid out on the GPU into per-head 32-token blocks
+// [Hkv][nb][2][32][d] (staging) + the partial tail, the metadata of every full
+// block is built, and since the blocks of one (request, layer, head) are
+// contiguous in their DRAM home (keys j = 0..nb-1 are consecutive), the save is
+// Hkv large DMA copies (cudaMemcpyAsync) -- no SM or CPU work for the bytes.
+namespace ss {
+
+__global__ void __launch_bounds__(kSaveThreads)
+prefill_relayout_kernel(const uint4* __restrict__ k_nhd, const uint4* __restrict__ v_nhd, int n_tok,
+                        int nb, int Hkv, int row_vecs, int b, int max_blk, uint4* __restrict__ staging,
+                        uint4* __restrict__ tail, int64_t* __restrict__ dst_idx) {
+    const int j = blockIdx.x, h = blockIdx.y;
+    const int block_vecs = 2 * kBlockTokens * row_vecs;
+    uint4* dst = j < nb ? staging + ((int64_t)h * nb + j) * block_vecs
+                        : tail + ((int64_t)b * Hkv + h) * block_vecs;
+    for (int i = threadIdx.x; i < block_vecs; i += kSaveThreads) {
+        const int half = i / (kBlockTokens * row_vecs);
+        const int t = (i / row_vecs) % kBlockTokens;
+        const int v = i % row_vecs;
+        const int64_t tok = (int64_t)j * kBlockTokens + t;
+        if (tok < n_tok) {
+            const uint4* src = half ? v_nhd : k_nhd;
+            dst[i] = src[(tok * Hkv + h) * row_vecs + v];
+        } else if (j < nb) {
+            // (cannot happen: full blocks only)
+        }
+    }
+    if (threadIdx.x == 0 && j < nb) dst_idx[(int64_t)h * nb + j] = ((int64_t)b * Hkv + h) * max_blk + j;
+}
+
+__global__ void prefill_counters_kernel(int32_t* n_blk, int32_t* tail_len, int b, int nb, int rem) {
+    n_blk[b] = nb;
+    tail_len[b] = rem;
+}
+
+ss_status launch_prefill_layer_save(const void* k_nhd, const void* v_nhd, int n_tok, int b, int req,
+                                    int layer, int num_layers, int max_blk, const ss_dims& d,
+                                    ss_dtype dt, void* staging, void* meta, void* tail_kv,
+                                    int32_t* n_blk, int32_t* tail_len, void* host_kv,
+                                    int64_t host_blocks, void* ws, cudaStream_t stream) {
+    const int es = dt == SS_BF16 ? 2 : 4;
+    const int row_vecs = kHeadDim * es / 16;
+    const int nb = n_tok / kBlockTokens, rem = n_tok % kBlockTokens;
+    const int Hkv = d.num_kv_heads;
+    const int64_t bb = 2LL * kBlockTokens * kHeadDim * es;
+    int64_t* dst_idx = (int64_t*)ws;
+    const int grid_x = nb + (rem ? 1 : 0);
+    if (grid_x > 0) {
+        prefill_relayout_kernel<<<dim3(grid_x, Hkv), kSaveThreads, 0, stream>>>(
+            (const uint4*)k_nhd, (const uint4*)v_nhd, n_tok, nb, Hkv, row_vecs, b, max_blk,
+            (uint4*)staging, (uint4*)tail_kv, dst_idx);
+        SS_LAUNCH_CHECK();
+    }
+    if (nb > 0) {
+        ss_status st = launch_meta_update(staging, 2 * kBlockTokens * kHeadDim, dst_idx,
+                                          (int64_t)nb * Hkv, meta, dt, stream);
+        if (st != SS_OK) return st;
+        for (int h = 0; h < Hkv; ++h) {
+            const int64_t key0 = (((int64_t)req * num_layers + layer) * Hkv + h) * max_blk;
+            const int64_t phys0 = key0 % host_blocks;
+            if (cudaMemcpyAsync((char*)host_kv + phys0 * bb, (const char*)staging + (int64_t)h * nb * bb,
+                                (size_t)(nb * bb), cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+                return SS_ERR_CUDA;
+        }
+    }
+    prefill_counters_kernel<<<1, 1, 0, stream>>>(n_blk, tail_len, b, nb, rem);
+    SS_LAUNCH_CHECK();
+    return SS_OK;
+}
+
+}  // namespace ss

@@ -248,3 +248,20 @@ def ss_admit(ws_bytes, m_avl: int):
     if n < 0:
         raise _lib.SparseServeError("ss_admit: invalid arguments")
     return [bool(x) for x in out]
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: layer-segmented prefill, storage side
+# ---------------------------------------------------------------------------
+def prefill_layer_save(k_nhd: torch.Tensor, v_nhd: torch.Tensor, n_tok: int, b: int, req: int,
+                       layer: int, num_layers: int, max_blk: int, d: SSDims, staging: torch.Tensor,
+                       meta: torch.Tensor, tail_kv: torch.Tensor, n_blk: torch.Tensor,
+                       tail_len: torch.Tensor, host_kv: torch.Tensor, host_blocks: int,
+                       ws: torch.Tensor, stream=None) -> None:
+    """(N,H,D) prefill KV of one layer -> per-head blocks + metadata + DMA save to DRAM + tail."""
+    assert host_kv.is_pinned()
+    check(_lib.load().prefill_layer_save(_ptr(k_nhd), _ptr(v_nhd), n_tok, b, req, layer, num_layers,
+                                         max_blk, d, _dt(k_nhd), _ptr(staging), _ptr(meta),
+                                         _ptr(tail_kv), _ptr(n_blk), _ptr(tail_len),
+                                         host_kv.data_ptr(), host_blocks, _ptr(ws), ws.numel(),
+                                         _stream(stream)), "prefill_layer_save")

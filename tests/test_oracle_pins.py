@@ -408,3 +408,32 @@ def test_d2h_scatter_matches_numpy():
     exp[keys % 11] = st
     oracle.d2h_scatter(st, keys, host, 11)
     np.testing.assert_array_equal(host, exp)
+
+
+def test_prefill_save_matches_numpy_relayout():
+    # NEXT-4: (N,H,D) -> per-head 32-token blocks, metadata,
+    # DRAM home of each block, tail -- checked with numpy reshapes / transposes
+    rng = synth.rng_for(900, 30)
+    n, Hkv, L, layer, max_blk, B, b, req = 32 * 5 + 11, 3, 4, 2, 32, 2, 1, 1
+    k = synth.encode(rng.standard_normal((n, Hkv, D)), synth.DT_BF16)
+    v = synth.encode(rng.standard_normal((n, Hkv, D)), synth.DT_BF16)
+    meta = np.zeros((B, Hkv, max_blk, 2, D), np.uint16)
+    tail = np.zeros((B, Hkv, 2, 32, D), np.uint16)
+    n_blk = np.zeros(B, np.int32)
+    tl = np.zeros(B, np.int32)
+    hb = B * L * Hkv * max_blk
+    host = np.zeros((hb, 2 * 32 * D * 2), np.uint8)
+    oracle.prefill_save(k, v, b, req, layer, L, meta, tail, n_blk, tl, host, hb)
+    nb = n // 32
+    blocks = np.stack([k[:nb * 32].reshape(nb, 32, Hkv, D), v[:nb * 32].reshape(nb, 32, Hkv, D)], axis=1)
+    blocks = blocks.transpose(3, 0, 1, 2, 4)          # [Hkv][nb][2][32][d]
+    for h in range(Hkv):
+        key0 = ((req * L + layer) * Hkv + h) * max_blk
+        got = host[key0:key0 + nb].view(np.uint16).reshape(nb, 2, 32, D)
+        np.testing.assert_array_equal(got, blocks[h])
+        vals = _val(blocks[h][:, 0])
+        np.testing.assert_array_equal(_val(meta[b, h, :nb, 0]), vals.min(axis=1))
+        np.testing.assert_array_equal(_val(meta[b, h, :nb, 1]), vals.max(axis=1))
+        np.testing.assert_array_equal(tail[b, h, 0, :11], k[nb * 32:, h])
+        np.testing.assert_array_equal(tail[b, h, 1, :11], v[nb * 32:, h])
+    assert n_blk[b] == nb and tl[b] == 11

@@ -126,7 +126,7 @@ def main():
         print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}))
 
 
-if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] in ("overlap", "meta", "d2h")):
+if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] in ("overlap", "meta", "d2h", "prefill")):
     main()
 
 
@@ -240,3 +240,32 @@ def bench_d2h(n=2048, threads=8, iters=5):
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "d2h":
     for th in (1, 4, 8, 16):
         print(json.dumps({k: (round(v, 2) if isinstance(v, float) else v) for k, v in bench_d2h(threads=th).items()}))
+
+
+def bench_prefill(n_tok=131072, Hkv=32, max_blk=4096, iters=3):
+    """NEXT-4: one 128K-token prefill layer of one request (LWM-7B heads): GPU
+    relayout + metadata + one DMA save per head into pinned DRAM."""
+    d = ops.dims(1, Hkv, Hkv)
+    k = torch.randn(n_tok, Hkv, 128, device="cuda").to(torch.bfloat16)
+    v = torch.randn(n_tok, Hkv, 128, device="cuda").to(torch.bfloat16)
+    nb = n_tok // 32
+    staging = torch.empty(Hkv * max_blk * 8192, dtype=torch.bfloat16, device="cuda")
+    meta = torch.empty(Hkv * max_blk * 256, dtype=torch.bfloat16, device="cuda")
+    tail = torch.zeros(Hkv * 8192, dtype=torch.bfloat16, device="cuda")
+    n_blk = torch.zeros(1, dtype=torch.int32, device="cuda")
+    tl = torch.zeros(1, dtype=torch.int32, device="cuda")
+    hb = Hkv * max_blk
+    host = torch.empty(hb * 8192, dtype=torch.bfloat16, pin_memory=True)
+    ws = ops.alloc_workspace(4, d, max_blk, 64)
+
+    def f():
+        ops.prefill_layer_save(k, v, n_tok, 0, 0, 0, 1, max_blk, d, staging, meta, tail, n_blk, tl,
+                               host, hb, ws)
+    ms = timeit(f, iters, warm=1)
+    byts = nb * Hkv * 16384
+    return {"kernel": "prefill_layer_save", "tokens": n_tok, "us": ms * 1e3,
+            "dram_save_GBps": byts / ms / 1e6}
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "prefill":
+    print(json.dumps({k: (round(v, 2) if isinstance(v, float) else v) for k, v in bench_prefill().items()}))
