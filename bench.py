@@ -101,8 +101,10 @@ class ClockSampler:
 # workload
 # ----------------------------------------------------------------------------
 def workload_cfg(args, world: int):
-    wl = synth.C2
-    batch = wl.batch * world                     # weak scaling: 16 requests per GPU
+    # C2 (BASELINE.json configs[1], the metric's config) by default; C3
+    # (configs[2], Llama-3-8B GQA 1M-context FlashH2D stress) with --config C3
+    wl = synth.C3 if args.config == "C3" else synth.C2
+    batch = wl.batch * world                     # weak scaling: per-GPU batch fixed
     assert wl.num_kv_heads % world == 0, "KV heads must divide across ranks"
     return dict(name=wl.name, batch=batch, layers=wl.layers, num_q_heads=wl.num_q_heads,
                 num_kv_heads=wl.num_kv_heads, n_blk=wl.n_blk, max_blk=wl.max_blk, topk=wl.topk,
@@ -138,7 +140,7 @@ def setup_engine(args, rank: int, world: int):
                        num_requests=W["batch"], dtype=torch.bfloat16, groups=args.groups)
     eng = DecodeEngine(cfg)
     # physical host pool: a prime number of max_blk runs (aliasing, R15)
-    runs = args.host_runs
+    runs = args.host_runs if cfg.max_blk <= 4096 else max(1, (args.host_runs * 4096) // cfg.max_blk)
     phys = runs * cfg.max_blk
     host_t = torch.empty(phys * cfg.block_elems, dtype=torch.bfloat16, pin_memory=True)
     meta_phys = torch.empty(phys * 2 * 128, dtype=torch.bfloat16, device="cuda")
@@ -244,22 +246,26 @@ def measure_h2d_peak(nbytes=1 << 30):
 
 def cpu_sample(eng, W, q_np_step, n_req=1, n_layers=1):
     """Time the oracle (as it stands, single thread) on a bounded sample of the
-    same workload: n_req requests x n_layers layers x all KV heads of one step,
-    starting from an empty pool (all misses), including S0 for the sampled
-    blocks.  Returns (tokens/s extrapolated to all layers, seconds, description)."""
+    same workload: n_req requests x n_layers layers x all KV heads of one step
+    (S1..S5 from an empty pool; the metadata of the sampled blocks is built
+    first, untimed -- S0 runs once per 32 steps).  Returns (tokens/s
+    extrapolated to all layers, seconds timed, description)."""
     import oracle
     c = eng.cfg
     host_np = eng.host_kv.view(torch.int16).numpy().view(np.uint16)
     blocks = host_np.reshape(eng.host_blocks, 2, 32, 128)
-    t0 = time.perf_counter()
+    metas = []
     for l in range(n_layers):
         meta = np.empty((n_req, c.num_kv_heads, c.max_blk, 2, 128), np.uint16)
         for b in range(n_req):
             for h in range(c.num_kv_heads):
                 p0 = eng.key0(b, l, h) % eng.host_blocks
                 meta[b, h, :W["n_blk"]] = oracle.block_meta(blocks[p0:p0 + W["n_blk"]], key_stride=2 * 32 * 128)
+        metas.append(meta)
+    t0 = time.perf_counter()
+    for l in range(n_layers):
         pool = oracle.Pool(n_req * c.num_kv_heads * c.topk, c.fwd_len, c.block_bytes)
-        oracle.decode_layer(q_np_step[l, :n_req], meta, np.full(n_req, W["n_blk"], np.int32), c.topk,
+        oracle.decode_layer(q_np_step[l, :n_req], metas[l], np.full(n_req, W["n_blk"], np.int32), c.topk,
                             pool, np.arange(n_req, dtype=np.int32), l, c.layers, c.max_blk, 1,
                             host_np.view(np.uint8).reshape(eng.host_blocks, -1), eng.host_blocks,
                             np.zeros((n_req, c.num_kv_heads, 2, 32, 128), np.uint16),
@@ -267,7 +273,7 @@ def cpu_sample(eng, W, q_np_step, n_req=1, n_layers=1):
     dt = time.perf_counter() - t0
     per_step_s = dt / n_layers * c.layers / n_req        # seconds per request-step, all layers
     desc = (f"{n_req} request(s) x {n_layers} layer(s) x {c.num_kv_heads} KV heads of one C2 decode step "
-            f"(S0 for the sampled blocks + S1..S5 from an empty pool), extrapolated x{c.layers} layers")
+            f"(S1..S5 from an empty pool, metadata prebuilt), extrapolated x{c.layers} layers")
     return 1.0 / per_step_s, dt, desc
 
 
@@ -460,7 +466,7 @@ def bench_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         q_np = qs[0].view(torch.int16).cpu().numpy().view(np.uint16)
-        v, secs, desc = cpu_sample(eng, W, q_np, n_req=args.cpu_req, n_layers=1)
+        v, secs, desc = cpu_sample(eng, W, q_np, n_req=args.cpu_req, n_layers=args.cpu_layers)
         cpu = {"value": round(v, 4), "unit": "tokens/s", "cores": 1, "kind": "oracle",
                "sample": desc, "seconds": round(secs, 2)}
 
@@ -469,7 +475,7 @@ def bench_ours(args):
             "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (seeded K~N(0,1)*lognormal channel scales, V~N(0,1), drifting q rho=0.99)",
+            "data": f"synthetic (seeded K~N(0,1)*lognormal channel scales, V~N(0,1), drifting q rho={W['rho']})",
             "config": {"workload": W["name"], "batch_per_gpu": W["batch"] // world, "global_batch": W["batch"],
                        "layers": c.layers, "q_heads": W["num_q_heads"], "kv_heads": W["num_kv_heads"],
                        "head_dim": 128, "context": W["context"], "block_tokens": 32,
@@ -549,7 +555,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--host-runs", type=int, default=251,
                     help="physical host KV pool = host_runs x max_blk blocks (251 -> 15.7 GiB)")
-    ap.add_argument("--cpu-req", type=int, default=1)
+    ap.add_argument("--config", default="C2", choices=["C2", "C3"],
+                    help="workload: C2 (default, the metric's config) or C3 (GQA 1M-context stress)")
+    ap.add_argument("--cpu-req", type=int, default=2)
+    ap.add_argument("--cpu-layers", type=int, default=4)
     ap.add_argument("--timeline", default=None, help="write one step's op timeline (json, timing pass)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch kernels eagerly instead of replaying a captured CUDA graph per step")
@@ -558,6 +567,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # multi-GPU: one request group per rank and eager launches (the TP
+        # all-gather goes on the single compute stream; no NCCL inside a graph)
+        args.groups = 1
+        args.graph = False
     if args.impl == "reference":
         bench_reference(args)
     else:

@@ -407,44 +407,57 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
         const int64_t wl = warp_of_unit((p + 1) * Ku - 1, a.U, a.W);
         if (ticket != (int)(wl - wf)) continue;
         __threadfence();
-        // merge the contributors' partials in warp order (deterministic); the
-        // per-partial (m, l) are read lane-parallel, o with independent loads
+        // merge the contributors' partials in warp order (deterministic): the
+        // (m, l) of all (contributor, head) pairs are read lane-parallel, then
+        // every head's o with independent loads (all heads in one pass)
         const int nc = (int)(wl - wf + 1);
+        float mt[G], lt[G], oo[G][4];
+#pragma unroll
         for (int g = 0; g < G; ++g) {
-            float mt = -INFINITY;
-            for (int i = lane; i < nc; i += 32) {
-                const int64_t w2 = wf + i;
-                const int s2 = ((a.U * w2 / a.W) / Ku == p) ? 0 : 1;
-                mt = fmaxf(mt, __ldcg(a.part + ((w2 * 2 + s2) * G + g) * kAttnPartStride));
+            mt[g] = -INFINITY;
+            lt[g] = 0.f;
+            oo[g][0] = oo[g][1] = oo[g][2] = oo[g][3] = 0.f;
+        }
+        auto part_of = [&](int i, int g) -> const float* {
+            const int64_t w2 = wf + i;
+            const int s2 = ((a.U * w2 / a.W) / Ku == p) ? 0 : 1;
+            return a.part + ((w2 * 2 + s2) * G + g) * kAttnPartStride;
+        };
+        for (int i = lane; i < nc; i += 32) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) mt[g] = fmaxf(mt[g], __ldcg(part_of(i, g)));
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) mt[g] = warp_max(mt[g]);
+        for (int i = lane; i < nc; i += 32) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float* pp = part_of(i, g);
+                if (mt[g] != -INFINITY) lt[g] += __ldcg(pp + 1) * exp2f(__ldcg(pp) - mt[g]);
             }
-            mt = warp_max(mt);
-            float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f, lt = 0.f;
-            if (mt != -INFINITY) {
-                float lpart = 0.f;
-                for (int i = lane; i < nc; i += 32) {
-                    const int64_t w2 = wf + i;
-                    const int s2 = ((a.U * w2 / a.W) / Ku == p) ? 0 : 1;
-                    const float* pp = a.part + ((w2 * 2 + s2) * G + g) * kAttnPartStride;
-                    lpart += __ldcg(pp + 1) * exp2f(__ldcg(pp) - mt);
-                }
-                lt = warp_sum(lpart);
-#pragma unroll 4
-                for (int i = 0; i < nc; ++i) {
-                    const int64_t w2 = wf + i;
-                    const int s2 = ((a.U * w2 / a.W) / Ku == p) ? 0 : 1;
-                    const float* pp = a.part + ((w2 * 2 + s2) * G + g) * kAttnPartStride;
-                    const float sc = exp2f(__ldcg(pp) - mt);
-                    const float4 ov = __ldcg(reinterpret_cast<const float4*>(pp + 4 + 4 * lane));
-                    o0 = fmaf(ov.x, sc, o0);
-                    o1 = fmaf(ov.y, sc, o1);
-                    o2 = fmaf(ov.z, sc, o2);
-                    o3 = fmaf(ov.w, sc, o3);
-                }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) lt[g] = warp_sum(lt[g]);
+#pragma unroll 2
+        for (int i = 0; i < nc; ++i) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                if (mt[g] == -INFINITY) continue;
+                const float* pp = part_of(i, g);
+                const float sc = exp2f(__ldcg(pp) - mt[g]);
+                const float4 ov = __ldcg(reinterpret_cast<const float4*>(pp + 4 + 4 * lane));
+                oo[g][0] = fmaf(ov.x, sc, oo[g][0]);
+                oo[g][1] = fmaf(ov.y, sc, oo[g][1]);
+                oo[g][2] = fmaf(ov.z, sc, oo[g][2]);
+                oo[g][3] = fmaf(ov.w, sc, oo[g][3]);
             }
-            const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const float inv = lt[g] > 0.f ? 1.f / lt[g] : 0.f;
             const int hq = h * G + g;
             *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) =
-                make_float4(o0 * inv, o1 * inv, o2 * inv, o3 * inv);
+                make_float4(oo[g][0] * inv, oo[g][1] * inv, oo[g][2] * inv, oo[g][3] * inv);
         }
         if (lane == 0) a.tickets[p] = 0;
     }
