@@ -18,16 +18,22 @@
 // contributing warp in the workspace and the last contributor (atomic ticket,
 // self-resetting) merges them in warp order -- deterministic.
 //
-// Per block, lane t computes token t's logits for the G query heads of the KV
-// head (K row read with a lane-rotated chunk order: conflict-free 16-byte
-// shared loads), an online softmax in exp2 domain, and lane l accumulates
-// output dims 4l..4l+3 from the V rows.  float32 CUDA-core math: at 1 (MHA) to
-// 4 (GQA G=4) flop per HBM byte the kernel is far below the tensor-core ridge
-// and fp32 keeps the 2e-3 / 1e-5 tolerances with margin.
+// Two compute paths share that schedule.  bf16 (default): sparse_attn_mma_kernel
+// below -- tensor-core mma.sync over 2-D TMA, 128B-swizzled tiles.  f32 (and
+// bf16 with SS_ATTN_MMA=0): sparse_attn_kernel -- per block, lane t computes
+// token t's logits for the G query heads of the KV head (K row read with a
+// lane-rotated chunk order: conflict-free 16-byte shared loads), an online
+// softmax in exp2 domain, and lane l accumulates output dims 4l..4l+3 from the
+// V rows in float32 (keeps the 1e-5 f32 tolerance).
 //
 // Roofline: HBM-bound; algorithmic bytes = block_bytes per attended unit
 // (+ q, out: negligible).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <mutex>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -82,7 +88,7 @@ struct AttnArgs {
     float scale_log2;
     int64_t U;  // pairs * (k + 1)
     int W;      // total warps
-    int l2pf;   // L2 prefetch of the following unit
+    unsigned long long* trace;  // debug (SS_ATTN_TRACE=1): per warp globaltimer at entry / last unit / exit / merge start / merge end
 };
 
 template <bool BF16>
@@ -122,6 +128,123 @@ __device__ __forceinline__ void load_q(const AttnArgs& a, int b, int h, int lane
             r[g] = __ldg(reinterpret_cast<const float4*>((const float*)a.q + qi));
         }
     }
+}
+
+// A warp whose range cut pair p has written its partial (m, l, o) of the G
+// heads: take a ticket; the last contributor merges all partials in warp
+// order (deterministic) and writes the output, then resets the ticket.
+template <int G>
+__device__ __forceinline__ void finish_partial(const AttnArgs& a, int64_t p, int w) {
+    const int lane = lane_id();
+    const int Ku = a.k + 1;
+    const int b = (int)(p / a.Hkv), h = (int)(p % a.Hkv);
+    __threadfence();
+    __syncwarp();
+    int ticket = 0;
+    if (lane == 0) ticket = atomicAdd(&a.tickets[p], 1);
+    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    const int64_t wf = warp_of_unit(p * Ku, a.U, a.W);
+    const int64_t wl = warp_of_unit((p + 1) * Ku - 1, a.U, a.W);
+    if (ticket != (int)(wl - wf)) return;
+    __threadfence();
+    auto trace = [&](int i) {
+        if (a.trace != nullptr && lane == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.trace[(int64_t)w * 5 + i] = t;
+        }
+    };
+    trace(3);
+    // merge the contributors' partials in warp order (deterministic).  Which of
+    // its two partial slots contributor w2 used for p: slot 0 iff its range
+    // starts inside p, i.e. floor(U*w2/W) >= p*Ku  <=>  U*w2 >= p*Ku*W (no
+    // division: 64-bit integer division is a long software sequence).
+    const int nc = (int)(wl - wf + 1);
+    const int64_t pkw = p * Ku * (int64_t)a.W;
+    auto base_of = [&](int i) -> int64_t {  // float offset of contributor i's head-0 partial
+        const int64_t w2 = wf + i;
+        return ((w2 * 2 + (a.U * w2 >= pkw ? 0 : 1)) * G) * kAttnPartStride;
+    };
+    // heads in chunks of GC (register pressure for G = 8)
+    constexpr int GC = G < 4 ? G : 4;
+#pragma unroll 1
+    for (int g0 = 0; g0 < G; g0 += GC) {
+        float mt[GC], lt[GC], oo[GC][4];
+#pragma unroll
+        for (int g = 0; g < GC; ++g) {
+            mt[g] = -INFINITY;
+            lt[g] = 0.f;
+            oo[g][0] = oo[g][1] = oo[g][2] = oo[g][3] = 0.f;
+        }
+        // (m, l) of contributors lane, lane + 32, ...; the first 32 stay in
+        // registers (nc <= 32 is the common case: one memory round trip)
+        float m0[GC], l0[GC];
+        int64_t b0 = 0;
+#pragma unroll
+        for (int g = 0; g < GC; ++g) m0[g] = -INFINITY, l0[g] = 0.f;
+        for (int i = lane; i < nc; i += 32) {
+            const int64_t bi = base_of(i) + g0 * kAttnPartStride;
+#pragma unroll
+            for (int g = 0; g < GC; ++g) {
+                const float mv = __ldcg(a.part + bi + g * kAttnPartStride);
+                mt[g] = fmaxf(mt[g], mv);
+                if (i == lane) {
+                    m0[g] = mv;
+                    l0[g] = __ldcg(a.part + bi + g * kAttnPartStride + 1);
+                }
+            }
+            if (i == lane) b0 = bi;
+        }
+#pragma unroll
+        for (int g = 0; g < GC; ++g) mt[g] = warp_max(mt[g]);
+        for (int i0 = 0; i0 < nc; i0 += 32) {
+            // lane-parallel: contributor i0 + lane's partial offset and scale per head
+            const int i = i0 + lane;
+            int64_t base_i = b0;
+            float sc_i[GC];
+#pragma unroll
+            for (int g = 0; g < GC; ++g) sc_i[g] = 0.f;
+            if (i < nc) {
+                if (i0 > 0) base_i = base_of(i) + g0 * kAttnPartStride;
+#pragma unroll
+                for (int g = 0; g < GC; ++g) {
+                    const float* pp = a.part + base_i + g * kAttnPartStride;
+                    const float mv = i0 == 0 ? m0[g] : __ldcg(pp);
+                    const float lv = i0 == 0 ? l0[g] : __ldcg(pp + 1);
+                    if (mt[g] != -INFINITY) {
+                        sc_i[g] = exp2f(mv - mt[g]);
+                        lt[g] += lv * sc_i[g];
+                    }
+                }
+            }
+            const int n = min(32, nc - i0);
+            constexpr int UNR = GC >= 4 ? 4 : 8;  // loads in flight vs registers
+#pragma unroll UNR
+            for (int j = 0; j < n; ++j) {
+                const int64_t bj = __shfl_sync(0xffffffffu, base_i, j);
+#pragma unroll
+                for (int g = 0; g < GC; ++g) {
+                    const float sc = __shfl_sync(0xffffffffu, sc_i[g], j);
+                    const float4 ov = __ldcg(reinterpret_cast<const float4*>(
+                        a.part + bj + g * kAttnPartStride + 4 + 4 * lane));
+                    oo[g][0] = fmaf(ov.x, sc, oo[g][0]);
+                    oo[g][1] = fmaf(ov.y, sc, oo[g][1]);
+                    oo[g][2] = fmaf(ov.z, sc, oo[g][2]);
+                    oo[g][3] = fmaf(ov.w, sc, oo[g][3]);
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < GC; ++g) {
+            const float lsum = warp_sum(lt[g]);
+            const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+            const int hq = h * G + g0 + g;
+            *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) =
+                make_float4(oo[g][0] * inv, oo[g][1] * inv, oo[g][2] * inv, oo[g][3] * inv);
+        }
+    }
+    trace(4);
+    if (lane == 0) a.tickets[p] = 0;
 }
 
 template <bool BF16, int G>
@@ -398,69 +521,372 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
             *reinterpret_cast<float4*>(pp + 4 + 4 * lane) =
                 make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
         }
-        __threadfence();
-        __syncwarp();
-        int ticket = 0;
-        if (lane == 0) ticket = atomicAdd(&a.tickets[p], 1);
-        ticket = __shfl_sync(0xffffffffu, ticket, 0);
-        const int64_t wf = warp_of_unit(p * Ku, a.U, a.W);
-        const int64_t wl = warp_of_unit((p + 1) * Ku - 1, a.U, a.W);
-        if (ticket != (int)(wl - wf)) continue;
-        __threadfence();
-        // merge the contributors' partials in warp order (deterministic): the
-        // (m, l) of all (contributor, head) pairs are read lane-parallel, then
-        // every head's o with independent loads (all heads in one pass)
-        const int nc = (int)(wl - wf + 1);
-        float mt[G], lt[G], oo[G][4];
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            mt[g] = -INFINITY;
-            lt[g] = 0.f;
-            oo[g][0] = oo[g][1] = oo[g][2] = oo[g][3] = 0.f;
-        }
-        auto part_of = [&](int i, int g) -> const float* {
-            const int64_t w2 = wf + i;
-            const int s2 = ((a.U * w2 / a.W) / Ku == p) ? 0 : 1;
-            return a.part + ((w2 * 2 + s2) * G + g) * kAttnPartStride;
-        };
-        for (int i = lane; i < nc; i += 32) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) mt[g] = fmaxf(mt[g], __ldcg(part_of(i, g)));
-        }
-#pragma unroll
-        for (int g = 0; g < G; ++g) mt[g] = warp_max(mt[g]);
-        for (int i = lane; i < nc; i += 32) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float* pp = part_of(i, g);
-                if (mt[g] != -INFINITY) lt[g] += __ldcg(pp + 1) * exp2f(__ldcg(pp) - mt[g]);
-            }
-        }
-#pragma unroll
-        for (int g = 0; g < G; ++g) lt[g] = warp_sum(lt[g]);
-#pragma unroll 2
-        for (int i = 0; i < nc; ++i) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                if (mt[g] == -INFINITY) continue;
-                const float* pp = part_of(i, g);
-                const float sc = exp2f(__ldcg(pp) - mt[g]);
-                const float4 ov = __ldcg(reinterpret_cast<const float4*>(pp + 4 + 4 * lane));
-                oo[g][0] = fmaf(ov.x, sc, oo[g][0]);
-                oo[g][1] = fmaf(ov.y, sc, oo[g][1]);
-                oo[g][2] = fmaf(ov.z, sc, oo[g][2]);
-                oo[g][3] = fmaf(ov.w, sc, oo[g][3]);
-            }
-        }
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const float inv = lt[g] > 0.f ? 1.f / lt[g] : 0.f;
-            const int hq = h * G + g;
-            *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) =
-                make_float4(oo[g][0] * inv, oo[g][1] * inv, oo[g][2] * inv, oo[g][3] * inv);
-        }
-        if (lane == 0) a.tickets[p] = 0;
+        finish_partial<G>(a, p, w);
     }
+}
+
+// ============================================================================
+// bf16 tensor-core variant (the north star's "tensor cores only for the
+// batched-GQA QK^T/PV contractions").  Same unit schedule, pipeline and
+// partial merge as above; per unit (one 32-token block of one (b, h) pair) one
+// warp computes, transposed so that every MMA row is a real token / dim:
+//   S^T[32 x 8]   = K[32 x 128] Q^T[128 x 8]     (columns 0..G-1 = the G heads)
+//   O^T[128 x 8] += V^T[128 x 32] P^T[32 x 8]    (P split as bf16 hi + lo)
+// with mma.sync m16n8k16 (bf16 in, f32 accumulate): 16 + 32 HMMA, 32 ldmatrix
+// and 8 movmatrix (P^T from the S^T accumulator layout into the B-operand
+// layout) per 16 KiB block, instead of ~2000 FMA/LDS instructions for G = 4.
+// Why not tcgen05: a decode block contracts G <= 8 query heads with 32 tokens;
+// tcgen05.mma wants >= 64-row tiles and a TMEM round trip per 32-token softmax
+// step on the critical path of a kernel that is HBM/latency-bound at 1-4
+// flop/byte, far below any tensor-core ridge.
+//
+// Staging: 2-D TMA (cp.async.bulk.tensor) with SWIZZLE_128B, so ldmatrix reads
+// of 8 token rows (256 B apart in HBM) are bank-conflict-free.  A [2][32][128]
+// block is four 32 x 64 boxes (K dims 0-63 | K 64-127 | V 0-63 | V 64-127),
+// 4 KiB each; 16-byte chunk j of row r sits at chunk j ^ (r & 7).
+//
+// Precision: Q and K are exact in bf16 and the HMMA accumulates in f32, as the
+// FMA path does; P is split p = hi + lo (both bf16, |p - hi - lo| <= 2^-17 p),
+// so P V carries ~2^-17 relative error instead of bf16's 2^-9.
+// ============================================================================
+constexpr int kMmaNW = 6;  // warps per CTA: 6 x 32 KiB of stages
+
+struct MmaWarpSmem {
+    alignas(1024) unsigned char buf[2][16384];  // [stage] K-lo | K-hi | V-lo | V-hi
+    uint64_t bar[2][2];                          // [stage][K half / V half]
+};
+
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* tm, int x, int y,
+                                       uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr)
+                 : "memory");
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr)
+                 : "memory");
+}
+// 8x8 b16 transpose across the warp (fragment layout in and out)
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+    uint32_t y;
+    asm("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+// D[16x8] += A[16x16] B[16x8], bf16 in, f32 accumulate
+__device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t bf16x2_bits(__nv_bfloat162 v) {
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int G>
+__global__ void __launch_bounds__(kMmaNW * 32, 1)
+sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_pool,
+                       const __grid_constant__ CUtensorMap tm_tail) {
+    if (a.counts != nullptr && a.counts[3] != 0) return;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    MmaWarpSmem& sm = reinterpret_cast<MmaWarpSmem*>(base)[warp_id()];
+    const int lane = lane_id();
+    const int w = warp_id() * gridDim.x + blockIdx.x;
+    if (w >= a.W) return;
+    const int64_t u0 = a.U * w / a.W, u1 = a.U * (w + 1) / a.W;
+    const int Ku = a.k + 1;
+    const int r = lane >> 2, c = lane & 3;  // fragment row group / column pair
+    auto trace = [&](int i) {
+        if (a.trace != nullptr && lane == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.trace[(int64_t)w * 5 + i] = t;
+        }
+    };
+    trace(0);
+
+    if (lane == 0) {
+        mbar_init(&sm.bar[0][0], 1);
+        mbar_init(&sm.bar[0][1], 1);
+        mbar_init(&sm.bar[1][0], 1);
+        mbar_init(&sm.bar[1][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_pool)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_tail)) : "memory");
+    }
+    __syncwarp();
+
+    // ---- producer: the warp's unit descriptors, 32 at a time, lane-parallel.
+    // Lane l holds unit wbase + l: kind (0 skip, 1 pool slot, 2 tail), the
+    // tensor-map row of its K, and its pair -- one division per lane per 32
+    // units; the consumer never divides.
+    int64_t wbase = u0;
+    int wkind = 0, wrow = 0, wpair = 0;
+    auto refill = [&]() {
+        const int64_t u = wbase + lane;
+        wkind = 0;
+        if (u < u1) {
+            const int64_t p = u / Ku;
+            const int rr = (int)(u - p * Ku);
+            wpair = (int)p;
+            if (rr < a.k) {
+                const int32_t sl = __ldg(a.slot + p * a.k + rr);
+                wkind = sl >= 0 ? 1 : 0;
+                wrow = sl * 64;
+            } else {
+                wkind = __ldg(a.tail_len + p / a.Hkv) > 0 ? 2 : 0;
+                wrow = (int)p * 64;
+            }
+        }
+    };
+    refill();
+    int next_l = 0;                       // next lane of the window to consider
+    int kind0 = 0, kind1 = 0;             // unit held by stage 0 / 1: kind (0 = none)
+    int row0 = 0, row1 = 0;               // its K row in the tensor map
+    int pair0 = -1, pair1 = -1;           // its pair (-1 = none)
+    auto issue_half = [&](int stage, int half) {
+        const int kind = stage ? kind1 : kind0;
+        if (lane == 0 && kind != 0) {
+            const CUtensorMap* tm = kind == 1 ? &tm_pool : &tm_tail;
+            const int row = (stage ? row1 : row0) + 32 * half;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&sm.bar[stage][half], 8192);
+            const uint32_t dst = smem_u32(sm.buf[stage]) + half * 8192;
+            tma_2d(dst, tm, 0, row, &sm.bar[stage][half]);
+            tma_2d(dst + 4096, tm, 64, row, &sm.bar[stage][half]);
+        }
+    };
+    auto issue_k = [&](int stage) {
+        while (true) {
+            const unsigned m = __ballot_sync(0xffffffffu, wkind != 0 && lane >= next_l);
+            if (m) {
+                const int l = __ffs(m) - 1;
+                next_l = l + 1;
+                (stage ? kind1 : kind0) = __shfl_sync(0xffffffffu, wkind, l);
+                (stage ? row1 : row0) = __shfl_sync(0xffffffffu, wrow, l);
+                (stage ? pair1 : pair0) = __shfl_sync(0xffffffffu, wpair, l);
+                issue_half(stage, 0);
+                return;
+            }
+            if (wbase + 32 >= u1) {
+                next_l = 32;
+                (stage ? kind1 : kind0) = 0;
+                (stage ? pair1 : pair0) = -1;
+                return;
+            }
+            wbase += 32;
+            next_l = 0;
+            refill();
+        }
+    };
+    issue_k(0);
+    issue_half(0, 1);
+    issue_k(1);
+    issue_half(1, 1);
+    uint32_t phases = 0u;
+    int stage = 0;
+
+    // per-lane ldmatrix addressing: matrix mi = lane / 8, row rr = lane % 8
+    const int mi = lane >> 3, rr = lane & 7;
+    // QK, A = K[token][dim] (non-transposed): matrices {tok 0-7, 8-15, 0-7, 8-15}
+    // x {dims lo 8, lo, hi 8, hi} of a 16-token x 16-dim tile
+    const uint32_t k_off = (uint32_t)((8 * (mi & 1) + rr) * 128);
+    const uint32_t k_hi = (uint32_t)(mi >> 1);
+    // PV, A = V^T (transposed load of V[token][dim]): matrices {dims lo, hi, lo,
+    // hi} x {tok 0-7, 0-7, 8-15, 8-15}
+    const uint32_t v_off = (uint32_t)((8 * (mi >> 1) + rr) * 128);
+    const uint32_t v_hi = (uint32_t)(mi & 1);
+
+    const int64_t p_first = u0 / Ku, p_last = (u1 - 1) / Ku;
+    for (int64_t p = p_first; p <= p_last; ++p) {
+        const int b = (int)(p / a.Hkv), h = (int)(p % a.Hkv);
+        // Q^T fragment (B operand): k-step s holds head r's dims 16s+2c, +1 (b0)
+        // and 16s+8+2c, +1 (b1); heads r >= G are zero columns
+        uint32_t qb[8][2];
+        {
+            const uint32_t* qp = reinterpret_cast<const uint32_t*>(
+                (const uint16_t*)a.q + ((int64_t)b * a.Hq + (int64_t)h * G + (r < G ? r : 0)) * kHeadDim);
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                qb[s][0] = r < G ? __ldg(qp + 8 * s + c) : 0u;
+                qb[s][1] = r < G ? __ldg(qp + 8 * s + 4 + c) : 0u;
+            }
+        }
+        // running max / sum of heads 2c, 2c+1; O^T tile md: rows dims 16md + r
+        // (+8), columns heads 2c, 2c+1
+        float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+        float o[8][4];
+#pragma unroll
+        for (int md = 0; md < 8; ++md) o[md][0] = o[md][1] = o[md][2] = o[md][3] = 0.f;
+        const int tl = __ldg(a.tail_len + b);
+
+        while ((stage ? pair1 : pair0) == (int)p) {
+            const bool is_tail = (stage ? kind1 : kind0) == 2;
+            mbar_wait(&sm.bar[stage][0], (phases >> (2 * stage)) & 1u);
+            phases ^= 1u << (2 * stage);
+            const uint32_t kb = smem_u32(sm.buf[stage]);
+            // ---- S^T = K Q^T: m-tile mt = tokens 16mt..16mt+15; two partial
+            // accumulators per tile (dims 0-63 / 64-127) halve the HMMA chains ----
+            float sa[2][2][4];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) sa[mt][hh][0] = sa[mt][hh][1] = sa[mt][hh][2] = sa[mt][hh][3] = 0.f;
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                const uint32_t chunk = (uint32_t)(2 * (s & 3)) + k_hi;
+                const uint32_t col = ((chunk ^ (uint32_t)rr) << 4) + (uint32_t)(s >> 2) * 4096u;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    uint32_t ka[4];
+                    ldsm_x4(kb + col + mt * 2048 + k_off, ka);
+                    hmma(sa[mt][s >> 2], ka, qb[s][0], qb[s][1]);
+                }
+            }
+            // lane holds S^T at tokens t(mt, e2) = 16mt + 8*e2 + r, heads 2c + e
+            float z[2][2][2];  // [mt][e2][e]
+            float rmax[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int e2 = 0; e2 < 2; ++e2) {
+                    const bool valid = !is_tail || (16 * mt + 8 * e2 + r) < tl;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const float sv = sa[mt][0][2 * e2 + e] + sa[mt][1][2 * e2 + e];
+                        z[mt][e2][e] = valid ? sv * a.scale_log2 : -INFINITY;
+                        rmax[e] = fmaxf(rmax[e], z[mt][e2][e]);
+                    }
+                }
+            // reduce over the 8 row groups (lane bits 2..4)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                rmax[e] = fmaxf(rmax[e], __shfl_xor_sync(0xffffffffu, rmax[e], 4));
+                rmax[e] = fmaxf(rmax[e], __shfl_xor_sync(0xffffffffu, rmax[e], 8));
+                rmax[e] = fmaxf(rmax[e], __shfl_xor_sync(0xffffffffu, rmax[e], 16));
+            }
+            float corr[2], rsum[2] = {0.f, 0.f};
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const float mnew = fmaxf(m[e], rmax[e]);
+                corr[e] = exp2f(m[e] - mnew);
+                m[e] = mnew;
+            }
+            // P^T as the PV B operand: k-step ks = tokens 16ks..16ks+15; b0 =
+            // tokens 16ks+2c, +1 of head r, b1 = tokens 16ks+8+2c, +1.  The
+            // accumulator layout holds (token r-row, head pair) -> movmatrix.
+            uint32_t pbh[2][2], pbl[2][2];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int e2 = 0; e2 < 2; ++e2) {
+                    const float p0 = exp2f(z[mt][e2][0] - m[0]);
+                    const float p1 = exp2f(z[mt][e2][1] - m[1]);
+                    rsum[0] += p0;
+                    rsum[1] += p1;
+                    const __nv_bfloat162 hi = __floats2bfloat162_rn(p0, p1);
+                    const float2 hf = __bfloat1622float2(hi);
+                    const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+                    pbh[mt][e2] = movm_t(bf16x2_bits(hi));
+                    pbl[mt][e2] = movm_t(bf16x2_bits(lo));
+                }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                rsum[e] += __shfl_xor_sync(0xffffffffu, rsum[e], 4);
+                rsum[e] += __shfl_xor_sync(0xffffffffu, rsum[e], 8);
+                rsum[e] += __shfl_xor_sync(0xffffffffu, rsum[e], 16);
+                l[e] = l[e] * corr[e] + rsum[e];
+            }
+#pragma unroll
+            for (int md = 0; md < 8; ++md) {
+                o[md][0] *= corr[0];
+                o[md][1] *= corr[1];
+                o[md][2] *= corr[0];
+                o[md][3] *= corr[1];
+            }
+            __syncwarp();
+            issue_k(stage);  // K half consumed: next unit's K into this stage
+            mbar_wait(&sm.bar[stage][1], (phases >> (2 * stage + 1)) & 1u);
+            phases ^= 1u << (2 * stage + 1);
+            const uint32_t vb = kb + 8192;
+            if (is_tail && tl < kBlockTokens) {
+                // rows >= tl of a tail may hold anything (0 * NaN = NaN): zero them
+                unsigned char* vp = sm.buf[stage] + 8192;
+                for (int i = lane; i < 2 * kBlockTokens * 8; i += 32) {
+                    const int half = i / (kBlockTokens * 8), row = (i / 8) % kBlockTokens;
+                    if (row >= tl)
+                        *reinterpret_cast<uint4*>(vp + half * 4096 + row * 128 + (i % 8) * 16) =
+                            make_uint4(0, 0, 0, 0);
+                }
+                __syncwarp();
+            }
+            // ---- O^T += V^T P^T: m-tile md = dims 16md..16md+15 ----
+#pragma unroll
+            for (int md = 0; md < 8; ++md) {
+                const uint32_t chunk = (uint32_t)(2 * (md & 3)) + v_hi;
+                const uint32_t col = ((chunk ^ (uint32_t)rr) << 4) + (uint32_t)(md >> 2) * 4096u;
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    uint32_t va[4];
+                    ldsm_x4_t(vb + col + ks * 2048 + v_off, va);
+                    hmma(o[md], va, pbh[ks][0], pbh[ks][1]);
+                    hmma(o[md], va, pbl[ks][0], pbl[ks][1]);
+                }
+            }
+            __syncwarp();
+            issue_half(stage, 1);  // V half of this stage's next unit
+            stage ^= 1;
+        }
+
+        // ---- flush pair p: lane holds heads 2c + e, dims 16md + r (+8) ----
+        if (p == p_last) trace(1);
+        const bool full = (p * Ku >= u0) && ((p + 1) * Ku <= u1);
+        if (full) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if (2 * c + e < G) {
+                    const float inv = l[e] > 0.f ? 1.f / l[e] : 0.f;
+                    float* op = a.out + ((int64_t)(h * G + 2 * c + e) * a.B + b) * kHeadDim + r;
+#pragma unroll
+                    for (int md = 0; md < 8; ++md) {
+                        op[16 * md] = o[md][e] * inv;
+                        op[16 * md + 8] = o[md][2 + e] * inv;
+                    }
+                }
+            }
+            continue;
+        }
+        const int seg = (p == p_first) ? 0 : 1;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            if (2 * c + e < G) {
+                float* pp = a.part + (((int64_t)w * 2 + seg) * G + 2 * c + e) * kAttnPartStride;
+                if (r == 0) {
+                    pp[0] = m[e];
+                    pp[1] = l[e];
+                }
+#pragma unroll
+                for (int md = 0; md < 8; ++md) {
+                    pp[4 + 16 * md + r] = o[md][e];
+                    pp[4 + 16 * md + 8 + r] = o[md][2 + e];
+                }
+            }
+        }
+        finish_partial<G>(a, p, w);
+    }
+    trace(2);
 }
 
 template <bool BF16, int G>
@@ -472,12 +898,71 @@ static int attn_total_warps(ss_dtype dt) {
     return kNumSMs * (dt == SS_BF16 ? AttnTraits<true>::NW : AttnTraits<false>::NW);
 }
 
-size_t attn_ws_bytes(const ss_dims& d, int k, ss_dtype dt) {
+static bool attn_trace_on() {
+    static const bool on = getenv("SS_ATTN_TRACE") && atoi(getenv("SS_ATTN_TRACE")) != 0;
+    return on;
+}
+
+static size_t attn_ws_bytes_core(const ss_dims& d, ss_dtype dt) {
     int G = d.num_q_heads / d.num_kv_heads;
     size_t W = attn_total_warps(dt);
     size_t part = W * 2 * G * kAttnPartStride * 4;
     size_t pairs = (size_t)d.batch * d.num_kv_heads;
     return ((part + pairs * 4) + 255) & ~(size_t)255;
+}
+
+size_t attn_ws_bytes(const ss_dims& d, int k, ss_dtype dt) {
+    // + debug timeline (5 x u64 per warp) after the core workspace when traced
+    return attn_ws_bytes_core(d, dt) + (attn_trace_on() ? (size_t)attn_total_warps(dt) * 5 * 8 : 0);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+// [rows][128] bf16 view of a KV array (row = one token's K or V vector of a
+// head-block; block b = rows 64b .. 64b+63), 32 x 64 boxes, 128-byte swizzle.
+static bool encode_kv_map(CUtensorMap* m, const void* base, uint64_t rows) {
+    auto enc = tensor_map_encoder();
+    if (enc == nullptr) return false;
+    const cuuint64_t gdim[2] = {(cuuint64_t)kHeadDim, (cuuint64_t)rows};
+    const cuuint64_t gstride[1] = {(cuuint64_t)kHeadDim * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)kBlockTokens};
+    const cuuint32_t estride[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box,
+               estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr size_t kMmaSmem = sizeof(MmaWarpSmem) * kMmaNW + 1024;  // + base alignment slack
+
+template <int G>
+static ss_status launch_attn_mma_t(const AttnArgs& a, const void* pool, const void* tail,
+                                   cudaStream_t stream) {
+    CUtensorMap tm_pool, tm_tail;
+    // the pool's slot count is not part of the call: its map spans the whole
+    // int32 row range (TMA reads only the boxes requested = valid slots)
+    if (!encode_kv_map(&tm_pool, pool, (uint64_t)INT32_MAX) ||
+        !encode_kv_map(&tm_tail, tail, (uint64_t)a.B * a.Hkv * 2 * kBlockTokens))
+        return SS_ERR_CUDA;
+    auto kern = sparse_attn_mma_kernel<G>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem) !=
+        cudaSuccess)
+        return SS_ERR_CUDA;
+    kern<<<kNumSMs, kMmaNW * 32, kMmaSmem, stream>>>(a, tm_pool, tm_tail);
+    SS_LAUNCH_CHECK();
+    return SS_OK;
 }
 
 template <bool BF16, int G>
@@ -511,8 +996,6 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
     a.scale_log2 = scale * 1.4426950408889634f;
     const int G = d.num_q_heads / d.num_kv_heads;
     a.U = (int64_t)d.batch * d.num_kv_heads * (k + 1);
-    static const int l2pf = getenv("SS_ATTN_L2PF") ? atoi(getenv("SS_ATTN_L2PF")) : 0;  // measured slower
-    a.l2pf = l2pf;
     // at least kMinUnitsPerWarp units (256 KiB in bf16) per warp: fewer, longer
     // ranges when the problem is small (C3: ~8 partials per pair to merge instead
     // of ~28); W <= U keeps every range non-empty
@@ -522,8 +1005,12 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
     size_t part = (size_t)a.W * 2 * G * kAttnPartStride * 4;
     a.part = (float*)ws;
     a.tickets = (int32_t*)((char*)ws + part);
+    a.trace = attn_trace_on() ? (unsigned long long*)((char*)ws + attn_ws_bytes_core(d, dt)) : nullptr;
+    // bf16: tensor-core path (SS_ATTN_MMA=0 selects the CUDA-core FMA path)
+    static const int use_mma = getenv("SS_ATTN_MMA") ? atoi(getenv("SS_ATTN_MMA")) : 1;
 #define SS_ATTN_CASE(GG)                                                                    \
     case GG:                                                                                \
+        if (dt == SS_BF16 && use_mma) return launch_attn_mma_t<GG>(a, pool_kv, tail_kv, stream); \
         return dt == SS_BF16 ? launch_attn_t<true, GG>(a, stream) : launch_attn_t<false, GG>(a, stream);
     switch (G) {
         SS_ATTN_CASE(1)

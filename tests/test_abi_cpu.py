@@ -52,6 +52,8 @@ def test_library_is_sm100a_sass(lib):
     sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "UBLKCP" in sass          # TMA bulk copies in the attention kernel
     assert "DFMA" in sass            # fp64 block scoring
+    assert "UTMALDG" in sass         # 2-D tensor-map TMA (swizzled K/V tiles)
+    assert "HMMA" in sass and "LDSM" in sass   # tensor-core QK^T / PV (bf16 attention)
 
 
 def test_host_validation_without_gpu(lib):

@@ -283,12 +283,22 @@ def test_flash_h2d_gather_byte_exact(ops, bb):
 # ----------------------------------------------------------------------------
 # S5
 # ----------------------------------------------------------------------------
-def _attn_case(ops, dt, B, Hq, Hkv, k, S, tails, seed, empty_pair=False):
+def _attn_case(ops, dt, B, Hq, Hkv, k, S, tails, seed, empty_pair=False, q_scale=1.0,
+               tail_garbage=False):
     rng = synth.rng_for(1000, 5, seed)
     pool_f = synth.kv_blocks(rng, S, D, synth.channel_scales(rng))
     tail_f = synth.kv_blocks(rng, B * Hkv, D).reshape(B, Hkv, 2, 32, D)
-    q = rng.standard_normal((B, Hq, D)).astype(np.float32)
+    q = rng.standard_normal((B, Hq, D)).astype(np.float32) * q_scale
     pool, tail, qs = synth.encode(pool_f, dt), synth.encode(tail_f, dt), synth.encode(q, dt)
+    if tail_garbage:
+        # rows >= tail_len are outside the contract: fill them with NaN / Inf bit
+        # patterns, which must not reach the output (0 * NaN = NaN in a P.V product)
+        nan = np.uint16(0x7FC0) if dt == synth.DT_BF16 else np.uint32(0x7FC00000)
+        inf = np.uint16(0x7F80) if dt == synth.DT_BF16 else np.uint32(0x7F800000)
+        tv = tail.view(np.uint16 if dt == synth.DT_BF16 else np.uint32)
+        for b in range(B):
+            tv[b, :, 0, tails[b]:] = nan
+            tv[b, :, 1, tails[b]:] = inf
     slot = np.full((B, Hkv, k), -1, np.int32)
     for b in range(B):
         for h in range(Hkv):
@@ -328,6 +338,18 @@ def test_attention_gqa_more(ops, G):
 def test_attention_empty_and_tail_only(ops):
     # pair (0,0) has no blocks and tail 0 -> O = 0 ; other pairs mixed
     _attn_case(ops, synth.DT_BF16, 2, 4, 4, 8, 64, [0, 9], seed=50, empty_pair=True)
+
+
+@pytest.mark.parametrize("dt", [synth.DT_BF16, synth.DT_F32])
+def test_attention_tail_rows_beyond_len_ignored(ops, dt):
+    _attn_case(ops, dt, 3, 8, 2, 16, 200, [0, 1, 30], seed=70, tail_garbage=True)
+
+
+@pytest.mark.parametrize("G", [1, 4])
+def test_attention_sharp_softmax(ops, G):
+    # |q| x 8: logits spread over tens of units, a few tokens carry the weight --
+    # the regime where rounding P to bf16 alone (2^-9) would exceed 2e-3
+    _attn_case(ops, synth.DT_BF16, 2, 4 * G, 4, 64, 500, [7, 20], seed=80 + G, q_scale=8.0)
 
 
 def test_attention_many_pairs_stream_k(ops):

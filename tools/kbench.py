@@ -80,6 +80,9 @@ def bench_attn(c, iters):
     ts = []
     for _ in range(iters):
         torch.sum(flush, dim=0, out=sink)
+        # keep the GPU busy ~150 us so the host has enqueued f() before the
+        # start event fires (host launch overhead must not count as kernel time)
+        torch.cuda._sleep(300000)
         s.record()
         f()
         e.record()
@@ -87,6 +90,29 @@ def bench_attn(c, iters):
         ts.append(s.elapsed_time(e))
     ms = sorted(ts)[len(ts) // 2]
     byts = B * Hkv * k * 16384
+    if os.environ.get("SS_ATTN_TRACE"):
+        # per-warp globaltimer (ns) at entry / last unit done / exit (debug timeline)
+        nw = 148 * 6
+        tr = ws.view(torch.uint8)[-nw * 40:].view(torch.int64).view(nw, 5).cpu()
+        ok = tr[:, 0] > 0
+        widx = torch.arange(nw)[ok]
+        tr = tr[ok]
+        t0 = int(tr[:, 0].min())
+        rel = (tr[:, :3] - t0).double() / 1e3
+        q = lambda x: [round(float(x.quantile(v)), 2) for v in (0.0, 0.5, 0.9, 1.0)]
+        mg = tr[tr[:, 3] > 0]
+        mdur = (mg[:, 4] - mg[:, 3]).double() / 1e3
+        mstart = (mg[:, 3] - t0).double() / 1e3
+        print(json.dumps({"trace_warps": len(tr), "entry_us_q0/50/90/100": q(rel[:, 0]),
+                          "last_unit_us": q(rel[:, 1]), "exit_us": q(rel[:, 2]),
+                          "merges": len(mg), "merge_us": q(mdur) if len(mg) else None,
+                          "merge_start_us": q(mstart) if len(mg) else None}))
+        # imbalance structure: mean last-unit time by warp slot in the CTA and by SM id
+        lu = rel[:, 1]
+        slot, sm = widx // 148, widx % 148
+        print(json.dumps({"last_unit_by_warp_slot": [round(float(lu[slot == i].mean()), 2) for i in range(6) if (slot == i).any()],
+                          "last_unit_by_sm_decile": [round(float(lu[(sm >= 15 * i) & (sm < 15 * i + 15)].mean()), 2) for i in range(10)],
+                          "last_unit_even_odd_sm": [round(float(lu[sm % 2 == 0].mean()), 2), round(float(lu[sm % 2 == 1].mean()), 2)]}))
     return {"kernel": "attn", "us": ms * 1e3, "GBps": byts / ms / 1e6, "frac": byts / ms / 1e6 / PEAK}
 
 
