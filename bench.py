@@ -455,8 +455,13 @@ def bench_ours(args):
     }
     if world > 1:
         kernels["nccl_all_gather"] = {"us_per_launch": round(tot["allgather"] * 1e3 / max(1, nlaunch["allgather"]), 2)}
-    share = {k: tot[n] for k, n in (("ss_block_select", "select"), ("sparse_decode_attn", "attn"),
-                                    ("flash_h2d_gather", "gather"))}
+    # dominant kernel = the largest share of the step at each kernel's own roofline
+    # (algorithmic bytes / peak).  The event times above are taken while request
+    # groups overlap (a launch's time includes co-running kernels and waits for
+    # SMs), so they are not used to rank; ncu's serialised launch list agrees
+    # (profiles/*launch_shares*).
+    share = {"ss_block_select": sel_bytes / hbm_peak, "sparse_decode_attn": attn_bytes / hbm_peak,
+             "flash_h2d_gather": miss_bytes_kt / h2d_peak if h2d_peak else 0.0}
     dom = max(share, key=share.get)
     dk = kernels[dom]
     traffic = None

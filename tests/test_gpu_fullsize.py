@@ -1,6 +1,9 @@
 """Full-size parity in bench.py's launch configuration (BASELINE.json configs[1],
 C2: 16 requests x 32 layers x 32 heads, 128K context = 4096 blocks, top-64,
-131072-slot HBM pool per layer, two request groups on separate streams).
+131072-slot HBM pool per layer, two request groups on separate streams; and
+configs[2], C3: 4 requests x 32 layers x 32 query / 8 KV heads (GQA G = 4), 1M
+context = 32768 blocks, top-128, 8192-slot pool per layer -- the miss-heavy
+FlashH2D stress, bench.py --config C3).
 
 The engine runs every layer of every step exactly as bench.py does; the oracle
 replays one of the 32 layers (17) in full -- its own metadata for all
@@ -25,21 +28,21 @@ CHECK_LAYERS = (17,)
 STEPS = 3
 
 
-def test_c2_fullsize_layer17_three_steps():
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_fullsize_layer17_three_steps(name):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
+    wl, runs, need_gb = {"C2": (synth.C2, 13, 110), "C3": (synth.C3, 2, 30)}[name]
     free, _ = torch.cuda.mem_get_info()
-    if free < 110 * (1 << 30):
-        pytest.skip("needs ~110 GB of free HBM")
+    if free < need_gb * (1 << 30):
+        pytest.skip(f"needs ~{need_gb} GB of free HBM")
     from paper_2509_24626_b200.engine import DecodeEngine, EngineConfig
-    wl = synth.C2
     cfg = EngineConfig(batch=wl.batch, layers=wl.layers, num_q_heads=wl.num_q_heads,
                        num_kv_heads=wl.num_kv_heads, max_blk=wl.max_blk, topk=wl.topk,
                        slots_per_layer=wl.slots_per_layer, num_requests=wl.batch,
                        dtype=torch.bfloat16, groups=2)
     eng = DecodeEngine(cfg)
-    runs = 13                                           # physical host pool = 13 x 4096 blocks (832 MiB)
-    hb = runs * cfg.max_blk
+    hb = runs * cfg.max_blk                             # physical host pool (C2 832 MiB, C3 1 GiB)
     rng = synth.rng_for(8000, 1)
     scales = synth.channel_scales(rng)
     host_np = np.empty((hb, 2, 32, D), np.uint16)
@@ -54,6 +57,9 @@ def test_c2_fullsize_layer17_three_steps():
     eng.build_meta(nbk, host_t.cuda())
     qs = synth.encode(synth.queries(rng, STEPS, (cfg.layers, cfg.batch, cfg.num_q_heads, D), wl.rho),
                       synth.DT_BF16)
+    if name == "C3":
+        # C3 is the miss-heavy case: with rho = 0 every step selects mostly new blocks
+        assert wl.rho == 0.0
     # oracle state for the checked layers
     metas, pools = {}, {}
     for l in CHECK_LAYERS:
