@@ -45,6 +45,8 @@ def lib():
         L.or_block_meta.argtypes = [P, I64, I64, I32, I32, P]
         L.or_block_score.argtypes = [P, P, P, I32, I32, I32, I32, I32, I32, P]
         L.or_topk.argtypes = [P, P, I32, I32, I32, I32, P]
+        L.or_block_mean.argtypes = [P, I64, I64, I32, I32, P]
+        L.or_block_score_mean.argtypes = [P, P, P, I32, I32, I32, I32, I32, I32, P]
         L.or_lru.argtypes = [P, I64, P, P, ctypes.c_int32, P, P, I32, I32, I32, I32, I32, I32,
                              I64, P, P, P, P, P]
         L.or_lru.restype = ctypes.c_int
@@ -97,6 +99,32 @@ def block_score(q: np.ndarray, meta: np.ndarray, n_blk: np.ndarray) -> np.ndarra
     n_blk = np.ascontiguousarray(n_blk, dtype=np.int32)
     out = np.full((B, Hkv, max_blk), np.nan, dtype=np.float64)
     lib().or_block_score(_p(q), _p(meta), _p(n_blk), B, Hq, Hkv, d, max_blk, _dt(q), _p(out))
+    return out
+
+
+def block_mean(keys: np.ndarray, key_stride: Optional[int] = None) -> np.ndarray:
+    """NEXT-3 mean-of-keys metadata. keys: [n][32][d] (or blocks [n][2][32][d]
+    with key_stride=2*32*d).  Returns float32 [n][d]."""
+    keys = np.ascontiguousarray(keys)
+    n = keys.shape[0]
+    d = keys.shape[-1]
+    if key_stride is None:
+        key_stride = int(np.prod(keys.shape[1:]))
+    out = np.empty((n, d), dtype=np.float32)
+    lib().or_block_mean(_p(keys), key_stride, n, _dt(keys), d, _p(out))
+    return out
+
+
+def block_score_mean(q: np.ndarray, meta: np.ndarray, n_blk: np.ndarray) -> np.ndarray:
+    """NEXT-3 score. q: [B][Hq][d] (uint16 bf16 bits or float32); meta: float32
+    [B][Hkv][max_blk][d]; returns float64 [B][Hkv][max_blk] (NaN for j >= n_blk)."""
+    q = np.ascontiguousarray(q)
+    meta = np.ascontiguousarray(meta, dtype=np.float32)
+    B, Hq, d = q.shape
+    _, Hkv, max_blk, _ = meta.shape
+    n_blk = np.ascontiguousarray(n_blk, dtype=np.int32)
+    out = np.full((B, Hkv, max_blk), np.nan, dtype=np.float64)
+    lib().or_block_score_mean(_p(q), _p(meta), _p(n_blk), B, Hq, Hkv, d, max_blk, _dt(q), _p(out))
     return out
 
 

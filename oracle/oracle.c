@@ -23,6 +23,10 @@
  *                       call), hand-traced fixture tests/golden/lru_trace.json,
  *                       capacity error leaves state byte-identical
  *   or_gather       S4  pinned: numpy fancy-index byte comparison
+ *   or_block_mean   NEXT-3 pinned: exact rational mean (fractions.Fraction),
+ *                       numpy float64 mean, identical-token blocks (mean = key)
+ *   or_block_score_mean NEXT-3 pinned: exact rationals; identical-token blocks
+ *                       score exactly like the min/max bound (M = m = mu)
  *   or_attention    S5  pinned: torch scaled_dot_product_attention (fp64, CPU)
  *                       when k covers all blocks; masked-dense equivalence
  */
@@ -103,6 +107,50 @@ void or_block_score(const void* q, const void* meta, const int32_t* n_blk, int B
                     if (g == 0 || acc > best) best = acc;
                 }
                 scores[((int64_t)b * Hkv + h) * max_blk + j] = best + 0.0; /* -0 -> +0 */
+            }
+}
+
+/* ------------------------------------------------------------------------
+ * NEXT-3  mean-of-keys metadata ("ranging from simply calculating the
+ * mean values of the token keys [45] to finding the bounding cuboid of the
+ * token keys [9]"; "other metadata construction methods [41, 45] can be
+ * easily integrated").  Reading R18: one metadata vector per
+ * block, mu_c = (sum_{t=0..31} K[t][c]) / 32 with the sum taken in float64
+ * sequentially t = 0..31 from +0.0 (the division by 32 is exact), rounded
+ * once to float32 (round-to-nearest-even) for storage.  meta_out: [n][d]
+ * float32 whatever the key dtype.
+ * ---------------------------------------------------------------------- */
+void or_block_mean(const void* keys, int64_t key_stride, int64_t n, int dt, int d,
+                   float* meta_out) {
+    for (int64_t i = 0; i < n; ++i)
+        for (int c = 0; c < d; ++c) {
+            double acc = 0.0;
+            for (int t = 0; t < OR_BLOCK_TOKENS; ++t)
+                acc = acc + ld(keys, dt, i * key_stride + (int64_t)t * d + c);
+            meta_out[i * d + c] = (float)(acc / 32.0);
+        }
+}
+
+/* NEXT-3 score: S(j) = max_g sum_c q_{g,c} * mu_{j,c} -- the dot product of the
+ * query with the block's metadata vector; float64, sequential in c from
+ * +0.0, +0 canonical (R3, R4 as for the min/max score).  Every product is exact
+ * in float64 (bf16 or f32 q times a float32 mu: <= 48 significant bits).
+ * q: [B][Hq][d] dtype dt; meta: [B][Hkv][max_blk][d] float32. */
+void or_block_score_mean(const void* q, const float* meta, const int32_t* n_blk, int B, int Hq,
+                         int Hkv, int d, int max_blk, int dt, double* scores) {
+    int G = Hq / Hkv;
+    for (int b = 0; b < B; ++b)
+        for (int h = 0; h < Hkv; ++h)
+            for (int j = 0; j < n_blk[b]; ++j) {
+                const float* mu = meta + (((int64_t)b * Hkv + h) * max_blk + j) * d;
+                double best = 0.0;
+                for (int g = 0; g < G; ++g) {
+                    int64_t qbase = ((int64_t)b * Hq + (int64_t)h * G + g) * d;
+                    double acc = 0.0;
+                    for (int c = 0; c < d; ++c) acc = acc + ld(q, dt, qbase + c) * (double)mu[c];
+                    if (g == 0 || acc > best) best = acc;
+                }
+                scores[((int64_t)b * Hkv + h) * max_blk + j] = best + 0.0;
             }
 }
 

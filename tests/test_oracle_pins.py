@@ -437,3 +437,77 @@ def test_prefill_save_matches_numpy_relayout():
         np.testing.assert_array_equal(tail[b, h, 0, :11], k[nb * 32:, h])
         np.testing.assert_array_equal(tail[b, h, 1, :11], v[nb * 32:, h])
     assert n_blk[b] == nb and tl[b] == 11
+
+
+# ----------------------------------------------------------------------------
+# NEXT-3 mean-of-keys metadata and its score ("simply calculating the mean
+# values of the token keys [45]"; reading R18)
+# ----------------------------------------------------------------------------
+def _f32_of_exact(fr):
+    """float32 nearest (RNE) to an exact rational that fits float64 exactly."""
+    x = float(fr)
+    assert Fraction(x) == fr
+    return np.float32(x)
+
+
+@pytest.mark.parametrize("dt", [synth.DT_BF16, synth.DT_F32])
+def test_mean_meta_is_exact_rational_mean(dt):
+    # dyadic keys: the exact mean is a float32 value, so mu must equal it exactly
+    rng = np.random.default_rng(31)
+    keys = (rng.integers(-16, 17, size=(5, 2, 32, D)) / 8.0).astype(np.float32)
+    store = synth.encode(keys, dt)
+    mu = oracle.block_mean(store, key_stride=2 * 32 * D)
+    kv = synth.decode_f64(store, dt)[:, 0]
+    for i in range(5):
+        for c in range(0, D, 7):
+            ex = sum(Fraction(v) for v in kv[i, :, c]) / 32
+            assert mu[i, c] == _f32_of_exact(ex)
+
+
+def test_mean_meta_gaussian_keys_round_once():
+    # realistic bf16 keys: the fp64 sum of 32 bf16 values is exact here, so mu is
+    # the float32 rounding of the exact mean; numpy's float64 mean agrees to 1 ulp
+    rng = synth.rng_for(901, 1)
+    blocks = synth.kv_blocks(rng, 9, D, synth.channel_scales(rng))
+    store = synth.encode(blocks, synth.DT_BF16)
+    mu = oracle.block_mean(store, key_stride=2 * 32 * D)
+    kv = synth.decode_f64(store, synth.DT_BF16)[:, 0]
+    for i in range(9):
+        for c in range(D):
+            ex = sum(Fraction(v) for v in kv[i, :, c]) / 32
+            if Fraction(float(ex)) == ex:
+                assert mu[i, c] == _f32_of_exact(ex)
+    np.testing.assert_allclose(mu, kv.mean(axis=1), rtol=2 ** -23, atol=0)
+
+
+def test_mean_score_exact_and_gqa_max():
+    rng = np.random.default_rng(32)
+    B, Hq, Hkv, n = 2, 8, 2, 5
+    G = Hq // Hkv
+    q = (rng.integers(-4, 5, size=(B, Hq, D)) / 2.0).astype(np.float32)
+    keys = (rng.integers(-8, 9, size=(B * Hkv * n, 2, 32, D)) / 4.0).astype(np.float32)
+    qs, ks = _bf16(q), _bf16(keys)
+    mu = oracle.block_mean(ks, key_stride=2 * 32 * D).reshape(B, Hkv, n, D)
+    sc = oracle.block_score_mean(qs, mu, np.array([n, n - 2], np.int32))
+    qv, kv = _val(qs), _val(ks)[:, 0].reshape(B, Hkv, n, 32, D)
+    for b in range(B):
+        for h in range(Hkv):
+            for j in range(n - 2 * b):
+                mean = [sum(Fraction(v) for v in kv[b, h, j, :, c]) / 32 for c in range(D)]
+                per = [sum(Fraction(qc) * m for qc, m in zip(qv[b, h * G + g], mean)) for g in range(G)]
+                assert Fraction(sc[b, h, j]) == max(per)
+    assert np.isnan(sc[1, :, n - 2:]).all()
+
+
+def test_mean_score_of_identical_tokens_equals_minmax_score():
+    # all tokens of a block equal: mean = M = m = the key, so the mean score and
+    # the (separately pinned) min/max bound are the same exact dot product
+    rng = synth.rng_for(901, 2)
+    k1 = rng.standard_normal((6, 1, 1, D)).astype(np.float32)
+    ks = _bf16(np.broadcast_to(k1, (6, 2, 32, D)).copy())
+    qs = _bf16(rng.standard_normal((1, 4, D)))
+    mu = oracle.block_mean(ks, key_stride=2 * 32 * D).reshape(1, 1, 6, D)
+    np.testing.assert_array_equal(mu[0, 0], _val(ks)[:, 0, 0])
+    s_mean = oracle.block_score_mean(qs, mu, np.array([6], np.int32))
+    s_mm = oracle.block_score(qs, _meta_from_blocks(ks, 1, 1, 6), np.array([6], np.int32))
+    np.testing.assert_array_equal(s_mean, s_mm)
