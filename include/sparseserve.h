@@ -115,6 +115,33 @@ ss_status ss_block_select(const void* q, const void* meta, const int32_t* n_blk,
                           int32_t max_blk, int32_t k, ss_dims dims, ss_dtype dt, int32_t* sel,
                           double* scores, void* ws, size_t ws_bytes, void* stream);
 
+/* NEXT-3  mean-of-keys metadata -- PAPER.md:94 "Different DSAs propose various
+ * metadata construction methods, ranging from simply calculating the mean
+ * values of the token keys [45] to finding the bounding cuboid of the token keys
+ * [9]"; "other metadata construction methods [41, 45] can be
+ * easily integrated into SparseServe".  An alternative to the min/max pair
+ * above (reading R18 in DESIGN.md).
+ *
+ * Mean metadata layout (HBM): ONE float32 vector per block, whatever the KV
+ * dtype: mu[c] = (sum_{t=0..31} K[t][c]) / 32, the sum in float64 sequentially
+ * t = 0..31 from +0.0, rounded once to float32 (round-to-nearest-even).  Tiled
+ * like the min/max layout: tile T = idx / 32, row r = idx % 32, channel c at
+ * float offset  T * (32 * d)  +  ((c / 4) * 32 + r) * 4  +  c % 4  (a tile is
+ * 16 KiB: the same bytes per block as bf16 min/max).
+ *
+ * block_meta_update_mean: arguments as block_meta_update; meta is the float32
+ *   mean layout above (device).
+ * ss_block_select_mean: arguments as ss_block_select, with meta the float32
+ *   mean layout; the score is S(j) = max_{g<G} sum_{c=0..d-1} q_c * mu_c
+ *   (float64, sequential in c, every product exact, +0 canonical); same top-k,
+ *   tie rule, output order, padding, workspace (SS_WS_SELECT) and errors. */
+ss_status block_meta_update_mean(const void* keys, int64_t key_stride, const int64_t* dst_idx,
+                                 int64_t n, float* meta, ss_dtype dt, int32_t head_dim,
+                                 void* stream);
+ss_status ss_block_select_mean(const void* q, const float* meta, const int32_t* n_blk,
+                               int32_t max_blk, int32_t k, ss_dims dims, ss_dtype dt, int32_t* sel,
+                               double* scores, void* ws, size_t ws_bytes, void* stream);
+
 /* S3  kv_cache_lookup_insert -- PAPER.md:124-125: the executor sends the
  * indices of the required blocks to the KV cache manager; hot blocks are cached
  * in the remaining HBM with LRU eviction; DRAM is the authoritative home (no

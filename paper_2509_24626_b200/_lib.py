@@ -19,7 +19,8 @@ SS_WS_SELECT, SS_WS_CACHE, SS_WS_ATTN, SS_WS_SEAL, SS_WS_PREFILL = 0, 1, 2, 3, 4
 EXPORTS = ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert", "flash_h2d_gather",
            "sparse_decode_attn", "ss_workspace_size", "ss_host_device_pointer",
            "ss_status_string", "ss_version", "kv_append", "kv_seal_blocks", "kv_commit",
-           "ss_d2h_create", "ss_d2h_destroy", "flash_d2h_save", "ws_track", "ss_admit", "prefill_layer_save")
+           "ss_d2h_create", "ss_d2h_destroy", "flash_d2h_save", "ws_track", "ss_admit", "prefill_layer_save",
+           "block_meta_update_mean", "ss_block_select_mean")
 
 
 class SSDims(ctypes.Structure):
@@ -54,6 +55,8 @@ def load() -> ctypes.CDLL:
     P, I32, I64, SZ, F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_float
     L.block_meta_update.argtypes = [P, I64, P, I64, P, I32, I32, P]
     L.ss_block_select.argtypes = [P, P, P, I32, I32, SSDims, I32, P, P, P, SZ, P]
+    L.block_meta_update_mean.argtypes = [P, I64, P, I64, P, I32, I32, P]
+    L.ss_block_select_mean.argtypes = [P, P, P, I32, I32, SSDims, I32, P, P, P, SZ, P]
     L.kv_cache_lookup_insert.argtypes = [SSCachePool, P, P, I32, I32, I32, I32, SSDims, I64, P, P,
                                          P, P, P, P, SZ, P]
     L.flash_h2d_gather.argtypes = [P, I64, P, P, P, I32, P, I64, P]
@@ -80,7 +83,7 @@ def load() -> ctypes.CDLL:
     for name in ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert",
                  "flash_h2d_gather", "sparse_decode_attn", "ss_host_device_pointer", "kv_append",
                  "kv_seal_blocks", "kv_commit", "ss_d2h_create", "ss_d2h_destroy",
-                 "flash_d2h_save"):
+                 "flash_d2h_save", "block_meta_update_mean", "ss_block_select_mean"):
         getattr(L, name).restype = I32
     _lib = L
     return L

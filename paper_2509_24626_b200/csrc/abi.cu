@@ -10,7 +10,9 @@ ss_status launch_meta_update(const void* keys, int64_t key_stride, const int64_t
                              int64_t n, void* meta, ss_dtype dt, cudaStream_t stream);
 ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_blk, int max_blk,
                               int k, const ss_dims& d, ss_dtype dt, int32_t* sel, double* scores,
-                              void* ws, cudaStream_t stream);
+                              void* ws, cudaStream_t stream, bool mean);
+ss_status launch_meta_mean(const void* keys, int64_t key_stride, const int64_t* dst_idx, int64_t n,
+                           float* meta, ss_dtype dt, cudaStream_t stream);
 size_t select_ws_bytes(const ss_dims& d, int max_blk, int k);
 ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int32_t* req_ids,
                        int layer, int num_layers, int max_blk, int k, const ss_dims& d,
@@ -80,7 +82,30 @@ ss_status ss_block_select(const void* q, const void* meta, const int32_t* n_blk,
     size_t need = ss::select_ws_bytes(dims, max_blk, k);
     if (ws_bytes < need || (need && !ws)) return SS_ERR_INVALID_ARG;
     return ss::launch_block_select(q, meta, n_blk, max_blk, k, dims, dt, sel, scores, ws,
-                                   (cudaStream_t)stream);
+                                   (cudaStream_t)stream, false);
+}
+
+ss_status block_meta_update_mean(const void* keys, int64_t key_stride, const int64_t* dst_idx,
+                                 int64_t n, float* meta, ss_dtype dt, int32_t head_dim, void* stream) {
+    if (n < 0 || !dt_ok(dt)) return SS_ERR_INVALID_ARG;
+    if (n == 0) return SS_OK;
+    if (!keys || !meta || key_stride < 32 * head_dim) return SS_ERR_INVALID_ARG;
+    if (head_dim != ss::kHeadDim) return SS_ERR_UNSUPPORTED;
+    return ss::launch_meta_mean(keys, key_stride, dst_idx, n, meta, dt, (cudaStream_t)stream);
+}
+
+ss_status ss_block_select_mean(const void* q, const float* meta, const int32_t* n_blk,
+                               int32_t max_blk, int32_t k, ss_dims dims, ss_dtype dt, int32_t* sel,
+                               double* scores, void* ws, size_t ws_bytes, void* stream) {
+    if (!q || !meta || !n_blk || !sel || !dt_ok(dt) || !dims_ok(dims)) return SS_ERR_INVALID_ARG;
+    if (k < 1 || max_blk < 0 || (max_blk % 32) != 0) return SS_ERR_INVALID_ARG;
+    if (!aligned16(q) || !aligned16(meta)) return SS_ERR_INVALID_ARG;
+    ss_status st = dims_supported(dims);
+    if (st != SS_OK) return st;
+    size_t need = ss::select_ws_bytes(dims, max_blk, k);
+    if (ws_bytes < need || (need && !ws)) return SS_ERR_INVALID_ARG;
+    return ss::launch_block_select(q, meta, n_blk, max_blk, k, dims, dt, sel, scores, ws,
+                                   (cudaStream_t)stream, true);
 }
 
 ss_status kv_cache_lookup_insert(ss_cache_pool pool, const int32_t* sel, const int32_t* req_ids,

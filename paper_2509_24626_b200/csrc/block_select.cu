@@ -55,6 +55,26 @@ __device__ __forceinline__ uint64_t ord_key(double s) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// Integer-built float64 operands (no F2F conversion).  A bf16 half-word h with
+// its 15 magnitude bits shifted into the float64 exponent/fraction fields (the
+// sign kept in bit 63) is the float64 whose value is EXACTLY h * 2^-896, for
+// every finite h including +-0 and subnormals (the 8-bit exponent lands in the
+// low bits of the 11-bit field; bf16 subnormals become float64 subnormals,
+// which DFMA handles at full rate).  q is pre-scaled by 2^896 (exact; a finite
+// bf16/f32 |q| < 2^128 stays below DBL_MAX), so fma(q*2^896, X', acc) rounds
+// acc + q*X once, exactly as the oracle does.  2.5 integer ops per channel
+// (arithmetic shift + LOP3 mask) replace a quarter-rate F2F.
+constexpr double kQScale = 0x1p896;
+__device__ __forceinline__ double bf16_lo_scaled(uint32_t w) {  // bits 15..0
+    return __hiloint2double(((int32_t)(w << 16) >> 3) & (int32_t)0x8FFFFFFF, 0);
+}
+__device__ __forceinline__ double bf16_hi_scaled(uint32_t w) {  // bits 31..16
+    return __hiloint2double(((int32_t)w >> 3) & (int32_t)0x8FFFE000, 0);
+}
+__device__ __forceinline__ double f32_scaled(uint32_t x) {
+    return __hiloint2double(((int32_t)x >> 3) & (int32_t)0x8FFFFFFF, (int32_t)(x << 29));
+}
+
 // ---------------------------------------------------------------------------
 // CTA-wide top-k over keys[0..n): largest keys, ties -> lower position.
 // Writes the selected positions, ascending, to out_pos (smem or global via
@@ -141,7 +161,7 @@ __device__ void cta_topk(const uint64_t* keys, int n, int k_sel, int* hist, int*
 }
 
 // ---------------------------------------------------------------------------
-template <bool BF16, int G>
+template <bool BF16, int G, bool ICV, bool MEAN>
 __global__ void __launch_bounds__(kSelThreads, 2)
 block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                     const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
@@ -177,12 +197,12 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     // f32->f64 convert and ONE DFMA: acc + q*(q>=0 ? M : m) == acc + max(qM, qm).
     double* qd1 = (double*)smem_raw;                        // [128]
     uint32_t* qmask1 = (uint32_t*)(smem_raw + kHeadDim * 8); // [128] (bf16 uses 64)
-    if constexpr (G == 1) {
+    if constexpr (G == 1 && !MEAN) {
         for (int c = tid; c < kHeadDim; c += kSelThreads) {
             size_t qi = ((size_t)b * Hq + h) * kHeadDim + c;
             double qv = BF16 ? (double)__uint_as_float(((uint32_t)((const uint16_t*)q)[qi]) << 16)
                              : (double)((const float*)q)[qi];
-            qd1[c] = qv;
+            qd1[c] = ICV ? qv * kQScale : qv;
         }
         __syncthreads();
         for (int i = tid; i < kHeadDim / (BF16 ? 2 : 1); i += kSelThreads) {
@@ -195,7 +215,17 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
         }
     }
     // G > 1: q for the G query heads of this KV head, as (q+, q-) = (max(q,0), min(q,0)).
-    if constexpr (G > 1)
+    // NEXT-3 mean metadata: q of the G heads as float64 (x 2^896 with ICV), [c][g]
+    double* qm = (double*)smem_raw;
+    if constexpr (MEAN)
+    for (int i = tid; i < kHeadDim * G; i += kSelThreads) {
+        const int g = i % G, c = i / G;
+        const size_t qi = ((size_t)b * Hq + (size_t)h * G + g) * kHeadDim + c;
+        const double qd = BF16 ? (double)__uint_as_float(((uint32_t)((const uint16_t*)q)[qi]) << 16)
+                               : (double)((const float*)q)[qi];
+        qm[i] = ICV ? qd * kQScale : qd;
+    }
+    if constexpr (G > 1 && !MEAN)
     for (int i = tid; i < kHeadDim * G; i += kSelThreads) {
         int g = i % G, c = i / G;
         size_t qi = ((size_t)b * Hq + (size_t)h * G + g) * kHeadDim + c;
@@ -204,6 +234,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
             qd = (double)__uint_as_float(((uint32_t)((const uint16_t*)q)[qi]) << 16);
         else
             qd = (double)((const float*)q)[qi];
+        if (ICV) qd *= kQScale;
         qpn[i] = make_double2(qd > 0.0 ? qd : 0.0, qd < 0.0 ? qd : 0.0);
     }
     __syncthreads();
@@ -211,9 +242,45 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     const int j0 = ci * CH;
     const int nb_chunk = min(CH, nb - j0);  // >= 0 (0 only if nb == 0)
     const int ntiles = (nb_chunk + 31) / 32;
-    const char* meta_pair = (const char*)meta + ((size_t)pair * (max_blk / 32)) * TILE_ELEMS * ES;
+    constexpr size_t TILE_BYTES = MEAN ? (size_t)32 * kHeadDim * 4 : (size_t)TILE_ELEMS * ES;
+    const char* meta_pair = (const char*)meta + ((size_t)pair * (max_blk / 32)) * TILE_BYTES;
 
-    if constexpr (G == 1)
+    // NEXT-3: S(j) = max_g sum_c q_{g,c} mu_{j,c}.  Tile [32 chunks][32 blocks][4 ch]
+    // float32: lane r scores block r; chunk s (channels 4s..4s+3) of the warp's 32
+    // blocks is one contiguous 512-byte segment.  One exact operand build per
+    // channel, G DFMAs (the products q*mu are exact: <= 48 significant bits).
+    if constexpr (MEAN)
+    for (int tl = warp; tl < ntiles; tl += kSelWarps) {
+        const char* tb = meta_pair + (size_t)(j0 / 32 + tl) * TILE_BYTES + lane * 16;
+        constexpr int NCM = kHeadDim / 4, D = 8, R = D + 1;
+        uint4 mv[R];
+#pragma unroll
+        for (int s = 0; s < D; ++s) mv[s] = ldg_stream(tb + (size_t)s * 512);
+        double acc[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[g] = 0.0;
+#pragma unroll
+        for (int s = 0; s < NCM; ++s) {
+            if (s + D < NCM) mv[(s + D) % R] = ldg_stream(tb + (size_t)(s + D) * 512);
+            const uint32_t w4[4] = {mv[s % R].x, mv[s % R].y, mv[s % R].z, mv[s % R].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int c = 4 * s + e;
+                const double x = ICV ? f32_scaled(w4[e]) : (double)__uint_as_float(w4[e]);
+#pragma unroll
+                for (int g = 0; g < G; ++g) acc[g] = __fma_rn(qm[c * G + g], x, acc[g]);
+            }
+        }
+        double sc = acc[0];
+#pragma unroll
+        for (int g = 1; g < G; ++g) sc = acc[g] > sc ? acc[g] : sc;
+        sc = sc + 0.0;
+        const int pos = tl * 32 + lane;
+        keys[pos] = ord_key(sc);
+        if (scores != nullptr && j0 + pos < nb) scores[(size_t)pair * max_blk + j0 + pos] = sc;
+    }
+
+    if constexpr (G == 1 && !MEAN)
     for (int tl = warp; tl < ntiles; tl += kSelWarps) {
         const int tile = j0 / 32 + tl;
         const char* tb = meta_pair + (size_t)tile * TILE_ELEMS * ES + lane * 16;
@@ -244,10 +311,10 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                 const uint32_t y = (ax[i] & am[i]) | (an[i] & ~am[i]);
                 if (BF16) {
                     const double2 qq = *reinterpret_cast<const double2*>(qd1 + s * 8 + 2 * i);
-                    acc = __fma_rn(qq.x, (double)__uint_as_float(y << 16), acc);
-                    acc = __fma_rn(qq.y, (double)__uint_as_float(y & 0xFFFF0000u), acc);
+                    acc = __fma_rn(qq.x, ICV ? bf16_lo_scaled(y) : (double)__uint_as_float(y << 16), acc);
+                    acc = __fma_rn(qq.y, ICV ? bf16_hi_scaled(y) : (double)__uint_as_float(y & 0xFFFF0000u), acc);
                 } else {
-                    acc = __fma_rn(qd1[s * 4 + i], (double)__uint_as_float(y), acc);
+                    acc = __fma_rn(qd1[s * 4 + i], ICV ? f32_scaled(y) : (double)__uint_as_float(y), acc);
                 }
             }
         }
@@ -258,7 +325,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
         if (scores != nullptr && j < nb) scores[(size_t)pair * max_blk + j] = s;
     }
 
-    if constexpr (G > 1)
+    if constexpr (G > 1 && !MEAN)
     for (int tl = warp; tl < ntiles; tl += 2 * kSelWarps) {
         // two tiles per warp pass (lane r scores block r of tile tl and of tile
         // tl + 8): each shared-memory (q+, q-) load serves two blocks and two
@@ -296,7 +363,18 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
 #pragma unroll
             for (int e = 0; e < CPC; ++e) {
                 double dminA, dmaxA, dminB, dmaxB;
-                if (BF16) {
+                if (BF16 && ICV) {
+                    const int w = e >> 1;
+                    dminA = (e & 1) ? bf16_hi_scaled(wnA[w]) : bf16_lo_scaled(wnA[w]);
+                    dmaxA = (e & 1) ? bf16_hi_scaled(wxA[w]) : bf16_lo_scaled(wxA[w]);
+                    dminB = (e & 1) ? bf16_hi_scaled(wnB[w]) : bf16_lo_scaled(wnB[w]);
+                    dmaxB = (e & 1) ? bf16_hi_scaled(wxB[w]) : bf16_lo_scaled(wxB[w]);
+                } else if (ICV) {
+                    dminA = f32_scaled(wnA[e]);
+                    dmaxA = f32_scaled(wxA[e]);
+                    dminB = f32_scaled(wnB[e]);
+                    dmaxB = f32_scaled(wxB[e]);
+                } else if (BF16) {
                     const int w = e >> 1;
                     dminA = (double)__uint_as_float((e & 1) ? (wnA[w] & 0xFFFF0000u) : (wnA[w] << 16));
                     dmaxA = (double)__uint_as_float((e & 1) ? (wxA[w] & 0xFFFF0000u) : (wxA[w] << 16));
@@ -379,39 +457,44 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     }  // work items
 }
 
-// Blocks scored per CTA.  2048 by default; SS_SEL_CHUNK (multiple of 32, <= 2048)
-// overrides it for tuning.  Workspace sizing and launches use the same value.
-static int sel_chunk() {
-    static int c = [] {
+// Blocks scored per CTA: 1024 for MHA (G = 1), 2048 for GQA (G > 1: 4-8x the
+// fp64 work per block, so longer CTAs amortise the q setup and the top-k);
+// measured best at C2 / C3 (tools/kbench.py).  SS_SEL_CHUNK (multiple of 32,
+// <= 2048) overrides both.  Workspace sizing and launches use the same value.
+static int sel_chunk(int G) {
+    static const int env = [] {
         const char* e = getenv("SS_SEL_CHUNK");
-        int v = e ? atoi(e) : kSelChunkDefault;
-        if (v < 32 || v > kSelChunkMax || (v % 32)) v = kSelChunkMax;
+        int v = e ? atoi(e) : 0;
+        if (e && (v < 32 || v > kSelChunkMax || (v % 32))) v = kSelChunkMax;
         return v;
     }();
-    return c;
+    if (env) return env;
+    return G > 1 ? kSelChunkMax : kSelChunkDefault;
 }
 
 size_t select_ws_bytes(const ss_dims& d, int max_blk, int k) {
-    int nchunks = (max_blk + sel_chunk() - 1) / sel_chunk();
+    const int G = d.num_kv_heads > 0 ? d.num_q_heads / d.num_kv_heads : 1;
+    int nchunks = (max_blk + sel_chunk(G) - 1) / sel_chunk(G);
     size_t pairs = (size_t)d.batch * d.num_kv_heads;
     size_t nc = (size_t)pairs * nchunks * k;
     size_t bytes = nc * 8 + nc * 4 + pairs * 4;
     return (bytes + 255) & ~(size_t)255;
 }
 
-template <bool BF16, int G>
+template <bool BF16, int G, bool ICV, bool MEAN>
 static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_blk, int max_blk,
                               int k, const ss_dims& d, int32_t* sel, double* scores, void* ws,
                               cudaStream_t stream) {
-    int nchunks = (max_blk + sel_chunk() - 1) / sel_chunk();
+    const int CH = sel_chunk(G);
+    int nchunks = (max_blk + CH - 1) / CH;
     size_t pairs = (size_t)d.batch * d.num_kv_heads;
     size_t nc = pairs * nchunks * k;
     uint64_t* cand_key = (uint64_t*)ws;
     int32_t* cand_j = (int32_t*)((char*)ws + nc * 8);
     int32_t* tickets = (int32_t*)((char*)ws + nc * 12);
-    int nkeys = max(sel_chunk(), min(nchunks * k, kSelMaxMerge));
+    int nkeys = max(CH, min(nchunks * k, kSelMaxMerge));
     size_t smem = SelSmemLayout::bytes(G, nkeys);
-    auto kern = block_select_kernel<BF16, G>;
+    auto kern = block_select_kernel<BF16, G, ICV, MEAN>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return SS_ERR_CUDA;
@@ -422,7 +505,7 @@ static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_
     static const int l2pf = getenv("SS_SEL_L2PF") ? atoi(getenv("SS_SEL_L2PF")) : 0;
     const int grid = (persist && items > 2 * kNumSMs) ? 2 * kNumSMs : items;
     kern<<<grid, kSelThreads, smem, stream>>>(q, meta, n_blk, max_blk, k, d.num_q_heads,
-                                              d.num_kv_heads, nchunks, sel_chunk(), (int)pairs, l2pf, sel, scores, cand_key,
+                                              d.num_kv_heads, nchunks, CH, (int)pairs, l2pf, sel, scores, cand_key,
                                               cand_j, tickets);
     SS_LAUNCH_CHECK();
     return SS_OK;
@@ -430,17 +513,23 @@ static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_
 
 ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_blk, int max_blk,
                               int k, const ss_dims& d, ss_dtype dt, int32_t* sel, double* scores,
-                              void* ws, cudaStream_t stream) {
-    int nchunks = (max_blk + sel_chunk() - 1) / sel_chunk();
-    if ((size_t)nchunks * k > kSelMaxMerge && nchunks > 1) return SS_ERR_UNSUPPORTED;
+                              void* ws, cudaStream_t stream, bool mean) {
     int G = d.num_q_heads / d.num_kv_heads;
-#define SS_SEL_CASE(GG)                                                                   \
-    case GG:                                                                              \
-        return dt == SS_BF16                                                              \
-                   ? launch_sel_t<true, GG>(q, meta, n_blk, max_blk, k, d, sel, scores, ws, \
-                                            stream)                                       \
-                   : launch_sel_t<false, GG>(q, meta, n_blk, max_blk, k, d, sel, scores, ws, \
-                                             stream);
+    int nchunks = (max_blk + sel_chunk(G) - 1) / sel_chunk(G);
+    if ((size_t)nchunks * k > kSelMaxMerge && nchunks > 1) return SS_ERR_UNSUPPORTED;
+    // integer-built float64 operands (default) or F2F conversions (SS_SEL_ICV=0, A/B only)
+    static const bool icv = getenv("SS_SEL_ICV") ? atoi(getenv("SS_SEL_ICV")) != 0 : true;
+#define SS_SEL_ARGS q, meta, n_blk, max_blk, k, d, sel, scores, ws, stream
+#define SS_SEL_CASE(GG)                                                                       \
+    case GG:                                                                                  \
+        if (mean)                                                                             \
+            return dt == SS_BF16 ? launch_sel_t<true, GG, true, true>(SS_SEL_ARGS)            \
+                                 : launch_sel_t<false, GG, true, true>(SS_SEL_ARGS);          \
+        if (dt == SS_BF16)                                                                    \
+            return icv ? launch_sel_t<true, GG, true, false>(SS_SEL_ARGS)                     \
+                       : launch_sel_t<true, GG, false, false>(SS_SEL_ARGS);                   \
+        return icv ? launch_sel_t<false, GG, true, false>(SS_SEL_ARGS)                        \
+                   : launch_sel_t<false, GG, false, false>(SS_SEL_ARGS);
     switch (G) {
         SS_SEL_CASE(1)
         SS_SEL_CASE(2)
@@ -450,6 +539,7 @@ ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_
             return SS_ERR_UNSUPPORTED;
     }
 #undef SS_SEL_CASE
+#undef SS_SEL_ARGS
 }
 
 }  // namespace ss

@@ -69,6 +69,9 @@ ss_status launch_flash_h2d(const void* host_kv, int64_t host_blocks, const int64
                            const int32_t* miss_slots, const int32_t* counts, int max_misses,
                            void* pool_kv, int64_t block_bytes, cudaStream_t stream) {
     if (max_misses <= 0) return SS_OK;
+    // experiment knob: SS_H2D_SKIP=1 launches nothing (the step without PCIe time)
+    static const bool skip = getenv("SS_H2D_SKIP") && atoi(getenv("SS_H2D_SKIP")) != 0;
+    if (skip) return SS_OK;
     int64_t warps_needed = max_misses;
     static const int threads = getenv("SS_H2D_THREADS") ? atoi(getenv("SS_H2D_THREADS")) : 128;
     int64_t grid = (warps_needed * 32 + threads - 1) / threads;

@@ -64,6 +64,49 @@ __global__ void __launch_bounds__(128) meta_update_kernel(const E* __restrict__ 
     }
 }
 
+// NEXT-3 mean-of-keys metadata ("simply calculating the mean values
+// of the token keys [45]"; reading R18): thread c sums channel c of the 32 keys
+// in float64, t = 0..31 in order from +0.0 (bit-identical to the oracle's
+// sequential sum), divides by 32 (exact) and rounds once to float32.  Tiled
+// float32 layout (include/sparseserve.h): tile T = idx / 32 holds 32 blocks x
+// d channels as [d/4 chunks][32 blocks][4 channels] (16 KiB), so lane r of a
+// select warp reads block r's 16-byte chunks as contiguous 512-byte segments.
+template <typename E>
+__global__ void __launch_bounds__(128) meta_mean_kernel(const E* __restrict__ keys,
+                                                        int64_t key_stride,
+                                                        const int64_t* __restrict__ dst_idx,
+                                                        int64_t n, float* __restrict__ meta) {
+    const int c = threadIdx.x;
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const E* kb = keys + i * key_stride;
+        double acc = 0.0;
+#pragma unroll 8
+        for (int t = 0; t < kBlockTokens; ++t) {
+            const E v = kb[t * kHeadDim + c];
+            const float f = sizeof(E) == 2 ? __uint_as_float((uint32_t)v << 16) : __uint_as_float((uint32_t)v);
+            acc = __dadd_rn(acc, (double)f);
+        }
+        const float mu = __double2float_rn(acc * (1.0 / 32.0));
+        const int64_t idx = dst_idx ? dst_idx[i] : i;
+        float* mt = meta + (idx >> 5) * (int64_t)(32 * kHeadDim);
+        mt[((c >> 2) * 32 + (int)(idx & 31)) * 4 + (c & 3)] = mu;
+    }
+}
+
+ss_status launch_meta_mean(const void* keys, int64_t key_stride, const int64_t* dst_idx, int64_t n,
+                           float* meta, ss_dtype dt, cudaStream_t stream) {
+    if (n == 0) return SS_OK;
+    int grid = (int)(n < 65535 * 4 ? n : 65535 * 4);
+    if (dt == SS_BF16)
+        meta_mean_kernel<uint16_t><<<grid, 128, 0, stream>>>((const uint16_t*)keys, key_stride,
+                                                               dst_idx, n, meta);
+    else
+        meta_mean_kernel<uint32_t><<<grid, 128, 0, stream>>>((const uint32_t*)keys, key_stride,
+                                                               dst_idx, n, meta);
+    SS_LAUNCH_CHECK();
+    return SS_OK;
+}
+
 ss_status launch_meta_update(const void* keys, int64_t key_stride, const int64_t* dst_idx,
                              int64_t n, void* meta, ss_dtype dt, cudaStream_t stream) {
     if (n == 0) return SS_OK;

@@ -290,7 +290,7 @@ class DecodeEngine:
     def outputs(self) -> List[torch.Tensor]:
         return [g.out for g in self.groups]
 
-    def capture_graph(self, q_static: torch.Tensor, post_attn=None) -> "torch.cuda.CUDAGraph":
+    def capture_graph(self, q_static: torch.Tensor, post_attn=None, timers=None) -> "torch.cuda.CUDAGraph":
         """Capture one whole decode step (all layers, all request groups and
         streams) into a CUDA graph reading q from `q_static` [L][B][Hq][d].
         Requires device clocks on the pools (`use_device_clock()`), so each
@@ -305,7 +305,7 @@ class DecodeEngine:
         try:
             with torch.cuda.graph(g, stream=side):
                 self.clock.add_(1)      # one new LRU stamp per replayed step
-                self.step(q_static, stamp=0, post_attn=post_attn)
+                self.step(q_static, stamp=0, timers=timers, post_attn=post_attn)
         finally:
             self._capturing = False
         torch.cuda.synchronize(self.device)

@@ -82,6 +82,35 @@ def ss_block_select(q: torch.Tensor, meta: torch.Tensor, n_blk: torch.Tensor, ma
                                       _stream(stream)), "ss_block_select")
 
 
+def mean_meta_numel(batch: int, num_kv_heads: int, max_blk: int) -> int:
+    """float32 elements of a (tiled) NEXT-3 mean-metadata array."""
+    assert max_blk % 32 == 0
+    return batch * num_kv_heads * max_blk * HEAD_DIM
+
+
+def block_meta_update_mean(keys: torch.Tensor, meta: torch.Tensor, n: int, key_stride: int,
+                           dst_idx: Optional[torch.Tensor] = None, stream=None) -> None:
+    """NEXT-3 S0: meta[dst_idx[i]] = float32 mean of the 32 keys at keys + i*key_stride."""
+    assert meta.dtype == torch.float32
+    if dst_idx is not None:
+        assert dst_idx.dtype == torch.int64
+    check(_lib.load().block_meta_update_mean(_ptr(keys), key_stride, _ptr(dst_idx), n, _ptr(meta),
+                                             _dt(keys), HEAD_DIM, _stream(stream)),
+          "block_meta_update_mean")
+
+
+def ss_block_select_mean(q: torch.Tensor, meta: torch.Tensor, n_blk: torch.Tensor, max_blk: int,
+                         k: int, d: SSDims, sel: torch.Tensor, ws: torch.Tensor,
+                         scores: Optional[torch.Tensor] = None, stream=None) -> None:
+    """NEXT-3 S1+S2 over mean metadata: top-k of max_g q_g . mu_j."""
+    assert n_blk.dtype == torch.int32 and sel.dtype == torch.int32 and meta.dtype == torch.float32
+    if scores is not None:
+        assert scores.dtype == torch.float64
+    check(_lib.load().ss_block_select_mean(_ptr(q), _ptr(meta), _ptr(n_blk), max_blk, k, d, _dt(q),
+                                           _ptr(sel), _ptr(scores), _ptr(ws), ws.numel(),
+                                           _stream(stream)), "ss_block_select_mean")
+
+
 class CachePool:
     """Device arrays of one (GPU, layer) HBM block-cache pool (S3 state)."""
 

@@ -47,3 +47,15 @@ def logical_to_tiled(logical: np.ndarray) -> np.ndarray:
 
 def storage(dtype_name: str):
     return np.uint16 if dtype_name == synth.DT_BF16 else np.float32
+
+
+def mean_tiled_to_logical(tiled: np.ndarray, B: int, Hkv: int, max_blk: int) -> np.ndarray:
+    """NEXT-3 float32 mean metadata: tiled [..][tiles][d/4][32][4] -> [B][Hkv][max_blk][d]."""
+    t = tiled.reshape(B, Hkv, max_blk // 32, D // 4, 32, 4).transpose(0, 1, 2, 4, 3, 5)
+    return np.ascontiguousarray(t).reshape(B, Hkv, max_blk, D)
+
+
+def mean_logical_to_tiled(logical: np.ndarray) -> np.ndarray:
+    B, Hkv, max_blk, _ = logical.shape
+    t = logical.reshape(B, Hkv, max_blk // 32, 32, D // 4, 4).transpose(0, 1, 2, 4, 3, 5)
+    return np.ascontiguousarray(t).reshape(-1)
