@@ -137,7 +137,9 @@ def setup_engine(args, rank: int, world: int):
     hq = W["num_q_heads"] // world
     cfg = EngineConfig(batch=W["batch"], layers=W["layers"], num_q_heads=hq, num_kv_heads=hkv,
                        max_blk=W["max_blk"], topk=W["topk"], slots_per_layer=W["slots"],
-                       num_requests=W["batch"], dtype=torch.bfloat16, groups=args.groups)
+                       num_requests=W["batch"], dtype=torch.bfloat16, groups=args.groups,
+                       h2d_streams=args.h2d_streams, select_priority=args.select_priority,
+                       cache_per_group=args.cache_per_group)
     eng = DecodeEngine(cfg)
     # physical host pool: a prime number of max_blk runs (aliasing, R15)
     runs = args.host_runs if cfg.max_blk <= 4096 else max(1, (args.host_runs * 4096) // cfg.max_blk)
@@ -187,12 +189,14 @@ class StepTimers:
     """CUDA events around each op of each layer, recorded on the launching
     stream (each request group's own stream)."""
 
-    def __init__(self):
+    def __init__(self, external=False):
         self.ev = {"select": [], "cache": [], "gather": [], "attn": [], "allgather": []}
         self.trace = []          # (name, group, layer, start_event, end_event) in issue order
+        self.external = external  # record nodes inside a captured CUDA graph
 
     def mark(self, name, group=0, layer=0):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s = torch.cuda.Event(enable_timing=True, external=self.external)
+        e = torch.cuda.Event(enable_timing=True, external=self.external)
         self.ev[name].append((s, e))
         self.trace.append((name, group, layer, s, e))
         return s, e
@@ -226,6 +230,64 @@ def run_step(eng, q_step, stamp, timers=None, pgs=None, world=1, gathered=None):
                 gather_outputs(g.out[l], gathered[gi][l], group=pgs[gi])
                 e.record()
     eng.step(q_step, stamp, timers=timers, post_attn=hook)
+
+
+def solo_pass(eng, q_src, layers, hbm_peak, h2d_peak, stamp):
+    """Each hot-path kernel timed ALONE: one request group's select, cache,
+    FlashH2D and attention of `layers` layers, each launch bracketed by a
+    synchronize and CUDA events on the current stream (no co-running kernels).
+    This is each kernel's own roofline fraction; the in-step `kernels` numbers
+    above include the overlap with the other request group."""
+    from paper_2509_24626_b200 import ops
+    c = eng.cfg
+    cur = torch.cuda.current_stream()
+    t = {"select": [], "cache": [], "gather": [], "attn": []}
+    sel_b = attn_b = miss_b = 0
+    for l in range(layers):
+        for g in eng.groups:
+            q = q_src[l, g.b0:g.b1]
+
+            def timed(name, fn):
+                torch.cuda.synchronize()
+                s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+                # a 100 us device spin ahead of the start event: the launch below is
+                # enqueued before the GPU reaches `s`, so host launch latency is not timed
+                torch.cuda._sleep(200000)
+                s.record(cur)
+                fn()
+                e.record(cur)
+                torch.cuda.synchronize()
+                t[name].append(s.elapsed_time(e))
+            timed("select", lambda: ops.ss_block_select(q, g.meta[l], g.n_blk, c.max_blk, c.topk, g.dims,
+                                                        g.sel[l], g.ws_select))
+            timed("cache", lambda: ops.kv_cache_lookup_insert(
+                eng.pools[l], g.sel[l], g.req_ids, l, c.layers, c.max_blk, c.topk, g.dims, stamp,
+                g.slot[l], g.hit[l], g.miss_keys[l], g.miss_slots[l], g.counts[l], g.ws_cache))
+            timed("gather", lambda: ops.flash_h2d_gather(eng.host_ptr, eng.host_blocks, g.miss_keys[l],
+                                                         g.miss_slots[l], g.counts[l], g.E, eng.pool_kv[l],
+                                                         c.block_bytes))
+            timed("attn", lambda: ops.sparse_decode_attn(q, eng.pool_kv[l], g.slot[l], c.topk, g.tail_kv[l],
+                                                         g.tail_len, g.dims, eng.scale, g.out[l], g.ws_attn,
+                                                         counts=g.counts[l]))
+            hits, miss = [int(x) for x in g.counts[l, :2].tolist()]
+            sel_b += g.nb * c.num_kv_heads * int(g.n_blk[0].item()) * 512 + q.numel() * 2
+            attn_b += (hits + miss) * c.block_bytes + c.num_q_heads * g.nb * 128 * 4
+            miss_b += miss * c.block_bytes
+    tot = {k: sum(v) * 1e-3 for k, v in t.items()}
+    n = len(t["select"])
+
+    def ent(bound, byts, sec, peak):
+        gbs = byts / sec / 1e9
+        return {"bound": bound, "achieved": round(gbs, 1 if bound == "hbm" else 2), "peak": round(peak, 2),
+                "unit": "GB/s", "frac": round(gbs / peak, 4), "us_per_launch": round(sec * 1e6 / n, 2),
+                "bytes_per_launch": int(byts / n)}
+    return {"ss_block_select": ent("hbm", sel_b, tot["select"], hbm_peak),
+            "sparse_decode_attn": ent("hbm", attn_b, tot["attn"], hbm_peak),
+            "flash_h2d_gather": ent("host-link", miss_b, tot["gather"], h2d_peak),
+            "kv_cache_lookup_insert": {"bound": "latency", "us_per_launch": round(tot["cache"] * 1e6 / n, 2)},
+            "launches_per_kernel": n,
+            "note": f"one request group ({eng.groups[0].nb} requests) per launch, {layers} layers, each launch "
+                    "alone (synchronize before and after), events on the launching stream"}
 
 
 def measure_h2d_peak(nbytes=1 << 30):
@@ -293,7 +355,7 @@ def bench_ours(args):
     t_timed = args.settle + args.warmup
     t_e2e = t_timed + args.steps
     t_kt = t_e2e + e2e_steps
-    qs = gen_queries(eng, t_kt + n_kt, W["rho"], seed=5000 + rank)
+    qs = gen_queries(eng, t_kt + n_kt + 1, W["rho"], seed=5000 + rank)
     gathered = None
     if world > 1:
         # one communicator per request group (their all-gathers run on different streams)
@@ -403,25 +465,42 @@ def bench_ours(args):
            "hit_rate": round(float(e2e_cnt[0]) / max(1.0, float(e2e_cnt[0] + e2e_cnt[1])), 4),
            "misses_per_step": float(e2e_cnt[1]) / e2e_steps}
 
-    # ---- per-kernel timing pass: eager launches with CUDA events recorded on
-    # each kernel's launching stream (the graph hides the individual kernels) ----
-    timers = StepTimers()
+    # ---- per-kernel timing pass: CUDA events recorded on each kernel's launching
+    # stream.  With --graph (default) the events are captured INSIDE a second
+    # copy of the step graph (event-record nodes), so the launch times are those
+    # of the replayed step, free of host launch latency; eager otherwise ----
     kcnt = torch.zeros(4, dtype=torch.int64, device="cuda")
     barrier()
-    k_s = torch.cuda.Event(True)
-    k_s.record()
-    for t in range(t_kt, t_kt + n_kt):
-        q_static.copy_(qs[t], non_blocking=True)
-        if graph is not None:
-            eng.advance_clock()          # device-clock stamps (the host stamp is ignored)
-        run_step(eng, q_static, stamp=t + 1, timers=timers, pgs=pgs, world=world, gathered=gathered)
-        counts_sum(kcnt)
-    barrier()
-    if args.timeline and rank == 0:
-        with open(args.timeline, "w") as f:
-            json.dump(timers.timeline(k_s, len(timers.trace) // n_kt), f)
-    tot = timers.totals_ms()
-    nlaunch = timers.counts()
+    if graph is not None:
+        timers = StepTimers(external=True)
+        tgraph = eng.capture_graph(q_static, post_attn=allgather_hook(), timers=timers)
+        tot = {k: 0.0 for k in timers.ev}
+        for t in range(t_kt, t_kt + n_kt):
+            q_static.copy_(qs[t], non_blocking=True)
+            tgraph.replay()
+            counts_sum(kcnt)
+            torch.cuda.synchronize()
+            for k, v in timers.totals_ms().items():
+                tot[k] += v
+        nlaunch = {k: v * n_kt for k, v in timers.counts().items()}
+        if args.timeline and rank == 0:
+            with open(args.timeline, "w") as f:
+                json.dump(timers.timeline(timers.trace[0][3], len(timers.trace)), f)
+        del tgraph
+    else:
+        timers = StepTimers()
+        k_s = torch.cuda.Event(True)
+        k_s.record()
+        for t in range(t_kt, t_kt + n_kt):
+            q_static.copy_(qs[t], non_blocking=True)
+            run_step(eng, q_static, stamp=t + 1, timers=timers, pgs=pgs, world=world, gathered=gathered)
+            counts_sum(kcnt)
+        barrier()
+        if args.timeline and rank == 0:
+            with open(args.timeline, "w") as f:
+                json.dump(timers.timeline(k_s, len(timers.trace) // n_kt), f)
+        tot = timers.totals_ms()
+        nlaunch = timers.counts()
     k_hits, k_miss = [int(x) for x in kcnt.cpu().tolist()[:2]]
 
     # ---- roofline of each kernel (algorithmic bytes / measured time) ----
@@ -449,9 +528,10 @@ def bench_ours(args):
                               "bytes_per_launch": int(miss_bytes_kt / max(1, nlaunch["gather"]))},
         "kv_cache_lookup_insert": {"bound": "latency",
                                    "us_per_launch": round(tot["cache"] * 1e3 / max(1, nlaunch["cache"]), 2)},
-        "timing_pass": {"steps": n_kt, "eager": True, "request_groups": len(eng.groups),
-                        "note": "events on each kernel's launching stream; kernels of different request "
-                                "groups overlap, so a launch's time includes co-running work"},
+        "timing_pass": {"steps": n_kt, "eager": graph is None, "request_groups": len(eng.groups),
+                        "note": ("events captured in the replayed step graph" if graph is not None else
+                                 "eager launches") + " on each kernel's launching stream; kernels of "
+                                "different request groups overlap, so a launch's time includes co-running work"},
     }
     if world > 1:
         kernels["nccl_all_gather"] = {"us_per_launch": round(tot["allgather"] * 1e3 / max(1, nlaunch["allgather"]), 2)}
@@ -471,6 +551,12 @@ def bench_ours(args):
     roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"], "peak": dk["peak"],
                 "unit": "GB/s", "frac": dk["frac"], "traffic": traffic,
                 "peak_source": peak_src if dk["bound"] == "hbm" else "bulk pinned cudaMemcpy H2D, measured in this run"}
+
+    # ---- each kernel alone (its own roofline fraction, no co-running group) ----
+    if graph is not None:
+        eng.advance_clock()
+    q_static.copy_(qs[t_kt + n_kt])
+    kernels_solo = solo_pass(eng, q_static, min(4, c.layers), hbm_peak, h2d_peak, stamp=t_kt + n_kt + 1)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -492,7 +578,8 @@ def bench_ours(args):
                        "topk_blocks": c.topk, "hbm_cache_slots_per_layer": c.slots_per_layer,
                        "host_pool_blocks": eng.host_blocks, "host_kv": "pinned DRAM, zero-copy (UVA)",
                        "parallelism": f"kv-heads/{world} per GPU" if world > 1 else "1 GPU",
-                       "request_groups": len(eng.groups), "cuda_graph": graph is not None,
+                       "request_groups": len(eng.groups), "h2d_streams": args.h2d_streams, "select_priority": args.select_priority, "cache_per_group": args.cache_per_group,
+                       "cuda_graph": graph is not None,
                        "cache_settle_steps": args.settle,
                        "l2": f"no flush needed: inputs larger than L2 ({meta_gib:.0f} GiB metadata streamed per step)",
                        "scope": "attention path only (no QKV/O projections, no FFN)"},
@@ -502,7 +589,7 @@ def bench_ours(args):
                           "link_peak_gbs": round(h2d_peak, 2), "link_theoretical_gbs": 63.0,
                           "frac": kernels["flash_h2d_gather"]["frac"],
                           "h2d_gbs_over_step": round(n_miss * c.block_bytes / (ms * 1e-3) / 1e9, 2)},
-            "roofline": roofline, "kernels": kernels,
+            "roofline": roofline, "kernels": kernels, "kernels_solo": kernels_solo,
             "cold_step_ms": round(cold_ms, 2) if cold_ms else None,
             "e2e": e2e, "gpu_launches": int(args.steps * c.layers * 6 * len(eng.groups)),
             "cpu_baseline": cpu, "clocks": clocks, "setup_s": round(setup_s, 1),
@@ -577,8 +664,14 @@ def main():
     ap.add_argument("--timeline", default=None, help="write one step's op timeline (json, timing pass)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch kernels eagerly instead of replaying a captured CUDA graph per step")
-    ap.add_argument("--groups", type=int, default=2,
+    ap.add_argument("--groups", type=int, default=3,
                     help="request groups pipelined on separate streams (PCIe of one overlaps HBM work of another)")
+    ap.add_argument("--h2d-streams", type=int, default=1,
+                    help="FlashH2D streams shared by the request groups (1: the link serves one group at a time)")
+    ap.add_argument("--select-priority", action="store_true",
+                    help="select on high-priority per-group streams (it feeds the PCIe link)")
+    ap.add_argument("--cache-per-group", action="store_true",
+                    help="per-group cache streams ordered per layer (no cross-layer cache-stream order)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"

@@ -166,7 +166,9 @@ ss_status ss_block_select_mean(const void* q, const float* meta, const int32_t* 
  *              evictable slots.  On status != 0 the pool is left byte-identical
  *              and the other outputs are unspecified.
  * Preconditions: req_ids unique; stamp >= every stamp previously used on the
- * pool.  ws: ss_workspace_size(SS_WS_CACHE, ...) bytes, no initialisation. */
+ * pool.  ws: ss_workspace_size(SS_WS_CACHE, ...) bytes, ZERO-FILLED ONCE
+ * before first use; every call (including a failing one) leaves it zeroed.
+ * One workspace serves one call at a time (calls sharing it must be ordered). */
 typedef struct {
     int32_t* fwd;
     int64_t fwd_len;

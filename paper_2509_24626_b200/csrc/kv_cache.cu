@@ -41,9 +41,11 @@ constexpr int kSlotChunk = 1024;  // order positions / slots per chunk CTA (4 pe
 constexpr int kSlotPer = kSlotChunk / kCacheThreads;
 
 struct CacheWs {
-    // ---- zeroed at the start of every call (one memset) ----
+    // ---- zero on entry to every call: zero-filled once by the caller, and
+    // every call leaves them zero again (K2 / K3 clean up; no memset node) ----
     int32_t* ctrl;        // [16]: 0 M, 1 hits, 2 status, 3 total_elig, 4 evictions,
-                          //       5 kept, 6 invalid, 7 K1 ticket; [8..9] = stamp (int64)
+                          //       5 kept, 6 invalid, 7 K1 ticket; [8..9] = stamp (int64),
+                          //       10 K3 ticket
     int64_t* ctrl64;      // = ctrl + 8
     uint8_t* touched;     // [S]  slot hit by this call
     uint8_t* victim;      // [S]  slot evicted/assigned by this call
@@ -175,6 +177,7 @@ __global__ void __launch_bounds__(kCacheThreads) cache_lookup_count_kernel(Cache
         // ---- entry CTA: probe fwd, mark hits, rank misses ----
         const int64_t e = (int64_t)blockIdx.x * kCacheThreads + threadIdx.x;
         int is_miss = 0, is_hit = 0;
+        int ch_elig = -1, ch_teq = -1;  // chunks whose counters this hit moves
         if (e < a.E) {
             int32_t j = a.sel[e];
             int32_t so = -1;
@@ -193,8 +196,8 @@ __global__ void __launch_bounds__(kCacheThreads) cache_lookup_count_kernel(Cache
                         const int64_t st = a.pool.slot_stamp[f];
                         // a hit slot leaves the eligible set and joins stamp == t
                         if (st < t) {
-                            atomicSub(&a.ws.elig_cnt[a.pool.order_pos[f] / kSlotChunk], 1);
-                            atomicAdd(&a.ws.teq_cnt[f / kSlotChunk], 1);
+                            ch_elig = a.pool.order_pos[f] / kSlotChunk;
+                            ch_teq = f / kSlotChunk;
                         }
                     } else {
                         is_miss = 1;
@@ -203,6 +206,14 @@ __global__ void __launch_bounds__(kCacheThreads) cache_lookup_count_kernel(Cache
             }
             a.slot_out[e] = so;
             a.hit_out[e] = ho;
+        }
+        // warp-aggregated counter updates: recent (hit) slots crowd into the last
+        // few order chunks, so per-hit atomics would serialise on a few words
+        {
+            const unsigned ge = __match_any_sync(0xffffffffu, ch_elig);
+            if (ch_elig >= 0 && lane_id() == __ffs(ge) - 1) atomicSub(&a.ws.elig_cnt[ch_elig], __popc(ge));
+            const unsigned gt = __match_any_sync(0xffffffffu, ch_teq);
+            if (ch_teq >= 0 && lane_id() == __ffs(gt) - 1) atomicAdd(&a.ws.teq_cnt[ch_teq], __popc(gt));
         }
         int tot;
         int rank = block_excl_scan<kCacheThreads>(is_miss, sw, tot);
@@ -240,6 +251,7 @@ __global__ void __launch_bounds__(kCacheThreads) cache_lookup_count_kernel(Cache
     __syncthreads();
     if (sw[48] != (int)gridDim.x - 1) return;
     __threadfence();
+    if (threadIdx.x == 0) a.ws.ctrl[7] = 0;  // K1 ticket back to zero
     cache_plan(a, sw);
 }
 
@@ -294,67 +306,86 @@ __global__ void __launch_bounds__(kCacheThreads) cache_victim_kernel(CacheArgs a
 __global__ void __launch_bounds__(kCacheThreads) cache_assign_place_kernel(CacheArgs a) {
     __shared__ int sw[64];
     __shared__ int s_base;
-    if (a.ws.ctrl[2] != 0) return;
+    const bool ok = a.ws.ctrl[2] == 0;
     const int64_t t = stamp_post_plan(a);
+    const int S = a.pool.num_slots;
     if ((int)blockIdx.x < a.nA) {
         const int64_t e = (int64_t)blockIdx.x * kCacheThreads + threadIdx.x;
-        if (e >= a.E) return;
-        if (a.hit_out[e]) {
-            a.pool.slot_stamp[a.slot_out[e]] = t;
-            return;
+        if (ok && e < a.E) {
+            if (a.hit_out[e]) {
+                a.pool.slot_stamp[a.slot_out[e]] = t;
+            } else {
+                const int ml = a.ws.miss_local[e];
+                if (ml >= 0) {
+                    const int i = a.ws.blk_off[blockIdx.x] + ml;
+                    const int32_t s = a.ws.vict[i];
+                    const int64_t key = cache_key(a, e, a.sel[e]);
+                    a.slot_out[e] = s;
+                    a.miss_keys[i] = key;
+                    a.miss_slots[i] = s;
+                    a.pool.slot_key[s] = key;
+                    a.pool.fwd[key] = s;
+                    a.pool.slot_stamp[s] = t;
+                }
+            }
         }
-        int ml = a.ws.miss_local[e];
-        if (ml < 0) return;
-        int i = a.ws.blk_off[blockIdx.x] + ml;
-        int32_t s = a.ws.vict[i];
-        int64_t key = cache_key(a, e, a.sel[e]);
-        a.slot_out[e] = s;
-        a.miss_keys[i] = key;
-        a.miss_slots[i] = s;
-        a.pool.slot_key[s] = key;
-        a.pool.fwd[key] = s;
-        a.pool.slot_stamp[s] = t;
-        return;
-    }
-    // chunk CTA c: slots [c*1024, (c+1)*1024) in slot order
-    const int S = a.pool.num_slots;
-    const int c = blockIdx.x - a.nA;
-    const int kept = a.ws.ctrl[5];
-    if (c == 0 && threadIdx.x == 0) a.counts[2] = a.ws.ctrl[4];
-    if (threadIdx.x < 32) {
-        int acc = 0;
-        for (int cc = threadIdx.x; cc < c; cc += 32) acc += a.ws.teq_cnt[cc];
-        acc = warp_sum(acc);
-        if (threadIdx.x == 0) s_base = kept + acc;
-    }
-    const int s0 = c * kSlotChunk + threadIdx.x * kSlotPer;
-    bool f[kSlotPer];
-    int n = 0;
+    } else {
+        // chunk CTA c: slots [c*1024, (c+1)*1024) in slot order
+        const int c = blockIdx.x - a.nA;
+        const int kept = a.ws.ctrl[5];
+        if (ok && c == 0 && threadIdx.x == 0) a.counts[2] = a.ws.ctrl[4];
+        if (threadIdx.x < 32) {
+            int acc = 0;
+            for (int cc = threadIdx.x; cc < c; cc += 32) acc += a.ws.teq_cnt[cc];
+            acc = warp_sum(acc);
+            if (threadIdx.x == 0) s_base = kept + acc;
+        }
+        const int s0 = c * kSlotChunk + threadIdx.x * kSlotPer;
+        bool f[kSlotPer];
+        int n = 0;
 #pragma unroll
-    for (int i = 0; i < kSlotPer; ++i) {
-        const int s = s0 + i;
-        // stamp == t after this call: hit, victim, or already stamped t (a
-        // concurrent K3 entry CTA may be writing t into hit / victim slots;
-        // their flags already decide those)
-        f[i] = s < S && (a.ws.touched[s] || a.ws.victim[s] || a.pool.slot_stamp[s] == t);
-        n += f[i];
-        // copy the kept prefix of the new order (K2) into order / order_pos
-        if (s < kept) {
-            const int32_t v = a.ws.new_order[s];
-            a.pool.order[s] = v;
-            a.pool.order_pos[v] = s;
+        for (int i = 0; i < kSlotPer; ++i) {
+            const int s = s0 + i;
+            // stamp == t after this call: hit, victim, or already stamped t (a
+            // concurrent K3 entry CTA may be writing t into hit / victim slots;
+            // their flags already decide those)
+            f[i] = ok && s < S && (a.ws.touched[s] || a.ws.victim[s] || a.pool.slot_stamp[s] == t);
+            n += f[i];
+            // this chunk's per-call flags go back to zero (K1 set touched even
+            // when the call fails)
+            if (s < S) {
+                a.ws.touched[s] = 0;
+                a.ws.victim[s] = 0;
+            }
+            // copy the kept prefix of the new order (K2) into order / order_pos
+            if (ok && s < kept) {
+                const int32_t v = a.ws.new_order[s];
+                a.pool.order[s] = v;
+                a.pool.order_pos[v] = s;
+            }
         }
-    }
-    int tot;
-    int ex = block_excl_scan<kCacheThreads>(n, sw, tot);  // syncs: s_base visible
-    int pos = s_base + ex;
+        if (threadIdx.x == 0) a.ws.elig_cnt[c] = 0;
+        int tot;
+        int ex = block_excl_scan<kCacheThreads>(n, sw, tot);  // syncs: s_base visible
+        int pos = s_base + ex;
 #pragma unroll
-    for (int i = 0; i < kSlotPer; ++i)
-        if (f[i]) {
-            a.pool.order[pos] = s0 + i;
-            a.pool.order_pos[s0 + i] = pos;
-            ++pos;
-        }
+        for (int i = 0; i < kSlotPer; ++i)
+            if (f[i]) {
+                a.pool.order[pos] = s0 + i;
+                a.pool.order_pos[s0 + i] = pos;
+                ++pos;
+            }
+    }
+    // the last K3 CTA (every CTA has read ctrl / teq_cnt by now) zeroes the
+    // call-wide words, leaving the workspace ready for the next call
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) sw[48] = atomicAdd(&a.ws.ctrl[10], 1);
+    __syncthreads();
+    if (sw[48] != (int)gridDim.x - 1) return;
+    __threadfence();
+    for (int c = threadIdx.x; c < a.nS; c += kCacheThreads) a.ws.teq_cnt[c] = 0;
+    if (threadIdx.x < 16) a.ws.ctrl[threadIdx.x] = 0;
 }
 
 ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int32_t* req_ids,
@@ -381,7 +412,6 @@ ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int3
     carve(&a.ws, ws, a.E, S);
     a.nA = (int)((a.E + kCacheThreads - 1) / kCacheThreads);
     a.nS = (S + kSlotChunk - 1) / kSlotChunk;
-    if (cudaMemsetAsync(a.ws.ctrl, 0, a.ws.zero_bytes, stream) != cudaSuccess) return SS_ERR_CUDA;
     cache_lookup_count_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
     cache_victim_kernel<<<a.nS, kCacheThreads, 0, stream>>>(a);
     cache_assign_place_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);

@@ -960,7 +960,16 @@ static ss_status launch_attn_mma_t(const AttnArgs& a, const void* pool, const vo
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem) !=
         cudaSuccess)
         return SS_ERR_CUDA;
-    kern<<<kNumSMs, kMmaNW * 32, kMmaSmem, stream>>>(a, tm_pool, tm_tail);
+    // persistent 6-warp CTAs, one per SM (default).  SS_ATTN_CTA_WARPS=1
+    // launches one-warp CTAs instead (each warp's 33 KiB of stages its own CTA,
+    // dispatched into whatever SM space co-running kernels leave); warps never
+    // synchronise, so the kernel is the same (warp w = warp_id * gridDim + CTA).
+    // Measured: 0.89 vs 0.85 of HBM peak alone at C2, no in-step difference.
+    static const int cta_warps = getenv("SS_ATTN_CTA_WARPS") ? atoi(getenv("SS_ATTN_CTA_WARPS")) : kMmaNW;
+    if (cta_warps == kMmaNW)
+        kern<<<kNumSMs, kMmaNW * 32, kMmaSmem, stream>>>(a, tm_pool, tm_tail);
+    else
+        kern<<<a.W, 32, sizeof(MmaWarpSmem) + 1024, stream>>>(a, tm_pool, tm_tail);
     SS_LAUNCH_CHECK();
     return SS_OK;
 }

@@ -41,6 +41,9 @@ class EngineConfig:
     num_requests: int          # size of the request-id space (fwd table extent)
     dtype: torch.dtype = torch.bfloat16
     groups: int = 1            # request groups pipelined on separate streams
+    h2d_streams: int = 1       # FlashH2D streams shared round-robin by the groups
+    select_priority: bool = False  # run select on a high-priority per-group stream
+    cache_per_group: bool = False  # per-group cache streams, ordered per layer only
 
     @property
     def group(self) -> int:
@@ -104,6 +107,10 @@ class RequestGroup:
         self.ev_sel = [torch.cuda.Event() for _ in range(c.layers)]
         # FlashH2D runs on the engine's shared high-priority stream (set below)
         self.h2d_stream = None
+        # select on a high-priority stream (EngineConfig.select_priority): the
+        # select -> cache -> FlashH2D chain feeds the PCIe link, the bottleneck
+        self.sel_stream = None
+        self.cache_stream = None      # own cache stream (EngineConfig.cache_per_group)
 
 
 class DecodeEngine:
@@ -138,6 +145,7 @@ class DecodeEngine:
         self.groups = [RequestGroup(self, bounds[i], bounds[i + 1],
                                     cur if ng == 1 else torch.cuda.Stream(dev))
                        for i in range(ng)]
+        self.h2d_streams = []
         if ng > 1:
             # One high-priority stream carries every group's FlashH2D in issue
             # order (layer l: group 0, 1, ...; then layer l+1): the PCIe link
@@ -145,10 +153,23 @@ class DecodeEngine:
             # while group A's misses stream in, group B runs its HBM-bound
             # attention / next-layer select -- and the gather CTAs are dispatched
             # ahead of queued HBM-kernel CTAs.
-            h2d = torch.cuda.Stream(dev, priority=-1)
-            for g in self.groups:
-                g.h2d_stream = h2d
+            # (h2d_streams > 1: group i uses stream i % h2d_streams, so one group's
+            # gather may start while another's is still streaming -- no link gap
+            # when a group's cache call finishes late)
+            h2d = [torch.cuda.Stream(dev, priority=-1) for _ in range(max(1, c.h2d_streams))]
+            for i, g in enumerate(self.groups):
+                g.h2d_stream = h2d[i % len(h2d)]
+            self.h2d_streams = h2d
         self.cache_stream = torch.cuda.Stream(dev, priority=-1) if ng > 1 else None
+        if ng > 1 and c.cache_per_group:
+            # a layer's pool orders its calls group 0, 1, ...; calls of different
+            # layers (different pools) need no order, so one shared cache stream
+            # would add false cross-layer dependencies
+            for g in self.groups:
+                g.cache_stream = torch.cuda.Stream(dev, priority=-1)
+        if ng > 1 and c.select_priority:
+            for g in self.groups:
+                g.sel_stream = torch.cuda.Stream(dev, priority=-1)
         self._capturing = False
         g0 = self.groups[0]
         # single-group aliases (tests, smoke)
@@ -205,9 +226,16 @@ class DecodeEngine:
                 s.record()
                 fn()
                 e.record()
-        timed("select", lambda: ops.ss_block_select(q, g.meta[l], g.n_blk, c.max_blk, c.topk, g.dims,
-                                                    g.sel[l], g.ws_select, scores=scores))
         multi = len(self.groups) > 1
+        if multi and g.sel_stream is not None:
+            g.sel_stream.wait_stream(g.stream)       # after this group's previous attention
+            with torch.cuda.stream(g.sel_stream):
+                timed("select", lambda: ops.ss_block_select(q, g.meta[l], g.n_blk, c.max_blk, c.topk,
+                                                            g.dims, g.sel[l], g.ws_select, scores=scores))
+                g.ev_sel[l].record(g.sel_stream)
+        else:
+            timed("select", lambda: ops.ss_block_select(q, g.meta[l], g.n_blk, c.max_blk, c.topk, g.dims,
+                                                        g.sel[l], g.ws_select, scores=scores))
 
         def _cache():
             timed("cache", lambda: ops.kv_cache_lookup_insert(
@@ -228,9 +256,12 @@ class DecodeEngine:
             # small cache kernels are dispatched ahead of queued select CTAs.  The
             # first group of step t also waits for every group's layer-l attention
             # of step t-1 (no eviction under a reader).
-            g.ev_sel[l].record(g.stream)
-            cs = self.cache_stream
+            if g.sel_stream is None:
+                g.ev_sel[l].record(g.stream)
+            cs = g.cache_stream if g.cache_stream is not None else self.cache_stream
             cs.wait_event(g.ev_sel[l])
+            if g.cache_stream is not None and gi > 0:
+                cs.wait_event(self.groups[gi - 1].ev_cache[l])   # same layer pool: in group order
             if gi == 0 and not self._capturing:
                 # (inside a captured graph, successive replays are serialised,
                 # which already orders step t+1 after all of step t)
@@ -275,7 +306,12 @@ class DecodeEngine:
         for g in self.groups:
             g.stream.wait_stream(cur)
         self.cache_stream.wait_stream(cur)
-        self.groups[0].h2d_stream.wait_stream(cur)
+        for g in self.groups:
+            if g.cache_stream is not None:
+                g.cache_stream.wait_stream(cur)
+        # (per-group select streams wait on their group stream, which waits on cur)
+        for hs in self.h2d_streams:
+            hs.wait_stream(cur)
         # issue layer by layer, group by group: group A's FlashH2D (PCIe) overlaps
         # group B's select / attention (HBM) on the other stream
         for l in range(c.layers):
@@ -286,6 +322,8 @@ class DecodeEngine:
                         post_attn(gi, g, l)
         for g in self.groups:
             cur.wait_stream(g.stream)
+        for hs in self.h2d_streams:
+            cur.wait_stream(hs)
 
     def outputs(self) -> List[torch.Tensor]:
         return [g.out for g in self.groups]
