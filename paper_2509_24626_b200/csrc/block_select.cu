@@ -71,6 +71,13 @@ __device__ __forceinline__ double bf16_lo_scaled(uint32_t w) {  // bits 15..0
 __device__ __forceinline__ double bf16_hi_scaled(uint32_t w) {  // bits 31..16
     return __hiloint2double(((int32_t)w >> 3) & (int32_t)0x8FFFE000, 0);
 }
+// the high words of bf16_lo_scaled / bf16_hi_scaled (the low word is 0)
+__device__ __forceinline__ int32_t bf16_lo_hiword(uint32_t w) {
+    return ((int32_t)(w << 16) >> 3) & (int32_t)0x8FFFFFFF;
+}
+__device__ __forceinline__ int32_t bf16_hi_hiword(uint32_t w) {
+    return ((int32_t)w >> 3) & (int32_t)0x8FFFE000;
+}
 __device__ __forceinline__ double f32_scaled(uint32_t x) {
     return __hiloint2double(((int32_t)x >> 3) & (int32_t)0x8FFFFFFF, (int32_t)(x << 29));
 }
@@ -161,8 +168,8 @@ __device__ void cta_topk(const uint64_t* keys, int n, int k_sel, int* hist, int*
 }
 
 // ---------------------------------------------------------------------------
-template <bool BF16, int G, bool ICV, bool MEAN>
-__global__ void __launch_bounds__(kSelThreads, 2)
+template <bool BF16, int G, bool ICV, bool MEAN, int TT>
+__global__ void __launch_bounds__(kSelThreads, (G > 1 && !MEAN && TT == 1) ? 3 : 2)
 block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                     const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
                     int nchunks, int CH, int npairs, int l2pf, int32_t* __restrict__ sel, double* __restrict__ scores,
@@ -174,6 +181,14 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     constexpr int TILE_ELEMS = 64 * kHeadDim;  // 32 blocks * 2 * d
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* qpn = (double2*)smem_raw;                                  // [128*G]
+    // GQA bf16 (SELQ): ONE DFMA per head and channel.  The sign of q_{g,c} is
+    // the same for every lane, and the min / max operands are integer-built
+    // float64s whose low words are 0, so the operand of head g is the high word
+    // hN + f_g * (hM - hN) (one IMAD, f_g = [q_{g,c} >= 0]) and
+    // acc + q * (q >= 0 ? M : m) == acc + max(q M, q m), rounded once.
+    constexpr bool SELQ = BF16 && ICV && G > 1 && !MEAN;
+    double* qs = (double*)smem_raw;                                     // [128*G] (SELQ)
+    int32_t* qf = (int32_t*)(smem_raw + kHeadDim * G * 8);              // [128*G] (SELQ)
     uint64_t* keys = (uint64_t*)(smem_raw + kHeadDim * G * 16);         // [nkeys]
     const int nkeys_cap = max(CH, min(nchunks * k, kSelMaxMerge));
     int32_t* jpos = (int32_t*)(keys + nkeys_cap);                       // [nkeys]
@@ -191,6 +206,43 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     const int nb = n_blk_arr[b];
     const int nch_b = max(1, (nb + CH - 1) / CH);
     if (ci >= nch_b) continue;
+
+    const int j0 = ci * CH;
+    const int nb_chunk = min(CH, nb - j0);  // >= 0 (0 only if nb == 0)
+    const int ntiles = (nb_chunk + 31) / 32;
+    constexpr size_t TILE_BYTES = MEAN ? (size_t)32 * kHeadDim * 4 : (size_t)TILE_ELEMS * ES;
+    const char* meta_pair = (const char*)meta + ((size_t)pair * (max_blk / 32)) * TILE_BYTES;
+
+    // G > 1 min/max: a warp pass scores TT tiles, tl and (TT = 2) tl + 8 (lane r:
+    // block r of each); pass p has tl = warp + 8*TT*p.  The 16-byte chunk loads run GD steps
+    // ahead in a register ring that carries across passes (the next pass's
+    // first chunks load during this pass's last steps), and the first GD steps
+    // are issued before the q setup below (they do not depend on q).
+    constexpr int GD = 3, GR = GD + 1;
+    static_assert(NCH % GR == 0, "ring slot of step s must be s % GR in every pass");
+    uint4 rnA[GR], rxA[GR], rnB[GR], rxB[GR];
+    const int npass = (G > 1 && !MEAN) ? (ntiles - warp + TT * kSelWarps - 1) / (TT * kSelWarps) : 0;
+    auto pass_ptr = [&](int p, const char*& pa, const char*& pb) {
+        const int tl = warp + p * TT * kSelWarps;
+        pa = meta_pair + (size_t)(j0 / 32 + tl) * TILE_BYTES + lane * 16;
+        pb = (TT == 2 && tl + kSelWarps < ntiles) ? pa + (size_t)kSelWarps * TILE_BYTES : pa;
+    };
+    auto ring_load = [&](const char* pa, const char* pb, int step, int slot) {
+        rnA[slot] = ldg_stream(pa + (size_t)((step * 2 + 0) * 32) * 16);
+        rxA[slot] = ldg_stream(pa + (size_t)((step * 2 + 1) * 32) * 16);
+        if constexpr (TT == 2) {
+            rnB[slot] = ldg_stream(pb + (size_t)((step * 2 + 0) * 32) * 16);
+            rxB[slot] = ldg_stream(pb + (size_t)((step * 2 + 1) * 32) * 16);
+        }
+    };
+    if constexpr (G > 1 && !MEAN) {
+        if (npass > 0) {
+            const char *pa, *pb;
+            pass_ptr(0, pa, pb);
+#pragma unroll
+            for (int st = 0; st < GD; ++st) ring_load(pa, pb, st, st);
+        }
+    }
 
     // G == 1 (MHA): q as float64 plus per-channel select masks (q >= 0 -> max
     // row, else min row), so each channel costs one LOP3-select, one exact
@@ -235,15 +287,15 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
         else
             qd = (double)((const float*)q)[qi];
         if (ICV) qd *= kQScale;
-        qpn[i] = make_double2(qd > 0.0 ? qd : 0.0, qd < 0.0 ? qd : 0.0);
+        if constexpr (SELQ) {
+            qs[i] = qd;                  // q * 2^896, signed
+            qf[i] = qd >= 0.0 ? 1 : 0;   // 1: the max row M, 0: the min row m
+        } else {
+            qpn[i] = make_double2(qd > 0.0 ? qd : 0.0, qd < 0.0 ? qd : 0.0);
+        }
     }
     __syncthreads();
 
-    const int j0 = ci * CH;
-    const int nb_chunk = min(CH, nb - j0);  // >= 0 (0 only if nb == 0)
-    const int ntiles = (nb_chunk + 31) / 32;
-    constexpr size_t TILE_BYTES = MEAN ? (size_t)32 * kHeadDim * 4 : (size_t)TILE_ELEMS * ES;
-    const char* meta_pair = (const char*)meta + ((size_t)pair * (max_blk / 32)) * TILE_BYTES;
 
     // NEXT-3: S(j) = max_g sum_c q_{g,c} mu_{j,c}.  Tile [32 chunks][32 blocks][4 ch]
     // float32: lane r scores block r; chunk s (channels 4s..4s+3) of the warp's 32
@@ -326,36 +378,30 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     }
 
     if constexpr (G > 1 && !MEAN)
-    for (int tl = warp; tl < ntiles; tl += 2 * kSelWarps) {
-        // two tiles per warp pass (lane r scores block r of tile tl and of tile
-        // tl + 8): each shared-memory (q+, q-) load serves two blocks and two
-        // independent DFMA chains / load streams are in flight per lane
-        const bool two = tl + kSelWarps < ntiles;
-        const char* tbA = meta_pair + (size_t)(j0 / 32 + tl) * TILE_ELEMS * ES + lane * 16;
-        const char* tbB = two ? tbA + (size_t)kSelWarps * TILE_ELEMS * ES : tbA;
+    for (int p = 0; p < npass; ++p) {
+        // two tiles per warp pass: each shared-memory (q+, q-) load serves two
+        // blocks, and two independent DFMA chains / load streams per lane
+        const int tl = warp + p * TT * kSelWarps;
+        const bool two = TT == 2 && tl + kSelWarps < ntiles;
+        const char *tbA, *tbB, *nxA, *nxB;
+        pass_ptr(p, tbA, tbB);
+        const bool has_next = p + 1 < npass;
+        if (has_next) pass_ptr(p + 1, nxA, nxB);
         double accA[G], accB[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) accA[g] = accB[g] = 0.0;
-        // fully unrolled over the NCH chunks, loads kept D chunks ahead; the
-        // min / max elements are converted once (exact f32 -> f64) and shared
-        // by the G heads: acc_g += q+_g * M + q-_g * m (one term is an exact 0)
-        constexpr int D = 3, R = D + 1;
-        uint4 mnA[R], mxA[R], mnB[R], mxB[R];
-#pragma unroll
-        for (int s = 0; s < D; ++s) {
-            mnA[s] = ldg_stream(tbA + (size_t)((s * 2 + 0) * 32) * 16);
-            mxA[s] = ldg_stream(tbA + (size_t)((s * 2 + 1) * 32) * 16);
-            mnB[s] = ldg_stream(tbB + (size_t)((s * 2 + 0) * 32) * 16);
-            mxB[s] = ldg_stream(tbB + (size_t)((s * 2 + 1) * 32) * 16);
-        }
+        // fully unrolled over the NCH chunks; the min / max elements are built
+        // once (exact) and shared by the G heads: acc_g += q+_g * M + q-_g * m
+        // (one term is an exact 0)
+        constexpr int R = GR;
+        uint4 (&mnA)[GR] = rnA; uint4 (&mxA)[GR] = rxA;
+        uint4 (&mnB)[GR] = rnB; uint4 (&mxB)[GR] = rxB;
 #pragma unroll
         for (int s = 0; s < NCH; ++s) {
-            if (s + D < NCH) {
-                mnA[(s + D) % R] = ldg_stream(tbA + (size_t)(((s + D) * 2 + 0) * 32) * 16);
-                mxA[(s + D) % R] = ldg_stream(tbA + (size_t)(((s + D) * 2 + 1) * 32) * 16);
-                mnB[(s + D) % R] = ldg_stream(tbB + (size_t)(((s + D) * 2 + 0) * 32) * 16);
-                mxB[(s + D) % R] = ldg_stream(tbB + (size_t)(((s + D) * 2 + 1) * 32) * 16);
-            }
+            if (s + GD < NCH)
+                ring_load(tbA, tbB, s + GD, (s + GD) % GR);
+            else if (has_next)
+                ring_load(nxA, nxB, s + GD - NCH, (s + GD) % GR);
             const uint32_t wnA[4] = {mnA[s % R].x, mnA[s % R].y, mnA[s % R].z, mnA[s % R].w};
             const uint32_t wxA[4] = {mxA[s % R].x, mxA[s % R].y, mxA[s % R].z, mxA[s % R].w};
             const uint32_t wnB[4] = {mnB[s % R].x, mnB[s % R].y, mnB[s % R].z, mnB[s % R].w};
@@ -387,13 +433,53 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                     dmaxB = (double)__uint_as_float(wxB[e]);
                 }
                 const int c = s * CPC + e;
+                if constexpr (SELQ) {
+                    const int w = e >> 1;
+                    const int32_t hNA = (e & 1) ? bf16_hi_hiword(wnA[w]) : bf16_lo_hiword(wnA[w]);
+                    const int32_t hMA = (e & 1) ? bf16_hi_hiword(wxA[w]) : bf16_lo_hiword(wxA[w]);
+                    const int32_t dA = hMA - hNA;
+                    int32_t hNB = 0, dB = 0;
+                    if constexpr (TT == 2) {
+                        hNB = (e & 1) ? bf16_hi_hiword(wnB[w]) : bf16_lo_hiword(wnB[w]);
+                        dB = ((e & 1) ? bf16_hi_hiword(wxB[w]) : bf16_lo_hiword(wxB[w])) - hNB;
+                    }
+                    double qv[G];
+                    int32_t fv[G];
+#pragma unroll
+                    for (int g = 0; g < G; g += 2) {
+                        const double2 t = *reinterpret_cast<const double2*>(qs + c * G + g);
+                        qv[g] = t.x;
+                        qv[g + 1] = t.y;
+                    }
+#pragma unroll
+                    for (int g = 0; g < G; g += (G >= 4 ? 4 : 2)) {
+                        if constexpr (G >= 4) {
+                            const int4 t = *reinterpret_cast<const int4*>(qf + c * G + g);
+                            fv[g] = t.x; fv[g + 1] = t.y; fv[g + 2] = t.z; fv[g + 3] = t.w;
+                        } else {
+                            const int2 t = *reinterpret_cast<const int2*>(qf + c * G + g);
+                            fv[g] = t.x; fv[g + 1] = t.y;
+                        }
+                    }
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        accA[g] = __fma_rn(qv[g], __hiloint2double(hNA + fv[g] * dA, 0), accA[g]);
+                        if constexpr (TT == 2)
+                            accB[g] = __fma_rn(qv[g], __hiloint2double(hNB + fv[g] * dB, 0), accB[g]);
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const double2 qq = qpn[c * G + g];
-                    accA[g] = __fma_rn(qq.x, dmaxA, accA[g]);
-                    accA[g] = __fma_rn(qq.y, dminA, accA[g]);
-                    accB[g] = __fma_rn(qq.x, dmaxB, accB[g]);
-                    accB[g] = __fma_rn(qq.y, dminB, accB[g]);
+                    {
+                        accA[g] = __fma_rn(qq.x, dmaxA, accA[g]);
+                        accA[g] = __fma_rn(qq.y, dminA, accA[g]);
+                        if constexpr (TT == 2) {
+                            accB[g] = __fma_rn(qq.x, dmaxB, accB[g]);
+                            accB[g] = __fma_rn(qq.y, dminB, accB[g]);
+                        }
+                    }
                 }
             }
         }
@@ -457,44 +543,57 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     }  // work items
 }
 
-// Blocks scored per CTA: 1024 for MHA (G = 1), 2048 for GQA (G > 1: 4-8x the
-// fp64 work per block, so longer CTAs amortise the q setup and the top-k);
-// measured best at C2 / C3 (tools/kbench.py).  SS_SEL_CHUNK (multiple of 32,
-// <= 2048) overrides both.  Workspace sizing and launches use the same value.
-static int sel_chunk(int G) {
+// Blocks scored per CTA (the chunk): 1024 for MHA (G = 1), 2048 for GQA
+// (G > 1: 4-8x the fp64 work per block, so longer CTAs amortise the q setup and
+// the top-k).  Measured (tools/kbench.py, C2 / C3 full batch and one request
+// group): a chooser that sized chunks to fill whole waves of resident CTAs lost
+// to these fixed sizes everywhere (smaller chunks pay more top-k and merge work
+// than the wave tail costs).  SS_SEL_CHUNK (multiple of 32, <= 2048) overrides.
+static int sel_chunk_env() {
     static const int env = [] {
         const char* e = getenv("SS_SEL_CHUNK");
         int v = e ? atoi(e) : 0;
         if (e && (v < 32 || v > kSelChunkMax || (v % 32))) v = kSelChunkMax;
         return v;
     }();
-    if (env) return env;
+    return env;
+}
+constexpr int kSelChunkMin = 512;  // workspace sizing bound (SS_SEL_CHUNK may go lower)
+
+static int sel_chunk(int G, size_t, int, int, int) {
+    if (sel_chunk_env()) return sel_chunk_env();
     return G > 1 ? kSelChunkMax : kSelChunkDefault;
 }
 
+// Workspace: tickets [pairs] first (fixed place: they must stay zero between
+// calls whatever chunk size a call picks), then the chunk candidates, sized for
+// the smallest chunk.
 size_t select_ws_bytes(const ss_dims& d, int max_blk, int k) {
     const int G = d.num_kv_heads > 0 ? d.num_q_heads / d.num_kv_heads : 1;
-    int nchunks = (max_blk + sel_chunk(G) - 1) / sel_chunk(G);
+    const int ch = sel_chunk_env() ? sel_chunk_env() : kSelChunkMin;
+    (void)G;
+    int nchunks = (max_blk + ch - 1) / ch;
     size_t pairs = (size_t)d.batch * d.num_kv_heads;
     size_t nc = (size_t)pairs * nchunks * k;
-    size_t bytes = nc * 8 + nc * 4 + pairs * 4;
+    size_t bytes = ((pairs * 4 + 255) & ~(size_t)255) + nc * 8 + nc * 4;
     return (bytes + 255) & ~(size_t)255;
 }
 
-template <bool BF16, int G, bool ICV, bool MEAN>
+template <bool BF16, int G, bool ICV, bool MEAN, int TT = 2>
 static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_blk, int max_blk,
                               int k, const ss_dims& d, int32_t* sel, double* scores, void* ws,
                               cudaStream_t stream) {
-    const int CH = sel_chunk(G);
-    int nchunks = (max_blk + CH - 1) / CH;
     size_t pairs = (size_t)d.batch * d.num_kv_heads;
+    constexpr int kCtasPerSm = (G > 1 && !MEAN && TT == 1) ? 3 : 2;  // = __launch_bounds__
+    const int CH = sel_chunk(G, pairs, max_blk, k, kCtasPerSm * kNumSMs);
+    int nchunks = (max_blk + CH - 1) / CH;
     size_t nc = pairs * nchunks * k;
-    uint64_t* cand_key = (uint64_t*)ws;
-    int32_t* cand_j = (int32_t*)((char*)ws + nc * 8);
-    int32_t* tickets = (int32_t*)((char*)ws + nc * 12);
+    int32_t* tickets = (int32_t*)ws;
+    uint64_t* cand_key = (uint64_t*)((char*)ws + ((pairs * 4 + 255) & ~(size_t)255));
+    int32_t* cand_j = (int32_t*)((char*)cand_key + nc * 8);
     int nkeys = max(CH, min(nchunks * k, kSelMaxMerge));
     size_t smem = SelSmemLayout::bytes(G, nkeys);
-    auto kern = block_select_kernel<BF16, G, ICV, MEAN>;
+    auto kern = block_select_kernel<BF16, G, ICV, MEAN, TT>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return SS_ERR_CUDA;
@@ -515,16 +614,23 @@ ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_
                               int k, const ss_dims& d, ss_dtype dt, int32_t* sel, double* scores,
                               void* ws, cudaStream_t stream, bool mean) {
     int G = d.num_q_heads / d.num_kv_heads;
-    int nchunks = (max_blk + sel_chunk(G) - 1) / sel_chunk(G);
-    if ((size_t)nchunks * k > kSelMaxMerge && nchunks > 1) return SS_ERR_UNSUPPORTED;
+    {   // the largest chunk must keep the candidate merge within kSelMaxMerge keys
+        const int ch = sel_chunk_env() ? sel_chunk_env() : kSelChunkMax;
+        const int nchunks = (max_blk + ch - 1) / ch;
+        if ((size_t)nchunks * k > kSelMaxMerge && nchunks > 1) return SS_ERR_UNSUPPORTED;
+    }
     // integer-built float64 operands (default) or F2F conversions (SS_SEL_ICV=0, A/B only)
     static const bool icv = getenv("SS_SEL_ICV") ? atoi(getenv("SS_SEL_ICV")) != 0 : true;
+    // GQA: one tile per warp pass at 3 CTAs / SM (SS_SEL_TT=1) vs two (default)
+    static const bool tt1 = getenv("SS_SEL_TT") && atoi(getenv("SS_SEL_TT")) == 1;
 #define SS_SEL_ARGS q, meta, n_blk, max_blk, k, d, sel, scores, ws, stream
 #define SS_SEL_CASE(GG)                                                                       \
     case GG:                                                                                  \
         if (mean)                                                                             \
             return dt == SS_BF16 ? launch_sel_t<true, GG, true, true>(SS_SEL_ARGS)            \
                                  : launch_sel_t<false, GG, true, true>(SS_SEL_ARGS);          \
+        if (dt == SS_BF16 && tt1 && GG > 1)                                                   \
+            return launch_sel_t<true, GG, true, false, 1>(SS_SEL_ARGS);                       \
         if (dt == SS_BF16)                                                                    \
             return icv ? launch_sel_t<true, GG, true, false>(SS_SEL_ARGS)                     \
                        : launch_sel_t<true, GG, false, false>(SS_SEL_ARGS);                   \

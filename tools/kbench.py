@@ -137,8 +137,11 @@ def main():
     ap.add_argument("what", nargs="?", default="all")
     ap.add_argument("--cfg", default="C2")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--batch", type=int, default=0, help="override the config's batch (e.g. one request group)")
     a = ap.parse_args()
-    c = CFG[a.cfg]
+    c = dict(CFG[a.cfg])
+    if a.batch:
+        c["B"] = a.batch
     res = []
     if a.what in ("select", "all"):
         res.append(bench_select(c, a.iters))
