@@ -290,6 +290,33 @@ def solo_pass(eng, q_src, layers, hbm_peak, h2d_peak, stamp):
                     "alone (synchronize before and after), events on the launching stream"}
 
 
+def measure_flash_h2d_alone(eng, n_miss=8192, reps=3):
+    """FlashH2D alone on a large random miss list (one launch, nothing else on
+    the GPU) into a scratch buffer: the zero-copy gather's own ceiling on this
+    host link, for comparison with the copy-engine peak and the in-step rate."""
+    from paper_2509_24626_b200 import ops
+    c = eng.cfg
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    keys = torch.randint(0, eng.host_blocks, (n_miss,), generator=g, device="cuda", dtype=torch.int64)
+    slots = torch.arange(n_miss, dtype=torch.int32, device="cuda")
+    counts = torch.tensor([0, n_miss, 0, 0], dtype=torch.int32, device="cuda")
+    dst = torch.empty(n_miss * c.block_elems, dtype=c.dtype, device="cuda")
+    ops.flash_h2d_gather(eng.host_ptr, eng.host_blocks, keys, slots, counts, n_miss, dst, c.block_bytes)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(reps):
+        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+        torch.cuda._sleep(200000)
+        s.record()
+        ops.flash_h2d_gather(eng.host_ptr, eng.host_blocks, keys, slots, counts, n_miss, dst, c.block_bytes)
+        e.record()
+        torch.cuda.synchronize()
+        best = max(best, n_miss * c.block_bytes / (s.elapsed_time(e) * 1e-3) / 1e9)
+    del dst
+    return best
+
+
 def measure_h2d_peak(nbytes=1 << 30):
     h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
@@ -363,6 +390,7 @@ def bench_ours(args):
         gathered = [torch.empty(c.layers, c.num_q_heads * world, g.nb, 128, dtype=torch.float32,
                                 device="cuda") for g in eng.groups]
     h2d_peak = measure_h2d_peak()
+    gather_alone = measure_flash_h2d_alone(eng)
     setup_s = time.time() - t_setup
 
     def barrier():
@@ -587,6 +615,9 @@ def bench_ours(args):
             "h2d_bytes_per_step": n_miss * c.block_bytes / args.steps,
             "flash_h2d": {"achieved_gbs": kernels["flash_h2d_gather"]["achieved"],
                           "link_peak_gbs": round(h2d_peak, 2), "link_theoretical_gbs": 63.0,
+                          "alone_8192_misses_gbs": round(gather_alone, 2),
+                          "frac_of_alone": round(kernels["flash_h2d_gather"]["achieved"] / gather_alone, 4)
+                          if gather_alone else None,
                           "frac": kernels["flash_h2d_gather"]["frac"],
                           "h2d_gbs_over_step": round(n_miss * c.block_bytes / (ms * 1e-3) / 1e9, 2)},
             "roofline": roofline, "kernels": kernels, "kernels_solo": kernels_solo,

@@ -38,30 +38,39 @@ flash_h2d_kernel(const uint4* __restrict__ host, int64_t host_blocks,
     const int lane = lane_id();
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = gw; i < n; i += nw) {
+    // work unit = one batch of 32 x kH2DUnroll 16-byte loads (8 KiB with the
+    // default 16) of one block; units are dealt round-robin to the warps, so the
+    // warps of a call finish within one batch latency of each other (a whole-
+    // block unit leaves a two-batch tail)
+    constexpr int64_t kBatch = 32 * kH2DUnroll;
+    const int64_t upb = (vpb + kBatch - 1) / kBatch;  // units per block
+    const int64_t nu = (int64_t)n * upb;
+    for (int64_t u = gw; u < nu; u += nw) {
+        const int64_t i = u / upb, part = u - i * upb;
         const int64_t phys = miss_keys[i] % host_blocks;
         const uint4* src = host + phys * vpb;
         uint4* dst = pool + (int64_t)miss_slots[i] * vpb;
-        int64_t v = lane;
-        for (; v + 32 * (kH2DUnroll - 1) < vpb; v += 32 * kH2DUnroll) {
+        const int64_t v0 = part * kBatch + lane;
+        if (v0 + 32 * (kH2DUnroll - 1) < vpb) {
             uint4 r[kH2DUnroll];
 #pragma unroll
-            for (int u = 0; u < kH2DUnroll; ++u) r[u] = ldg_stream(src + v + 32 * u);
+            for (int k = 0; k < kH2DUnroll; ++k) r[k] = ldg_stream(src + v0 + 32 * k);
             // `zero` is 0 at run time but opaque to the compiler: every store
             // depends on ALL loads of the batch, so ptxas cannot interleave
             // stores with loads and all kH2DUnroll loads are in flight together
             uint32_t fold = 0;
 #pragma unroll
-            for (int u = 0; u < kH2DUnroll; ++u) fold ^= r[u].w;
+            for (int k = 0; k < kH2DUnroll; ++k) fold ^= r[k].w;
             const uint32_t dep = fold & zero;
 #pragma unroll
-            for (int u = 0; u < kH2DUnroll; ++u) {
-                uint4 x = r[u];
+            for (int k = 0; k < kH2DUnroll; ++k) {
+                uint4 x = r[k];
                 x.x ^= dep;
-                stg_v4(dst + v + 32 * u, x);
+                stg_v4(dst + v0 + 32 * k, x);
             }
+        } else {
+            for (int64_t v = v0; v < min(vpb, (part + 1) * kBatch); v += 32) stg_v4(dst + v, ldg_stream(src + v));
         }
-        for (; v < vpb; v += 32) stg_v4(dst + v, ldg_stream(src + v));
     }
 }
 
@@ -72,7 +81,7 @@ ss_status launch_flash_h2d(const void* host_kv, int64_t host_blocks, const int64
     // experiment knob: SS_H2D_SKIP=1 launches nothing (the step without PCIe time)
     static const bool skip = getenv("SS_H2D_SKIP") && atoi(getenv("SS_H2D_SKIP")) != 0;
     if (skip) return SS_OK;
-    int64_t warps_needed = max_misses;
+    int64_t warps_needed = (int64_t)max_misses * 2;  // ~2 units per block (bf16)
     static const int threads = getenv("SS_H2D_THREADS") ? atoi(getenv("SS_H2D_THREADS")) : 128;
     int64_t grid = (warps_needed * 32 + threads - 1) / threads;
     // Few CTAs on purpose: zero-copy PCIe loads in flight on an SM slow down
