@@ -108,7 +108,7 @@ def workload_cfg(args, world: int):
     assert wl.num_kv_heads % world == 0, "KV heads must divide across ranks"
     return dict(name=wl.name, batch=batch, layers=wl.layers, num_q_heads=wl.num_q_heads,
                 num_kv_heads=wl.num_kv_heads, n_blk=wl.n_blk, max_blk=wl.max_blk, topk=wl.topk,
-                slots=wl.slots_per_layer, rho=wl.rho, context=wl.context)
+                slots=args.slots or wl.slots_per_layer, rho=wl.rho, context=wl.context)
 
 
 def gen_host_blocks_on_gpu(engine, host_t, phys_blocks, seed, meta_phys, chunk_blocks=16384):
@@ -390,7 +390,7 @@ def bench_ours(args):
         gathered = [torch.empty(c.layers, c.num_q_heads * world, g.nb, 128, dtype=torch.float32,
                                 device="cuda") for g in eng.groups]
     h2d_peak = measure_h2d_peak()
-    gather_alone = measure_flash_h2d_alone(eng)
+    gather_alone = None if args.no_gather_alone else measure_flash_h2d_alone(eng)
     setup_s = time.time() - t_setup
 
     def barrier():
@@ -418,6 +418,10 @@ def bench_ours(args):
         torch.cuda.synchronize()
         if t == 0:
             cold_ms = s.elapsed_time(e)
+        if args.hit_trace and rank == 0:
+            hc = sum(g.counts.to(torch.int64).sum(0) for g in eng.groups).tolist()
+            print(f"settle t={t} ms={s.elapsed_time(e):.2f} hit={hc[0] / max(1, hc[0] + hc[1]):.4f} "
+                  f"miss={hc[1]}", file=sys.stderr, flush=True)
 
     # steps from here on read q from one static buffer; with --graph (default)
     # the whole step (all layers, groups and streams) is one captured CUDA graph
@@ -615,7 +619,7 @@ def bench_ours(args):
             "h2d_bytes_per_step": n_miss * c.block_bytes / args.steps,
             "flash_h2d": {"achieved_gbs": kernels["flash_h2d_gather"]["achieved"],
                           "link_peak_gbs": round(h2d_peak, 2), "link_theoretical_gbs": 63.0,
-                          "alone_8192_misses_gbs": round(gather_alone, 2),
+                          "alone_8192_misses_gbs": round(gather_alone, 2) if gather_alone else None,
                           "frac_of_alone": round(kernels["flash_h2d_gather"]["achieved"] / gather_alone, 4)
                           if gather_alone else None,
                           "frac": kernels["flash_h2d_gather"]["frac"],
@@ -690,6 +694,10 @@ def main():
                     help="untimed decode steps before the W warm-up steps (cache steady state)")
     ap.add_argument("--config", default="C2", choices=["C2", "C3"],
                     help="workload: C2 (default, the metric's config) or C3 (GQA 1M-context stress)")
+    ap.add_argument("--slots", type=int, default=0,
+                    help="HBM cache slots per layer pool (0: the workload's default)")
+    ap.add_argument("--hit-trace", action="store_true",
+                    help="print each settle/warm-up step's hit rate and time to stderr")
     ap.add_argument("--cpu-req", type=int, default=2)
     ap.add_argument("--cpu-layers", type=int, default=4)
     ap.add_argument("--timeline", default=None, help="write one step's op timeline (json, timing pass)")
@@ -704,6 +712,8 @@ def main():
     ap.add_argument("--cache-per-group", action="store_true",
                     help="per-group cache streams ordered per layer (no cross-layer cache-stream order)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gather-alone", action="store_true",
+                    help="skip the FlashH2D-alone ceiling measurement (profiling runs: keeps launch counts fixed)")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
