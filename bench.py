@@ -139,7 +139,7 @@ def setup_engine(args, rank: int, world: int):
                        max_blk=W["max_blk"], topk=W["topk"], slots_per_layer=W["slots"],
                        num_requests=W["batch"], dtype=torch.bfloat16, groups=args.groups,
                        h2d_streams=args.h2d_streams, select_priority=args.select_priority,
-                       cache_per_group=args.cache_per_group)
+                       cache_per_group=args.cache_per_group, h2d_server=bool(args.h2d_server))
     eng = DecodeEngine(cfg)
     # physical host pool: a prime number of max_blk runs (aliasing, R15)
     runs = args.host_runs if cfg.max_blk <= 4096 else max(1, (args.host_runs * 4096) // cfg.max_blk)
@@ -421,7 +421,7 @@ def bench_ours(args):
         if args.hit_trace and rank == 0:
             hc = sum(g.counts.to(torch.int64).sum(0) for g in eng.groups).tolist()
             print(f"settle t={t} ms={s.elapsed_time(e):.2f} hit={hc[0] / max(1, hc[0] + hc[1]):.4f} "
-                  f"miss={hc[1]}", file=sys.stderr, flush=True)
+                  f"miss={hc[1]} err={hc[3]}", file=sys.stderr, flush=True)
 
     # steps from here on read q from one static buffer; with --graph (default)
     # the whole step (all layers, groups and streams) is one captured CUDA graph
@@ -557,7 +557,10 @@ def bench_ours(args):
                               "peak": round(h2d_peak, 2), "unit": "GB/s",
                               "frac": round(h2d_gbs / h2d_peak, 4) if h2d_peak else None,
                               "us_per_launch": round(tot["gather"] * 1e3 / max(1, nlaunch["gather"]), 2),
-                              "bytes_per_launch": int(miss_bytes_kt / max(1, nlaunch["gather"]))},
+                              "bytes_per_launch": int(miss_bytes_kt / max(1, nlaunch["gather"])),
+                              "launch": ("flash_h2d_serve: one persistent launch per step serving every "
+                                         "layer's and group's misses" if eng.server else
+                                         "flash_h2d_gather: one launch per layer and request group")},
         "kv_cache_lookup_insert": {"bound": "latency",
                                    "us_per_launch": round(tot["cache"] * 1e3 / max(1, nlaunch["cache"]), 2)},
         "timing_pass": {"steps": n_kt, "eager": graph is None, "request_groups": len(eng.groups),
@@ -576,12 +579,22 @@ def bench_ours(args):
              "flash_h2d_gather": miss_bytes_kt / h2d_peak if h2d_peak else 0.0}
     dom = max(share, key=share.get)
     dk = kernels[dom]
+    # traffic: measured DRAM (HBM kernels) or PCIe-read (FlashH2D) bytes per
+    # algorithmic byte from the committed ncu captures (profiles/traffic.json),
+    # scaled to this launch's algorithmic bytes
     traffic = None
     prof_t = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof_t):
-        traffic = json.load(open(prof_t)).get(dom)
+        tj = json.load(open(prof_t))
+        if dom == "flash_h2d_gather" and "flash_h2d_pcie_read_bytes_per_miss" in tj:
+            traffic = int(tj["flash_h2d_pcie_read_bytes_per_miss"] * k_miss / max(1, nlaunch["gather"]))
+        elif dom in tj.get("traffic_per_algorithmic_byte", {}):
+            traffic = int(tj["traffic_per_algorithmic_byte"][dom] * dk["bytes_per_launch"])
     roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"], "peak": dk["peak"],
                 "unit": "GB/s", "frac": dk["frac"], "traffic": traffic,
+                "traffic_metric": ("pcie__read_bytes.sum per launch (profiles/traffic.json x this launch's misses)"
+                                   if dom == "flash_h2d_gather" else
+                                   "dram__bytes_read.sum + dram__bytes_write.sum per launch (profiles/traffic.json ratio)"),
                 "peak_source": peak_src if dk["bound"] == "hbm" else "bulk pinned cudaMemcpy H2D, measured in this run"}
 
     # ---- each kernel alone (its own roofline fraction, no co-running group) ----
@@ -610,7 +623,7 @@ def bench_ours(args):
                        "topk_blocks": c.topk, "hbm_cache_slots_per_layer": c.slots_per_layer,
                        "host_pool_blocks": eng.host_blocks, "host_kv": "pinned DRAM, zero-copy (UVA)",
                        "parallelism": f"kv-heads/{world} per GPU" if world > 1 else "1 GPU",
-                       "request_groups": len(eng.groups), "h2d_streams": args.h2d_streams, "select_priority": args.select_priority, "cache_per_group": args.cache_per_group,
+                       "request_groups": len(eng.groups), "h2d_server": eng.server, "h2d_streams": args.h2d_streams, "select_priority": args.select_priority, "cache_per_group": args.cache_per_group,
                        "cuda_graph": graph is not None,
                        "cache_settle_steps": args.settle,
                        "l2": f"no flush needed: inputs larger than L2 ({meta_gib:.0f} GiB metadata streamed per step)",
@@ -626,7 +639,7 @@ def bench_ours(args):
                           "h2d_gbs_over_step": round(n_miss * c.block_bytes / (ms * 1e-3) / 1e9, 2)},
             "roofline": roofline, "kernels": kernels, "kernels_solo": kernels_solo,
             "cold_step_ms": round(cold_ms, 2) if cold_ms else None,
-            "e2e": e2e, "gpu_launches": int(args.steps * c.layers * 6 * len(eng.groups)),
+            "e2e": e2e, "gpu_launches": int(args.steps * (c.layers * 6 * len(eng.groups) + (1 if eng.server else 0))),
             "cpu_baseline": cpu, "clocks": clocks, "setup_s": round(setup_s, 1),
             "errors_in_timed_region": n_err,
         }
@@ -690,7 +703,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--host-runs", type=int, default=251,
                     help="physical host KV pool = host_runs x max_blk blocks (251 -> 15.7 GiB)")
-    ap.add_argument("--settle", type=int, default=30,
+    ap.add_argument("--settle", type=int, default=80,
                     help="untimed decode steps before the W warm-up steps (cache steady state)")
     ap.add_argument("--config", default="C2", choices=["C2", "C3"],
                     help="workload: C2 (default, the metric's config) or C3 (GQA 1M-context stress)")
@@ -711,6 +724,10 @@ def main():
                     help="select on high-priority per-group streams (it feeds the PCIe link)")
     ap.add_argument("--cache-per-group", action="store_true",
                     help="per-group cache streams ordered per layer (no cross-layer cache-stream order)")
+    ap.add_argument("--h2d-server", type=int, default=1,
+                    help="1: the step's FlashH2D gathers are served by one persistent launch "
+                         "(flash_h2d_serve); 0: one flash_h2d_gather launch per layer and group "
+                         "(use 0 under ncu, which serialises kernels)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gather-alone", action="store_true",
                     help="skip the FlashH2D-alone ceiling measurement (profiling runs: keeps launch counts fixed)")

@@ -205,6 +205,52 @@ ss_status flash_h2d_gather(const void* host_kv, int64_t host_blocks, const int64
                            const int32_t* miss_slots, const int32_t* counts, int32_t max_misses,
                            void* pool_kv, int64_t block_bytes, void* stream);
 
+/* S4, pipelined form -- the same FlashH2D copy (§3.2.1) for
+ * every gather of a decode step, served by ONE persistent launch so the host
+ * link does not drain at each layer boundary.  Each job is one
+ * flash_h2d_gather's arguments; jobs are served in array order.
+ *   jobs      device array of njobs ss_h2d_job (read-only except counts[3],
+ *             see abort below).  pool_kv / max_misses / block_bytes as above.
+ *   flags     device int32 [4*njobs + 1], ZEROED by the caller before the
+ *             launch: [0,nj) ready, [nj,2nj) done, [2nj,4nj) server scratch,
+ *             [4nj] abort.  Job j starts once ready[j] != 0 (set it with
+ *             ss_flag_signal, stream-ordered after the job's
+ *             kv_cache_lookup_insert); done[j] becomes 1 (release, GPU scope)
+ *             after all of job j's blocks are in HBM -- wait for it with
+ *             ss_flag_wait before reading the pool.
+ *   Errors: a job not ready within 3 s (SS_SERVE_TIMEOUT_MS) aborts the
+ *   server; every job not yet done then gets counts[3] = SS_ERR_CUDA and
+ *   done = 1 (no waiter hangs; downstream attention becomes a no-op).  The
+ *   launch never completes before every ready job is served, so a job whose
+ *   producer runs only after the server (e.g. a profiler serialising kernels)
+ *   aborts: use flash_h2d_gather there. */
+typedef struct {
+    const int64_t* miss_keys;
+    const int32_t* miss_slots;
+    int32_t* counts;
+    void* pool_kv;
+    int32_t max_misses;
+    int32_t reserved;
+} ss_h2d_job;
+
+ss_status flash_h2d_serve(const void* host_kv, int64_t host_blocks, const ss_h2d_job* jobs,
+                          int32_t njobs, int64_t block_bytes, int32_t* flags, void* stream);
+
+/* Stream-ordered flag signal / wait for flash_h2d_serve.
+ *   ss_flag_signal: *flag = 1 (device int32 that was 0), after all prior work
+ *                   on `stream` (a 1-byte memset: no kernel).
+ *   ss_flag_wait:   later work on `stream` starts only after *flag != 0
+ *                   (acquire, GPU scope), observed by a one-thread kernel;
+ *                   gives up after the same timeout. */
+ss_status ss_flag_signal(int32_t* flag, void* stream);
+
+/* Load every kernel of the library now (CUDA lazy module loading would load
+ * each one at its first launch; a first launch that has to wait behind a
+ * spinning flash_h2d_serve can stall it).  flash_h2d_serve calls it itself on
+ * its first call outside stream capture.  Idempotent; SS_ERR_CUDA on failure. */
+ss_status ss_preload_kernels(void);
+ss_status ss_flag_wait(const int32_t* flag, void* stream);
+
 /* S5  sparse_decode_attn -- PAPER.md:71-72 §2.1 (S = QK^T/sqrt(d), P =
  * softmax(S), O = PV) restricted to the selected blocks.
  *   q         device [B][Hq][d] dtype dt.

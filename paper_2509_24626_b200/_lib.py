@@ -20,7 +20,8 @@ EXPORTS = ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert", "fl
            "sparse_decode_attn", "ss_workspace_size", "ss_host_device_pointer",
            "ss_status_string", "ss_version", "kv_append", "kv_seal_blocks", "kv_commit",
            "ss_d2h_create", "ss_d2h_destroy", "flash_d2h_save", "ws_track", "ss_admit", "prefill_layer_save",
-           "block_meta_update_mean", "ss_block_select_mean")
+           "block_meta_update_mean", "ss_block_select_mean", "flash_h2d_serve", "ss_flag_signal",
+           "ss_flag_wait", "ss_preload_kernels")
 
 
 class SSDims(ctypes.Structure):
@@ -35,6 +36,12 @@ class SSCachePool(ctypes.Structure):
                 ("order", ctypes.c_void_p), ("order_pos", ctypes.c_void_p),
                 ("num_slots", ctypes.c_int32),
                 ("clock", ctypes.c_void_p)]
+
+
+class SSH2DJob(ctypes.Structure):
+    _fields_ = [("miss_keys", ctypes.c_void_p), ("miss_slots", ctypes.c_void_p),
+                ("counts", ctypes.c_void_p), ("pool_kv", ctypes.c_void_p),
+                ("max_misses", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class SparseServeError(RuntimeError):
@@ -60,6 +67,10 @@ def load() -> ctypes.CDLL:
     L.kv_cache_lookup_insert.argtypes = [SSCachePool, P, P, I32, I32, I32, I32, SSDims, I64, P, P,
                                          P, P, P, P, SZ, P]
     L.flash_h2d_gather.argtypes = [P, I64, P, P, P, I32, P, I64, P]
+    L.flash_h2d_serve.argtypes = [P, I64, P, I32, I64, P, P]
+    L.ss_flag_signal.argtypes = [P, P]
+    L.ss_flag_wait.argtypes = [P, P]
+    L.ss_preload_kernels.argtypes = []
     L.sparse_decode_attn.argtypes = [P, P, P, I32, P, P, SSDims, I32, F, P, P, P, SZ, P]
     L.ss_workspace_size.argtypes = [I32, SSDims, I32, I32, I32]
     L.ss_workspace_size.restype = SZ
@@ -83,7 +94,8 @@ def load() -> ctypes.CDLL:
     for name in ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert",
                  "flash_h2d_gather", "sparse_decode_attn", "ss_host_device_pointer", "kv_append",
                  "kv_seal_blocks", "kv_commit", "ss_d2h_create", "ss_d2h_destroy",
-                 "flash_d2h_save", "block_meta_update_mean", "ss_block_select_mean"):
+                 "flash_d2h_save", "block_meta_update_mean", "ss_block_select_mean", "flash_h2d_serve",
+                 "ss_flag_signal", "ss_flag_wait", "ss_preload_kernels"):
         getattr(L, name).restype = I32
     _lib = L
     return L

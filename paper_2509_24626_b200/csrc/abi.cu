@@ -22,6 +22,9 @@ size_t cache_ws_bytes(const ss_dims& d, int k, int S);
 ss_status launch_flash_h2d(const void* host_kv, int64_t host_blocks, const int64_t* miss_keys,
                            const int32_t* miss_slots, const int32_t* counts, int max_misses,
                            void* pool_kv, int64_t block_bytes, cudaStream_t stream);
+ss_status launch_flash_h2d_serve(const void* host_kv, int64_t host_blocks, const ss_h2d_job* jobs,
+                                 int njobs, int64_t block_bytes, int32_t* flags, cudaStream_t stream);
+ss_status launch_flag_wait(const int32_t* flag, cudaStream_t stream);
 ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* slot, int k,
                              const void* tail_kv, const int32_t* tail_len, const ss_dims& d,
                              ss_dtype dt, float scale, const int32_t* counts, float* out, void* ws,
@@ -42,6 +45,13 @@ ss_status launch_prefill_layer_save(const void* k_nhd, const void* v_nhd, int n_
 ss_status launch_ws_track(const int32_t* sel, int k, const ss_dims& d, int max_blk, int64_t t,
                           int w, int32_t* last_sel, int32_t* ring, int32_t* ws_count,
                           cudaStream_t stream);
+bool preload_select();
+bool preload_attn();
+bool preload_cache();
+bool preload_save();
+bool preload_ws();
+bool preload_meta();
+bool preload_h2d();
 }  // namespace ss
 
 namespace {
@@ -139,6 +149,41 @@ ss_status flash_h2d_gather(const void* host_kv, int64_t host_blocks, const int64
     if (!aligned16(host_kv) || !aligned16(pool_kv)) return SS_ERR_INVALID_ARG;
     return ss::launch_flash_h2d(host_kv, host_blocks, miss_keys, miss_slots, counts, max_misses,
                                 pool_kv, block_bytes, (cudaStream_t)stream);
+}
+
+ss_status ss_preload_kernels(void) {
+    static const bool ok = ss::preload_select() & ss::preload_attn() & ss::preload_cache() &
+                           ss::preload_save() & ss::preload_ws() & ss::preload_meta() & ss::preload_h2d();
+    return ok ? SS_OK : SS_ERR_CUDA;
+}
+
+ss_status flash_h2d_serve(const void* host_kv, int64_t host_blocks, const ss_h2d_job* jobs,
+                          int32_t njobs, int64_t block_bytes, int32_t* flags, void* stream) {
+    if (njobs < 0) return SS_ERR_INVALID_ARG;
+    if (njobs == 0) return SS_OK;
+    if (!host_kv || !jobs || !flags || host_blocks < 1) return SS_ERR_INVALID_ARG;
+    if (block_bytes < 16 || (block_bytes % 16) != 0 || !aligned16(host_kv)) return SS_ERR_INVALID_ARG;
+    // every kernel of the library must be loaded before a server spins (lazy
+    // module loading could otherwise stall a producer kernel's first launch
+    // behind the spinning server); outside stream capture only
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing((cudaStream_t)stream, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {
+        if (ss_preload_kernels() != SS_OK) return SS_ERR_CUDA;
+    }
+    return ss::launch_flash_h2d_serve(host_kv, host_blocks, jobs, njobs, block_bytes, flags,
+                                      (cudaStream_t)stream);
+}
+
+ss_status ss_flag_signal(int32_t* flag, void* stream) {
+    if (!flag) return SS_ERR_INVALID_ARG;
+    // little-endian: byte 0 = 1 makes the (zeroed) int32 equal to 1
+    if (cudaMemsetAsync(flag, 1, 1, (cudaStream_t)stream) != cudaSuccess) return SS_ERR_CUDA;
+    return SS_OK;
+}
+
+ss_status ss_flag_wait(const int32_t* flag, void* stream) {
+    if (!flag) return SS_ERR_INVALID_ARG;
+    return ss::launch_flag_wait(flag, (cudaStream_t)stream);
 }
 
 ss_status sparse_decode_attn(const void* q, const void* pool_kv, const int32_t* slot, int32_t k,

@@ -648,4 +648,21 @@ ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_
 #undef SS_SEL_ARGS
 }
 
+bool preload_select() {
+    bool ok = true;
+#define SS_PL(GG)                                                                     \
+    ok &= preload_fn(block_select_kernel<true, GG, true, true, 2>);                  \
+    ok &= preload_fn(block_select_kernel<false, GG, true, true, 2>);                 \
+    ok &= preload_fn(block_select_kernel<true, GG, true, false, 2>);                 \
+    ok &= preload_fn(block_select_kernel<true, GG, false, false, 2>);                \
+    ok &= preload_fn(block_select_kernel<false, GG, true, false, 2>);                \
+    ok &= preload_fn(block_select_kernel<false, GG, false, false, 2>);
+    SS_PL(1) SS_PL(2) SS_PL(4) SS_PL(8)
+#undef SS_PL
+    ok &= preload_fn(block_select_kernel<true, 2, true, false, 1>);
+    ok &= preload_fn(block_select_kernel<true, 4, true, false, 1>);
+    ok &= preload_fn(block_select_kernel<true, 8, true, false, 1>);
+    return ok;
+}
+
 }  // namespace ss

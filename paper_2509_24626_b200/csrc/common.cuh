@@ -39,6 +39,15 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// Force-load a kernel under CUDA lazy module loading (cudaFuncGetAttributes
+// loads the function).  A kernel first launched while a persistent kernel
+// spins on work it produces can otherwise stall behind the load.
+template <typename K>
+inline bool preload_fn(K* k) {
+    cudaFuncAttributes a;
+    return cudaFuncGetAttributes(&a, (const void*)k) == cudaSuccess;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -101,4 +101,160 @@ ss_status launch_flash_h2d(const void* host_kv, int64_t host_blocks, const int64
     return SS_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// FlashH2D server (flash_h2d_serve): ONE persistent launch serves the ordered
+// sequence of gathers ("jobs") of a whole decode step -- one job per (layer,
+// request group) -- so the PCIe link does not drain and refill at every layer
+// boundary.  Warps walk the jobs in order; job j's inputs are valid once
+// ready[j] != 0 (ss_flag_signal after its kv_cache_lookup_insert); its work
+// units are handed out by an atomic cursor, so warps done with job j start
+// job j+1's loads while others still finish job j.  The warp that completes
+// job j's last unit publishes done[j] = 1 (release), which ss_flag_wait turns
+// into a stream dependency for that job's attention.
+//
+// flags (device int32, zeroed by the caller before each launch):
+//   [0, nj) ready   [nj, 2nj) done   [2nj, 3nj) unit cursor
+//   [3nj, 4nj) finished units        [4nj] abort
+// A job that is not ready within the timeout aborts the server: every job not
+// yet done gets counts[3] = SS_ERR_CUDA (downstream attention becomes a no-op,
+// the error is visible in the counts) and done = 1, so nothing waits forever.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t gtimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int32_t* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int kU>
+__global__ void __launch_bounds__(kH2DThreadsMax)
+flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
+                        const ss_h2d_job* __restrict__ jobs, int njobs, int64_t vpb,
+                        int32_t* flags, uint32_t zero, uint64_t timeout_ns) {
+    int32_t* ready = flags;
+    int32_t* done = flags + njobs;
+    int32_t* cursor = flags + 2 * njobs;
+    int32_t* fin = flags + 3 * njobs;
+    int32_t* abort_flag = flags + 4 * njobs;
+    const int lane = lane_id();
+    constexpr int64_t kBatch = 32 * kU;
+    const int upb = (int)((vpb + kBatch - 1) / kBatch);  // units per block
+    int j = 0;
+    bool aborted = false;
+    for (; j < njobs; ++j) {
+        int ok = 1;
+        if (lane == 0) {
+            const uint64_t t0 = gtimer_ns();
+            while (ld_acquire_gpu(ready + j) == 0) {
+                if (*(volatile int32_t*)abort_flag) { ok = 0; break; }
+                if (gtimer_ns() - t0 > timeout_ns) { atomicExch(abort_flag, 1); ok = 0; break; }
+                __nanosleep(64);
+            }
+        }
+        if (!__shfl_sync(0xffffffffu, ok, 0)) { aborted = true; break; }
+        const ss_h2d_job jb = jobs[j];
+        const int err = __ldcg(jb.counts + 3);
+        const int n = err ? 0 : min(__ldcg(jb.counts + 1), jb.max_misses);
+        const int nu = n * upb;
+        int u = 0;
+        if (lane == 0) u = atomicAdd(cursor + j, 1);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (nu == 0) {
+            if (u == 0 && lane == 0) st_release_gpu(done + j, 1);
+            continue;
+        }
+        const uint4* hsrc = host;
+        uint4* pool = (uint4*)jb.pool_kv;
+        while (u < nu) {
+            const int i = u / upb, part = u - i * upb;
+            const int64_t phys = __ldcg(jb.miss_keys + i) % host_blocks;
+            const uint4* src = hsrc + phys * vpb;
+            uint4* dst = pool + (int64_t)__ldcg(jb.miss_slots + i) * vpb;
+            const int64_t v0 = (int64_t)part * kBatch + lane;
+            if (v0 + 32 * (kU - 1) < vpb) {
+                uint4 r[kU];
+#pragma unroll
+                for (int k = 0; k < kU; ++k) r[k] = ldg_stream(src + v0 + 32 * k);
+                uint32_t fold = 0;
+#pragma unroll
+                for (int k = 0; k < kU; ++k) fold ^= r[k].w;
+                const uint32_t dep = fold & zero;
+#pragma unroll
+                for (int k = 0; k < kU; ++k) {
+                    uint4 x = r[k];
+                    x.x ^= dep;
+                    stg_v4(dst + v0 + 32 * k, x);
+                }
+            } else {
+                for (int64_t v = v0; v < min(vpb, (int64_t)(part + 1) * kBatch); v += 32)
+                    stg_v4(dst + v, ldg_stream(src + v));
+            }
+            __threadfence();  // this lane's pool stores are visible GPU-wide ...
+            __syncwarp();
+            if (lane == 0) {  // ... before the unit is counted
+                const int f = atomicAdd(fin + j, 1);
+                if (f == nu - 1) {
+                    __threadfence();
+                    st_release_gpu(done + j, 1);
+                }
+                u = atomicAdd(cursor + j, 1);
+            }
+            u = __shfl_sync(0xffffffffu, u, 0);
+        }
+    }
+    if (aborted && lane == 0) {
+        for (int jj = j; jj < njobs; ++jj) {
+            if (ld_acquire_gpu(done + jj) == 0) {
+                atomicExch(jobs[jj].counts + 3, (int)SS_ERR_CUDA);
+                __threadfence();
+                st_release_gpu(done + jj, 1);
+            }
+        }
+    }
+}
+
+__global__ void flag_wait_kernel(const int32_t* flag, uint64_t timeout_ns) {
+    const uint64_t t0 = gtimer_ns();
+    while (ld_acquire_gpu(flag) == 0) {
+        if (gtimer_ns() - t0 > timeout_ns) break;
+        __nanosleep(128);
+    }
+}
+
+static uint64_t serve_timeout_ns() {
+    static const uint64_t t = getenv("SS_SERVE_TIMEOUT_MS") ? (uint64_t)atoll(getenv("SS_SERVE_TIMEOUT_MS")) * 1000000ull
+                                                            : 3000000000ull;  // 3 s
+    return t;
+}
+
+ss_status launch_flash_h2d_serve(const void* host_kv, int64_t host_blocks, const ss_h2d_job* jobs,
+                                 int njobs, int64_t block_bytes, int32_t* flags, cudaStream_t stream) {
+    if (njobs <= 0) return SS_OK;
+    static const int threads = getenv("SS_H2D_THREADS") ? atoi(getenv("SS_H2D_THREADS")) : 128;
+    static const int ctas = getenv("SS_H2D_CTAS") ? atoi(getenv("SS_H2D_CTAS")) : kH2DCtas;
+    flash_h2d_server_kernel<16><<<ctas, threads, 0, stream>>>(
+        (const uint4*)host_kv, host_blocks, jobs, njobs, block_bytes / 16, flags, 0u, serve_timeout_ns());
+    SS_LAUNCH_CHECK();
+    return SS_OK;
+}
+
+ss_status launch_flag_wait(const int32_t* flag, cudaStream_t stream) {
+    flag_wait_kernel<<<1, 32, 0, stream>>>(flag, serve_timeout_ns());
+    SS_LAUNCH_CHECK();
+    return SS_OK;
+}
+
+bool preload_h2d() {
+    return preload_fn(flash_h2d_kernel<16>) && preload_fn(flash_h2d_kernel<8>) &&
+           preload_fn(flash_h2d_server_kernel<16>) && preload_fn(flag_wait_kernel);
+}
+
 }  // namespace ss

@@ -419,4 +419,9 @@ ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int3
     return SS_OK;
 }
 
+bool preload_cache() {
+    return preload_fn(cache_lookup_count_kernel) && preload_fn(cache_victim_kernel) &&
+           preload_fn(cache_assign_place_kernel);
+}
+
 }  // namespace ss

@@ -345,4 +345,9 @@ ss_status launch_prefill_layer_save(const void* k_nhd, const void* v_nhd, int n_
     return SS_OK;
 }
 
+bool preload_save() {
+    return preload_fn(kv_append_kernel) && preload_fn(kv_seal_copy_kernel) && preload_fn(kv_commit_kernel) &&
+           preload_fn(prefill_relayout_kernel) && preload_fn(prefill_counters_kernel);
+}
+
 }  // namespace ss

@@ -121,4 +121,9 @@ ss_status launch_meta_update(const void* keys, int64_t key_stride, const int64_t
     return SS_OK;
 }
 
+bool preload_meta() {
+    return preload_fn(meta_update_kernel<uint16_t>) && preload_fn(meta_update_kernel<uint32_t>) &&
+           preload_fn(meta_mean_kernel<uint16_t>) && preload_fn(meta_mean_kernel<uint32_t>);
+}
+
 }  // namespace ss

@@ -1032,4 +1032,15 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
 #undef SS_ATTN_CASE
 }
 
+bool preload_attn() {
+    bool ok = true;
+#define SS_PL(GG)                                              \
+    ok &= preload_fn(sparse_attn_mma_kernel<GG>);             \
+    ok &= preload_fn(sparse_attn_kernel<true, GG>);           \
+    ok &= preload_fn(sparse_attn_kernel<false, GG>);
+    SS_PL(1) SS_PL(2) SS_PL(4) SS_PL(8)
+#undef SS_PL
+    return ok;
+}
+
 }  // namespace ss

@@ -61,4 +61,6 @@ ss_status launch_ws_track(const int32_t* sel, int k, const ss_dims& d, int max_b
     return SS_OK;
 }
 
+bool preload_ws() { return preload_fn(ws_track_kernel); }
+
 }  // namespace ss

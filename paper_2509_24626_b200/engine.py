@@ -44,6 +44,7 @@ class EngineConfig:
     h2d_streams: int = 1       # FlashH2D streams shared round-robin by the groups
     select_priority: bool = False  # run select on a high-priority per-group stream
     cache_per_group: bool = False  # per-group cache streams, ordered per layer only
+    h2d_server: bool = False   # one persistent FlashH2D launch per step (flash_h2d_serve)
 
     @property
     def group(self) -> int:
@@ -170,6 +171,17 @@ class DecodeEngine:
         if ng > 1 and c.select_priority:
             for g in self.groups:
                 g.sel_stream = torch.cuda.Stream(dev, priority=-1)
+        # FlashH2D server (EngineConfig.h2d_server, multi-group only): the step's
+        # gathers are jobs j = l * groups + gi of ONE persistent launch on the
+        # h2d stream; a cache call signals ready[j], the group's attention
+        # waits on done[j] (flash_h2d_serve in include/sparseserve.h)
+        self.server = ng > 1 and c.h2d_server
+        if self.server:
+            self.njobs = c.layers * ng
+            self.h2d_jobs = ops.h2d_jobs([(g.miss_keys[l], g.miss_slots[l], g.counts[l], self.pool_kv[l], g.E)
+                                          for l in range(c.layers) for g in self.groups], device=dev)
+            self.h2d_flags = ops.h2d_flags(self.njobs, device=dev)
+            ops.preload_kernels()      # no lazy kernel load while the server spins
         self._capturing = False
         g0 = self.groups[0]
         # single-group aliases (tests, smoke)
@@ -270,7 +282,11 @@ class DecodeEngine:
             with torch.cuda.stream(cs):
                 _cache()
                 g.ev_cache[l].record(cs)
-            if gather:
+            if gather and self.server:
+                j = l * len(self.groups) + gi
+                ops.flag_signal(self.h2d_flags[j:j + 1], stream=cs)
+                ops.flag_wait(self.h2d_flags[self.njobs + j:self.njobs + j + 1], stream=g.stream)
+            elif gather:
                 g.h2d_stream.wait_event(g.ev_cache[l])
                 with torch.cuda.stream(g.h2d_stream):
                     _gather()
@@ -303,6 +319,8 @@ class DecodeEngine:
                     post_attn(0, self.groups[0], l)
             return
         cur = torch.cuda.current_stream(self.device)
+        if self.server:
+            self.h2d_flags.zero_()     # before every stream below forks off `cur`
         for g in self.groups:
             g.stream.wait_stream(cur)
         self.cache_stream.wait_stream(cur)
@@ -312,6 +330,16 @@ class DecodeEngine:
         # (per-group select streams wait on their group stream, which waits on cur)
         for hs in self.h2d_streams:
             hs.wait_stream(cur)
+        if self.server:
+            hs = self.h2d_streams[0]
+            with torch.cuda.stream(hs):
+                if timers is not None:
+                    ts, te = timers.mark("gather", 0, 0)
+                    ts.record()
+                ops.flash_h2d_serve(self.host_ptr, self.host_blocks, self.h2d_jobs, self.njobs,
+                                    c.block_bytes, self.h2d_flags)
+                if timers is not None:
+                    te.record()
         # issue layer by layer, group by group: group A's FlashH2D (PCIe) overlaps
         # group B's select / attention (HBM) on the other stream
         for l in range(c.layers):
@@ -324,6 +352,12 @@ class DecodeEngine:
             cur.wait_stream(g.stream)
         for hs in self.h2d_streams:
             cur.wait_stream(hs)
+        # join the cache streams too (their last op, a ready-flag signal, has no
+        # other consumer on the host-visible streams)
+        cur.wait_stream(self.cache_stream)
+        for g in self.groups:
+            if g.cache_stream is not None:
+                cur.wait_stream(g.cache_stream)
 
     def outputs(self) -> List[torch.Tensor]:
         return [g.out for g in self.groups]

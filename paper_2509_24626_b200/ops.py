@@ -168,6 +168,46 @@ def flash_h2d_gather(host_kv_dev_ptr: int, host_blocks: int, miss_keys: torch.Te
           "flash_h2d_gather")
 
 
+def h2d_jobs(jobs, device=None) -> torch.Tensor:
+    """Device array of ss_h2d_job for flash_h2d_serve.  jobs: list of
+    (miss_keys int64, miss_slots int32, counts int32[4], pool_kv, max_misses)."""
+    arr = (_lib.SSH2DJob * len(jobs))()
+    for i, (mk, ms, cnt, pool, mm) in enumerate(jobs):
+        assert mk.dtype == torch.int64 and ms.dtype == torch.int32 and cnt.dtype == torch.int32
+        arr[i] = _lib.SSH2DJob(_ptr(mk), _ptr(ms), _ptr(cnt), _ptr(pool), int(mm), 0)
+    raw = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8)
+    return raw.to(device or "cuda")
+
+
+def h2d_flags(njobs: int, device=None) -> torch.Tensor:
+    """Zeroed flag words for flash_h2d_serve ([4*njobs + 1] int32)."""
+    return torch.zeros(4 * njobs + 1, dtype=torch.int32, device=device or "cuda")
+
+
+def flash_h2d_serve(host_kv_dev_ptr: int, host_blocks: int, jobs: torch.Tensor, njobs: int,
+                    block_bytes: int, flags: torch.Tensor, stream=None) -> None:
+    """S4, pipelined: one persistent launch serves njobs gathers in order (job j
+    once flags[j] != 0; sets flags[njobs + j] = 1 when its blocks are in HBM)."""
+    assert flags.dtype == torch.int32 and flags.numel() >= 4 * njobs + 1
+    check(_lib.load().flash_h2d_serve(host_kv_dev_ptr, host_blocks, _ptr(jobs), njobs, block_bytes,
+                                      _ptr(flags), _stream(stream)), "flash_h2d_serve")
+
+
+def preload_kernels() -> None:
+    """Load every kernel of the library now (see ss_preload_kernels)."""
+    check(_lib.load().ss_preload_kernels(), "ss_preload_kernels")
+
+
+def flag_signal(flag: torch.Tensor, stream=None) -> None:
+    """*flag = 1 after prior work on the stream (flag: one int32 element view)."""
+    check(_lib.load().ss_flag_signal(flag.data_ptr(), _stream(stream)), "ss_flag_signal")
+
+
+def flag_wait(flag: torch.Tensor, stream=None) -> None:
+    """Later work on the stream waits until *flag != 0."""
+    check(_lib.load().ss_flag_wait(flag.data_ptr(), _stream(stream)), "ss_flag_wait")
+
+
 def sparse_decode_attn(q: torch.Tensor, pool_kv: torch.Tensor, slot: torch.Tensor, k: int,
                        tail_kv: torch.Tensor, tail_len: torch.Tensor, d: SSDims, scale: float,
                        out: torch.Tensor, ws: torch.Tensor, counts: Optional[torch.Tensor] = None,

@@ -132,12 +132,14 @@ def test_f32_pipeline():
                   steps=8, rho=0.9, seed=3)
 
 
-@pytest.mark.parametrize("graph_after", [None, 4])
-def test_request_groups_pipeline_two_streams(graph_after):
+@pytest.mark.parametrize("graph_after,server,ngroups", [(None, False, 2), (4, False, 2), (None, True, 2),
+                                                        (4, True, 2), (4, True, 3)])
+def test_request_groups_pipeline_two_streams(graph_after, server, ngroups):
     """groups=2: the two request groups run on separate streams; per layer the
     oracle makes the same two cache calls (group order, same stamp).  With
     graph_after=4 the steps from 4 on are replays of one captured CUDA graph
-    whose LRU stamps come from the pools' device clocks."""
+    whose LRU stamps come from the pools' device clocks.  server=True: the
+    step's gathers are jobs of one persistent flash_h2d_serve launch."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     from paper_2509_24626_b200.engine import DecodeEngine, EngineConfig
@@ -148,9 +150,10 @@ def test_request_groups_pipeline_two_streams(graph_after):
     max_blk = 1504
     S = B * Hkv * k * 2
     cfg = EngineConfig(batch=B, layers=L, num_q_heads=Hq, num_kv_heads=Hkv, max_blk=max_blk, topk=k,
-                       slots_per_layer=S, num_requests=B, dtype=torch.bfloat16, groups=2)
+                       slots_per_layer=S, num_requests=B, dtype=torch.bfloat16, groups=ngroups,
+                       h2d_server=server)
     eng = DecodeEngine(cfg)
-    assert len(eng.groups) == 2
+    assert len(eng.groups) == ngroups and eng.server == server
     rng = synth.rng_for(2000, 9)
     hb = cfg.fwd_len
     host_np = synth.encode(synth.kv_blocks(rng, hb, D, synth.channel_scales(rng)), dt)
