@@ -108,7 +108,22 @@ def workload_cfg(args, world: int):
     assert wl.num_kv_heads % world == 0, "KV heads must divide across ranks"
     return dict(name=wl.name, batch=batch, layers=wl.layers, num_q_heads=wl.num_q_heads,
                 num_kv_heads=wl.num_kv_heads, n_blk=wl.n_blk, max_blk=wl.max_blk, topk=wl.topk,
-                slots=args.slots or wl.slots_per_layer, rho=wl.rho, context=wl.context)
+                slots=auto_slots(args, wl, batch, world) if args.slots < 0 and wl is synth.C2
+                else (args.slots if args.slots > 0 else wl.slots_per_layer), rho=wl.rho, context=wl.context)
+
+
+def auto_slots(args, wl, batch, world, reserve_gib=12):
+    """HBM cache slots per layer that fill the GPU's free memory after the
+    metadata, the key->slot table and a reserve for workspaces, temporaries and
+    graphs (B200: ~178 GiB usable).  Multiple of 4096, at most every block."""
+    hkv = wl.num_kv_heads // world
+    free, _ = torch.cuda.mem_get_info()
+    meta = wl.layers * batch * hkv * wl.max_blk * 2 * 128 * 2
+    fwd = batch * wl.layers * hkv * wl.max_blk * 4
+    per_slot = wl.layers * 2 * 32 * 128 * 2
+    s = (free - meta - fwd - (reserve_gib << 30)) // per_slot
+    s = min(s, batch * hkv * wl.n_blk)
+    return max(wl.slots_per_layer, int(s) // 4096 * 4096)
 
 
 def gen_host_blocks_on_gpu(engine, host_t, phys_blocks, seed, meta_phys, chunk_blocks=16384):
@@ -189,10 +204,14 @@ class StepTimers:
     """CUDA events around each op of each layer, recorded on the launching
     stream (each request group's own stream)."""
 
-    def __init__(self, external=False):
+    def __init__(self, external=False, only=None):
         self.ev = {"select": [], "cache": [], "gather": [], "attn": [], "allgather": []}
+        self.only = only          # time only these ops (None: all)
         self.trace = []          # (name, group, layer, start_event, end_event) in issue order
         self.external = external  # record nodes inside a captured CUDA graph
+
+    def wants(self, name):
+        return self.only is None or name in self.only
 
     def mark(self, name, group=0, layer=0):
         s = torch.cuda.Event(enable_timing=True, external=self.external)
@@ -382,7 +401,8 @@ def bench_ours(args):
     t_timed = args.settle + args.warmup
     t_e2e = t_timed + args.steps
     t_kt = t_e2e + e2e_steps
-    qs = gen_queries(eng, t_kt + n_kt + 1, W["rho"], seed=5000 + rank)
+    t_srv = t_kt + n_kt                               # server-only timing pass (h2d_server)
+    qs = gen_queries(eng, t_srv + n_kt + 1, W["rho"], seed=5000 + rank)
     gathered = None
     if world > 1:
         # one communicator per request group (their all-gathers run on different streams)
@@ -519,6 +539,21 @@ def bench_ours(args):
             with open(args.timeline, "w") as f:
                 json.dump(timers.timeline(timers.trace[0][3], len(timers.trace)), f)
         del tgraph
+        if eng.server:
+            # the FlashH2D server's launch timed in a graph that differs from the
+            # timed one by ONE event pair on the h2d stream (the per-op events
+            # above add ~600 record nodes, which stretch the step)
+            timers_s = StepTimers(external=True, only={"gather"})
+            sgraph = eng.capture_graph(q_static, post_attn=allgather_hook(), timers=timers_s)
+            srv_ms, srv_cnt = 0.0, torch.zeros(4, dtype=torch.int64, device="cuda")
+            for t in range(t_srv, t_srv + n_kt):
+                q_static.copy_(qs[t], non_blocking=True)
+                sgraph.replay()
+                counts_sum(srv_cnt)
+                torch.cuda.synchronize()
+                srv_ms += timers_s.totals_ms()["gather"]
+            del sgraph
+            srv_miss = int(srv_cnt[1])
     else:
         timers = StepTimers()
         k_s = torch.cuda.Event(True)
@@ -543,6 +578,11 @@ def bench_ours(args):
     miss_bytes_kt = k_miss * c.block_bytes
     sel_gbs = sel_bytes / (tot["select"] * 1e-3) / 1e9
     attn_gbs = attn_bytes / (tot["attn"] * 1e-3) / 1e9
+    if eng.server and graph is not None:
+        # one server launch per step: its own pass (above)
+        tot["gather"], nlaunch["gather"], miss_bytes_kt, k_miss_g = srv_ms, n_kt, srv_miss * c.block_bytes, srv_miss
+    else:
+        k_miss_g = k_miss
     h2d_gbs = miss_bytes_kt / (tot["gather"] * 1e-3) / 1e9 if tot["gather"] > 0 else 0.0
     kernels = {
         "ss_block_select": {"bound": "hbm", "achieved": round(sel_gbs, 1), "peak": hbm_peak,
@@ -587,7 +627,7 @@ def bench_ours(args):
     if os.path.exists(prof_t):
         tj = json.load(open(prof_t))
         if dom == "flash_h2d_gather" and "flash_h2d_pcie_read_bytes_per_miss" in tj:
-            traffic = int(tj["flash_h2d_pcie_read_bytes_per_miss"] * k_miss / max(1, nlaunch["gather"]))
+            traffic = int(tj["flash_h2d_pcie_read_bytes_per_miss"] * k_miss_g / max(1, nlaunch["gather"]))
         elif dom in tj.get("traffic_per_algorithmic_byte", {}):
             traffic = int(tj["traffic_per_algorithmic_byte"][dom] * dk["bytes_per_launch"])
     roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"], "peak": dk["peak"],
@@ -600,8 +640,8 @@ def bench_ours(args):
     # ---- each kernel alone (its own roofline fraction, no co-running group) ----
     if graph is not None:
         eng.advance_clock()
-    q_static.copy_(qs[t_kt + n_kt])
-    kernels_solo = solo_pass(eng, q_static, min(4, c.layers), hbm_peak, h2d_peak, stamp=t_kt + n_kt + 1)
+    q_static.copy_(qs[t_srv + n_kt])
+    kernels_solo = solo_pass(eng, q_static, min(4, c.layers), hbm_peak, h2d_peak, stamp=t_srv + n_kt + 1)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -703,12 +743,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--host-runs", type=int, default=251,
                     help="physical host KV pool = host_runs x max_blk blocks (251 -> 15.7 GiB)")
-    ap.add_argument("--settle", type=int, default=80,
+    ap.add_argument("--settle", type=int, default=300,
                     help="untimed decode steps before the W warm-up steps (cache steady state)")
     ap.add_argument("--config", default="C2", choices=["C2", "C3"],
                     help="workload: C2 (default, the metric's config) or C3 (GQA 1M-context stress)")
-    ap.add_argument("--slots", type=int, default=0,
-                    help="HBM cache slots per layer pool (0: the workload's default)")
+    ap.add_argument("--slots", type=int, default=-1,
+                    help="HBM cache slots per layer pool (-1: C2 fills the free HBM, C3 its 2x-demand "
+                         "stress size; 0: the workload's SURVEY size)")
     ap.add_argument("--hit-trace", action="store_true",
                     help="print each settle/warm-up step's hit rate and time to stderr")
     ap.add_argument("--cpu-req", type=int, default=2)

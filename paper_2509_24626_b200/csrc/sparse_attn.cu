@@ -41,7 +41,8 @@
 namespace ss {
 
 constexpr int kAttnPartStride = 132;
-constexpr int kMinUnitsPerWarp = 16;  // floats per (warp, seg, g) partial: m, l, pad, pad, o[128]
+// floats per (warp, seg, g) partial: m, l, pad, pad, o[128]
+constexpr int kMinUnitsPerWarp = 8;  // measured: C3 26.6 us at 8 vs 30.7 at 4 / 16, C2 unchanged
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -1005,8 +1006,8 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
     a.scale_log2 = scale * 1.4426950408889634f;
     const int G = d.num_q_heads / d.num_kv_heads;
     a.U = (int64_t)d.batch * d.num_kv_heads * (k + 1);
-    // at least kMinUnitsPerWarp units (256 KiB in bf16) per warp: fewer, longer
-    // ranges when the problem is small (C3: ~8 partials per pair to merge instead
+    // at least kMinUnitsPerWarp units (128 KiB in bf16) per warp: fewer, longer
+    // ranges when the problem is small (C3: ~16 partials per pair to merge instead
     // of ~28); W <= U keeps every range non-empty
     static const int min_units = getenv("SS_ATTN_MIN_UNITS") ? atoi(getenv("SS_ATTN_MIN_UNITS"))
                                                               : kMinUnitsPerWarp;

@@ -231,7 +231,7 @@ class DecodeEngine:
         c = self.cfg
 
         def timed(name, fn):
-            if timers is None:
+            if timers is None or not timers.wants(name):
                 fn()
             else:
                 s, e = timers.mark(name, gi, l)
@@ -333,12 +333,13 @@ class DecodeEngine:
         if self.server:
             hs = self.h2d_streams[0]
             with torch.cuda.stream(hs):
-                if timers is not None:
+                tm = timers is not None and timers.wants("gather")
+                if tm:
                     ts, te = timers.mark("gather", 0, 0)
                     ts.record()
                 ops.flash_h2d_serve(self.host_ptr, self.host_blocks, self.h2d_jobs, self.njobs,
                                     c.block_bytes, self.h2d_flags)
-                if timers is not None:
+                if tm:
                     te.record()
         # issue layer by layer, group by group: group A's FlashH2D (PCIe) overlaps
         # group B's select / attention (HBM) on the other stream
