@@ -72,6 +72,15 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_ready(self, n=3, timeout=10.0):
+        """Block until nvidia-smi has printed n samples: its start-up (NVML
+        init, heavier driver queries) must not land in the timed region
+        (measured: one ~12 ms stalled step when it did)."""
+        t0 = time.time()
+        while self.proc is not None and len(self.lines) < n and time.time() - t0 < timeout:
+            time.sleep(0.02)
+        self.first = len(self.lines)
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -81,7 +90,8 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # samples from the timed region on (the last pre-region one included)
+        for ln in self.lines[max(0, getattr(self, "first", 0) - 1):]:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -473,7 +483,7 @@ def bench_ours(args):
     # ---- timed region (value): inputs resident in HBM ----
     sampler = ClockSampler(local)
     sampler.start()
-    time.sleep(0.3)
+    sampler.wait_ready()
     barrier()
     start, end = torch.cuda.Event(True), torch.cuda.Event(True)
     cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
@@ -493,7 +503,8 @@ def bench_ours(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms = float(tt.item())
     ms_step = ms / args.steps
-    per_step = sorted(step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps))
+    raw_steps = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
+    per_step = sorted(raw_steps)
     n_hits, n_miss, n_evict, n_err = cnt.cpu().tolist()
     lookups = n_hits + n_miss
     hit_rate = n_hits / lookups if lookups else 0.0
@@ -672,6 +683,7 @@ def bench_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
             "step_ms_min_median_max": [round(per_step[0], 3), round(statistics.median(per_step), 3),
                                        round(per_step[-1], 3)],
+            "step_ms_argmax": int(max(range(args.steps), key=lambda i: raw_steps[i])),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": f"synthetic (seeded K~N(0,1)*lognormal channel scales, V~N(0,1), drifting q rho={W['rho']})",
             "config": {"workload": W["name"], "batch_per_gpu": W["batch"] // world, "global_batch": W["batch"],

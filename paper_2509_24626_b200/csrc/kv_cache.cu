@@ -16,7 +16,9 @@
 // and the new order is [eligible entries not evicted, in old order] ++ [all
 // slots with stamp == t, in slot order] -- two stable compactions.
 //
-// Three kernels per call (stream-ordered; chunk = 1024 order positions / slots):
+// Three phases per call (chunk = 1024 order positions / slots), run by ONE
+// persistent kernel with grid barriers between them (cache_fused_kernel,
+// default) or as three stream-ordered kernels (SS_CACHE_FUSED=0):
 //   K1 lookup+count : entry CTAs probe fwd, mark hits, rank misses per CTA;
 //                     chunk CTAs count stamp < t per order chunk and
 //                     stamp == t per slot chunk; hits correct both counts
@@ -32,6 +34,10 @@
 // On status != 0, K2 and K3 are no-ops: the pool is left byte-identical.
 //
 // Roofline: integer / latency bound; ~20 B per selection + ~30 B per slot.
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace ss {
@@ -170,12 +176,11 @@ __device__ void cache_plan(const CacheArgs& a, int* sw) {
     }
 }
 
-__global__ void __launch_bounds__(kCacheThreads) cache_lookup_count_kernel(CacheArgs a) {
-    __shared__ int sw[64];
-    const int64_t t = stamp_pre_plan(a);
-    if ((int)blockIdx.x < a.nA) {
+// Phase 1 work item (entry item < nA, else order/slot chunk item - nA).
+__device__ void p1_item(const CacheArgs& a, int item, int* sw, int64_t t) {
+    if (item < a.nA) {
         // ---- entry CTA: probe fwd, mark hits, rank misses ----
-        const int64_t e = (int64_t)blockIdx.x * kCacheThreads + threadIdx.x;
+        const int64_t e = (int64_t)item * kCacheThreads + threadIdx.x;
         int is_miss = 0, is_hit = 0;
         int ch_elig = -1, ch_teq = -1;  // chunks whose counters this hit moves
         if (e < a.E) {
@@ -220,13 +225,13 @@ __global__ void __launch_bounds__(kCacheThreads) cache_lookup_count_kernel(Cache
         if (e < a.E) a.ws.miss_local[e] = is_miss ? rank : -1;
         int hits = block_sum<kCacheThreads>(is_hit, sw);
         if (threadIdx.x == 0) {
-            a.ws.blk_miss[blockIdx.x] = tot;
-            a.ws.blk_hit[blockIdx.x] = hits;
+            a.ws.blk_miss[item] = tot;
+            a.ws.blk_hit[item] = hits;
         }
     } else {
         // ---- chunk CTA: stamp < t per order chunk, stamp == t per slot chunk ----
         const int S = a.pool.num_slots;
-        const int c = blockIdx.x - a.nA;
+        const int c = item - a.nA;
         const int p0 = c * kSlotChunk + threadIdx.x * kSlotPer;
         int lt = 0, eq = 0;
 #pragma unroll
@@ -244,6 +249,11 @@ __global__ void __launch_bounds__(kCacheThreads) cache_lookup_count_kernel(Cache
             if (eq) atomicAdd(&a.ws.teq_cnt[c], eq);
         }
     }
+}
+
+__global__ void __launch_bounds__(kCacheThreads) cache_lookup_count_kernel(CacheArgs a) {
+    __shared__ int sw[64];
+    p1_item(a, blockIdx.x, sw, stamp_pre_plan(a));
     // ---- last CTA plans ----
     __threadfence();
     __syncthreads();
@@ -258,13 +268,9 @@ __global__ void __launch_bounds__(kCacheThreads) cache_lookup_count_kernel(Cache
 // ----------------------------------------------------------------------------
 // K2: victims + kept prefix of the new order
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(kCacheThreads) cache_victim_kernel(CacheArgs a) {
-    __shared__ int sw[64];
-    if (a.ws.ctrl[2] != 0) return;
+__device__ void p2_item(const CacheArgs& a, int item, int* sw, int M, int64_t t) {
     const int S = a.pool.num_slots;
-    const int M = a.ws.ctrl[0];
-    const int64_t t = stamp_post_plan(a);
-    const int p0 = blockIdx.x * kSlotChunk + threadIdx.x * kSlotPer;
+    const int p0 = item * kSlotChunk + threadIdx.x * kSlotPer;
     int32_t sl[kSlotPer];
     bool el[kSlotPer];
     int c = 0;
@@ -272,11 +278,11 @@ __global__ void __launch_bounds__(kCacheThreads) cache_victim_kernel(CacheArgs a
     for (int i = 0; i < kSlotPer; ++i) {
         int p = p0 + i;
         sl[i] = p < S ? a.pool.order[p] : -1;
-        el[i] = p < S && !a.ws.touched[sl[i]] && a.pool.slot_stamp[sl[i]] < t;
+        el[i] = p < S && !__ldcg(a.ws.touched + sl[i]) && a.pool.slot_stamp[sl[i]] < t;
         c += el[i];
     }
     int tot;
-    int rank = a.ws.elig_off[blockIdx.x] + block_excl_scan<kCacheThreads>(c, sw, tot);
+    int rank = __ldcg(a.ws.elig_off + item) + block_excl_scan<kCacheThreads>(c, sw, tot);
     int ev = 0;
 #pragma unroll
     for (int i = 0; i < kSlotPer; ++i) {
@@ -300,25 +306,29 @@ __global__ void __launch_bounds__(kCacheThreads) cache_victim_kernel(CacheArgs a
     if (threadIdx.x == 0 && evs) atomicAdd(&a.ws.ctrl[4], evs);
 }
 
+__global__ void __launch_bounds__(kCacheThreads) cache_victim_kernel(CacheArgs a) {
+    __shared__ int sw[64];
+    if (a.ws.ctrl[2] != 0) return;
+    p2_item(a, blockIdx.x, sw, a.ws.ctrl[0], stamp_post_plan(a));
+}
+
 // ----------------------------------------------------------------------------
 // K3: assign misses / stamp hits (entry CTAs) || place stamp==t slots (chunk CTAs)
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(kCacheThreads) cache_assign_place_kernel(CacheArgs a) {
-    __shared__ int sw[64];
-    __shared__ int s_base;
-    const bool ok = a.ws.ctrl[2] == 0;
-    const int64_t t = stamp_post_plan(a);
+__device__ void p3_item(const CacheArgs& a, int item, int* sw, int* s_base_p, bool ok, int kept,
+                        int evictions, int64_t t) {
+    int& s_base = *s_base_p;
     const int S = a.pool.num_slots;
-    if ((int)blockIdx.x < a.nA) {
-        const int64_t e = (int64_t)blockIdx.x * kCacheThreads + threadIdx.x;
+    if (item < a.nA) {
+        const int64_t e = (int64_t)item * kCacheThreads + threadIdx.x;
         if (ok && e < a.E) {
-            if (a.hit_out[e]) {
-                a.pool.slot_stamp[a.slot_out[e]] = t;
+            if (__ldcg(a.hit_out + e)) {
+                a.pool.slot_stamp[__ldcg(a.slot_out + e)] = t;
             } else {
-                const int ml = a.ws.miss_local[e];
+                const int ml = __ldcg(a.ws.miss_local + e);
                 if (ml >= 0) {
-                    const int i = a.ws.blk_off[blockIdx.x] + ml;
-                    const int32_t s = a.ws.vict[i];
+                    const int i = __ldcg(a.ws.blk_off + item) + ml;
+                    const int32_t s = __ldcg(a.ws.vict + i);
                     const int64_t key = cache_key(a, e, a.sel[e]);
                     a.slot_out[e] = s;
                     a.miss_keys[i] = key;
@@ -331,12 +341,11 @@ __global__ void __launch_bounds__(kCacheThreads) cache_assign_place_kernel(Cache
         }
     } else {
         // chunk CTA c: slots [c*1024, (c+1)*1024) in slot order
-        const int c = blockIdx.x - a.nA;
-        const int kept = a.ws.ctrl[5];
-        if (ok && c == 0 && threadIdx.x == 0) a.counts[2] = a.ws.ctrl[4];
+        const int c = item - a.nA;
+        if (ok && c == 0 && threadIdx.x == 0) a.counts[2] = evictions;
         if (threadIdx.x < 32) {
             int acc = 0;
-            for (int cc = threadIdx.x; cc < c; cc += 32) acc += a.ws.teq_cnt[cc];
+            for (int cc = threadIdx.x; cc < c; cc += 32) acc += __ldcg(a.ws.teq_cnt + cc);
             acc = warp_sum(acc);
             if (threadIdx.x == 0) s_base = kept + acc;
         }
@@ -349,7 +358,7 @@ __global__ void __launch_bounds__(kCacheThreads) cache_assign_place_kernel(Cache
             // stamp == t after this call: hit, victim, or already stamped t (a
             // concurrent K3 entry CTA may be writing t into hit / victim slots;
             // their flags already decide those)
-            f[i] = ok && s < S && (a.ws.touched[s] || a.ws.victim[s] || a.pool.slot_stamp[s] == t);
+            f[i] = ok && s < S && (__ldcg(a.ws.touched + s) || __ldcg(a.ws.victim + s) || a.pool.slot_stamp[s] == t);
             n += f[i];
             // this chunk's per-call flags go back to zero (K1 set touched even
             // when the call fails)
@@ -359,7 +368,7 @@ __global__ void __launch_bounds__(kCacheThreads) cache_assign_place_kernel(Cache
             }
             // copy the kept prefix of the new order (K2) into order / order_pos
             if (ok && s < kept) {
-                const int32_t v = a.ws.new_order[s];
+                const int32_t v = __ldcg(a.ws.new_order + s);
                 a.pool.order[s] = v;
                 a.pool.order_pos[v] = s;
             }
@@ -375,17 +384,90 @@ __global__ void __launch_bounds__(kCacheThreads) cache_assign_place_kernel(Cache
                 a.pool.order_pos[s0 + i] = pos;
                 ++pos;
             }
+        __syncthreads();  // s_base is reused by the CTA's next item
     }
-    // the last K3 CTA (every CTA has read ctrl / teq_cnt by now) zeroes the
-    // call-wide words, leaving the workspace ready for the next call
+}
+
+// the last CTA of the final phase (every CTA has read ctrl / teq_cnt by now)
+// zeroes the call-wide words, leaving the workspace ready for the next call
+__device__ void cache_cleanup(const CacheArgs& a, int* sw, int ticket_idx, int nctas) {
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) sw[48] = atomicAdd(&a.ws.ctrl[10], 1);
+    if (threadIdx.x == 0) sw[48] = atomicAdd(&a.ws.ctrl[ticket_idx], 1);
     __syncthreads();
-    if (sw[48] != (int)gridDim.x - 1) return;
+    if (sw[48] != nctas - 1) return;
     __threadfence();
     for (int c = threadIdx.x; c < a.nS; c += kCacheThreads) a.ws.teq_cnt[c] = 0;
+    __syncthreads();
     if (threadIdx.x < 16) a.ws.ctrl[threadIdx.x] = 0;
+}
+
+__global__ void __launch_bounds__(kCacheThreads) cache_assign_place_kernel(CacheArgs a) {
+    __shared__ int sw[64];
+    __shared__ int s_base;
+    p3_item(a, blockIdx.x, sw, &s_base, a.ws.ctrl[2] == 0, a.ws.ctrl[5], a.ws.ctrl[4], stamp_post_plan(a));
+    cache_cleanup(a, sw, 10, gridDim.x);
+}
+// ----------------------------------------------------------------------------
+// Fused form (default): the three phases in ONE launch of a small persistent
+// grid with two software grid barriers (plan by CTA 0 between them).  Inside a
+// decode step the three separate kernels each queue for SM slots behind the
+// other request groups' long select / attention CTAs; the fused call queues
+// once.  Every cross-phase read goes through L2 (__ldcg).  The grid (<= 128
+// CTAs of 256 threads, 8 K registers each) is far below what the 148 SMs hold,
+// so every CTA becomes resident once co-running kernels release slots.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void grid_barrier(int32_t* count, int32_t* gen, int n) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int g;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+        __threadfence();
+        if (atomicAdd(count, 1) == n - 1) {
+            atomicExch(count, 0);
+            __threadfence();
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
+        } else {
+            int v = g;
+            while (v == g) {
+                __nanosleep(32);
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(gen) : "memory");
+            }
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kCacheThreads) cache_fused_kernel(CacheArgs a) {
+    __shared__ int sw[64];
+    __shared__ int s_base;
+    // the clock advances only between decode steps: one read serves all phases
+    const int64_t t = stamp_pre_plan(a);
+    const int n1 = a.nA + a.nS;
+    int32_t* bar_count = a.ws.ctrl + 11;
+    int32_t* bar_gen = a.ws.ctrl + 12;
+    for (int it = blockIdx.x; it < n1; it += gridDim.x) {
+        p1_item(a, it, sw, t);
+        __syncthreads();
+    }
+    grid_barrier(bar_count, bar_gen, gridDim.x);
+    if (blockIdx.x == 0) cache_plan(a, sw);
+    grid_barrier(bar_count, bar_gen, gridDim.x);
+    const int status = __ldcg(a.ws.ctrl + 2);
+    const int M = __ldcg(a.ws.ctrl + 0);
+    const int kept = __ldcg(a.ws.ctrl + 5);
+    if (status == 0)
+        for (int it = blockIdx.x; it < a.nS; it += gridDim.x) {
+            p2_item(a, it, sw, M, t);
+            __syncthreads();
+        }
+    grid_barrier(bar_count, bar_gen, gridDim.x);
+    const int evictions = __ldcg(a.ws.ctrl + 4);
+    for (int it = blockIdx.x; it < n1; it += gridDim.x) {
+        p3_item(a, it, sw, &s_base, status == 0, kept, evictions, t);
+        __syncthreads();
+    }
+    cache_cleanup(a, sw, 10, gridDim.x);
 }
 
 ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int32_t* req_ids,
@@ -412,16 +494,24 @@ ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int3
     carve(&a.ws, ws, a.E, S);
     a.nA = (int)((a.E + kCacheThreads - 1) / kCacheThreads);
     a.nS = (S + kSlotChunk - 1) / kSlotChunk;
-    cache_lookup_count_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
-    cache_victim_kernel<<<a.nS, kCacheThreads, 0, stream>>>(a);
-    cache_assign_place_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
+    // SS_CACHE_FUSED=0 selects the three-kernel form (A/B; same results)
+    static const int fused = getenv("SS_CACHE_FUSED") ? atoi(getenv("SS_CACHE_FUSED")) : 1;
+    static const int fused_ctas = getenv("SS_CACHE_CTAS") ? atoi(getenv("SS_CACHE_CTAS")) : 128;
+    if (fused) {
+        const int grid = std::max(1, std::min(a.nA + a.nS, std::min(fused_ctas, kNumSMs)));
+        cache_fused_kernel<<<grid, kCacheThreads, 0, stream>>>(a);
+    } else {
+        cache_lookup_count_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
+        cache_victim_kernel<<<a.nS, kCacheThreads, 0, stream>>>(a);
+        cache_assign_place_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
+    }
     SS_LAUNCH_CHECK();
     return SS_OK;
 }
 
 bool preload_cache() {
     return preload_fn(cache_lookup_count_kernel) && preload_fn(cache_victim_kernel) &&
-           preload_fn(cache_assign_place_kernel);
+           preload_fn(cache_assign_place_kernel) && preload_fn(cache_fused_kernel);
 }
 
 }  // namespace ss
