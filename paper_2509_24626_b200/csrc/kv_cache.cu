@@ -16,9 +16,9 @@
 // and the new order is [eligible entries not evicted, in old order] ++ [all
 // slots with stamp == t, in slot order] -- two stable compactions.
 //
-// Three phases per call (chunk = 1024 order positions / slots), run by ONE
-// persistent kernel with grid barriers between them (cache_fused_kernel,
-// default) or as three stream-ordered kernels (SS_CACHE_FUSED=0):
+// Three phases per call (chunk = 1024 order positions / slots), run as three
+// stream-ordered kernels (default) or by ONE persistent kernel with grid
+// barriers between them (cache_fused_kernel, SS_CACHE_FUSED=1; measured slower):
 //   K1 lookup+count : entry CTAs probe fwd, mark hits, rank misses per CTA;
 //                     chunk CTAs count stamp < t per order chunk and
 //                     stamp == t per slot chunk; hits correct both counts
@@ -251,8 +251,19 @@ __device__ void p1_item(const CacheArgs& a, int item, int* sw, int64_t t) {
     }
 }
 
+// Programmatic dependent launch (PDL) between the three kernels: K1 lets K2's
+// CTAs launch at once (they take their SM slots while K1 runs and block in
+// griddepcontrol.wait until K1 has completed and its writes are visible), and
+// K2 does the same for K3 -- inside a decode step the next kernel no longer
+// queues for slots behind other request groups' long select / attention CTAs.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __global__ void __launch_bounds__(kCacheThreads) cache_lookup_count_kernel(CacheArgs a) {
     __shared__ int sw[64];
+    pdl_launch_dependents();
     p1_item(a, blockIdx.x, sw, stamp_pre_plan(a));
     // ---- last CTA plans ----
     __threadfence();
@@ -308,6 +319,8 @@ __device__ void p2_item(const CacheArgs& a, int item, int* sw, int M, int64_t t)
 
 __global__ void __launch_bounds__(kCacheThreads) cache_victim_kernel(CacheArgs a) {
     __shared__ int sw[64];
+    pdl_wait();
+    pdl_launch_dependents();
     if (a.ws.ctrl[2] != 0) return;
     p2_item(a, blockIdx.x, sw, a.ws.ctrl[0], stamp_post_plan(a));
 }
@@ -405,11 +418,12 @@ __device__ void cache_cleanup(const CacheArgs& a, int* sw, int ticket_idx, int n
 __global__ void __launch_bounds__(kCacheThreads) cache_assign_place_kernel(CacheArgs a) {
     __shared__ int sw[64];
     __shared__ int s_base;
+    pdl_wait();
     p3_item(a, blockIdx.x, sw, &s_base, a.ws.ctrl[2] == 0, a.ws.ctrl[5], a.ws.ctrl[4], stamp_post_plan(a));
     cache_cleanup(a, sw, 10, gridDim.x);
 }
 // ----------------------------------------------------------------------------
-// Fused form (default): the three phases in ONE launch of a small persistent
+// Fused form (SS_CACHE_FUSED=1): the three phases in ONE launch of a small persistent
 // grid with two software grid barriers (plan by CTA 0 between them).  Inside a
 // decode step the three separate kernels each queue for SM slots behind the
 // other request groups' long select / attention CTAs; the fused call queues
@@ -494,16 +508,33 @@ ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int3
     carve(&a.ws, ws, a.E, S);
     a.nA = (int)((a.E + kCacheThreads - 1) / kCacheThreads);
     a.nS = (S + kSlotChunk - 1) / kSlotChunk;
-    // SS_CACHE_FUSED=0 selects the three-kernel form (A/B; same results)
-    static const int fused = getenv("SS_CACHE_FUSED") ? atoi(getenv("SS_CACHE_FUSED")) : 1;
+    // three kernels (default) or the fused form (SS_CACHE_FUSED=1; same results).
+    // Measured in the C2 step: fused 54.8 us alone / 76 us in-step vs 38.7 / 56.6
+    // for three kernels -- the 128-CTA grid serialises items per CTA and its
+    // barriers cost more than two kernel boundaries (profiles/r01s3_cache_fused_ab.txt)
+    static const int fused = getenv("SS_CACHE_FUSED") ? atoi(getenv("SS_CACHE_FUSED")) : 0;
     static const int fused_ctas = getenv("SS_CACHE_CTAS") ? atoi(getenv("SS_CACHE_CTAS")) : 128;
     if (fused) {
         const int grid = std::max(1, std::min(a.nA + a.nS, std::min(fused_ctas, kNumSMs)));
         cache_fused_kernel<<<grid, kCacheThreads, 0, stream>>>(a);
     } else {
         cache_lookup_count_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
-        cache_victim_kernel<<<a.nS, kCacheThreads, 0, stream>>>(a);
-        cache_assign_place_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
+        // K2, K3: programmatic dependent launches (SS_CACHE_PDL=0: plain launches;
+        // griddepcontrol.wait is then a no-op)
+        static const int pdl = getenv("SS_CACHE_PDL") ? atoi(getenv("SS_CACHE_PDL")) : 1;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchConfig_t lc = {};
+        lc.blockDim = dim3(kCacheThreads);
+        lc.dynamicSmemBytes = 0;
+        lc.stream = stream;
+        lc.attrs = attr;
+        lc.numAttrs = pdl ? 1 : 0;
+        lc.gridDim = dim3(a.nS);
+        if (cudaLaunchKernelEx(&lc, cache_victim_kernel, a) != cudaSuccess) return SS_ERR_CUDA;
+        lc.gridDim = dim3(a.nA + a.nS);
+        if (cudaLaunchKernelEx(&lc, cache_assign_place_kernel, a) != cudaSuccess) return SS_ERR_CUDA;
     }
     SS_LAUNCH_CHECK();
     return SS_OK;

@@ -33,15 +33,24 @@ def test_fullsize_layer17_three_steps(name):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     wl, runs, need_gb = {"C2": (synth.C2, 13, 110), "C3": (synth.C3, 2, 30)}[name]
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if free < need_gb * (1 << 30):
         pytest.skip(f"needs ~{need_gb} GB of free HBM")
     from paper_2509_24626_b200.engine import DecodeEngine, EngineConfig
+    import bench
+    # the launch configuration bench.py times: 3 request groups on streams, the
+    # FlashH2D server, steps after the first replayed from one captured CUDA
+    # graph with device-clock stamps, and (C2) the HBM-filling cache size
+    slots = bench.auto_slots(None, wl, wl.batch, 1) if name == "C2" else wl.slots_per_layer
     cfg = EngineConfig(batch=wl.batch, layers=wl.layers, num_q_heads=wl.num_q_heads,
                        num_kv_heads=wl.num_kv_heads, max_blk=wl.max_blk, topk=wl.topk,
-                       slots_per_layer=wl.slots_per_layer, num_requests=wl.batch,
-                       dtype=torch.bfloat16, groups=2)
+                       slots_per_layer=slots, num_requests=wl.batch,
+                       dtype=torch.bfloat16, groups=3, h2d_server=True)
     eng = DecodeEngine(cfg)
+    assert eng.server and len(eng.groups) == 3
     hb = runs * cfg.max_blk                             # physical host pool (C2 832 MiB, C3 1 GiB)
     rng = synth.rng_for(8000, 1)
     scales = synth.channel_scales(rng)
@@ -73,8 +82,17 @@ def test_fullsize_layer17_three_steps(name):
     host_u8 = host_np.view(np.uint8).reshape(hb, -1)
     tails = np.zeros((cfg.batch, cfg.num_kv_heads, 2, 32, D), np.uint16)
     tl = np.zeros(cfg.batch, np.int32)
+    graph, q_static = None, None
     for t in range(STEPS):
-        eng.step(to_torch(qs[t]), stamp=t + 1)
+        if t == 1:
+            eng.use_device_clock(start=1)
+            q_static = torch.empty_like(to_torch(qs[0]))
+            graph = eng.capture_graph(q_static)
+        if graph is None:
+            eng.step(to_torch(qs[t]), stamp=t + 1)
+        else:
+            q_static.copy_(to_torch(qs[t]))
+            graph.replay()
         torch.cuda.synchronize()
         for l in CHECK_LAYERS:
             for g in eng.groups:

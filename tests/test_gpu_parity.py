@@ -406,18 +406,18 @@ def test_cache_device_clock_mode(ops):
         assert int(gp.clock.item()) == t + 1
 
 
-def test_cache_three_kernel_form_bit_exact(ops):
-    """The three-kernel form of kv_cache_lookup_insert (SS_CACHE_FUSED=0, read
-    once per process) against the oracle: the cache parity tests and a
-    two-group pipeline re-run in a subprocess."""
+def test_cache_fused_form_bit_exact(ops):
+    """The fused one-launch form of kv_cache_lookup_insert (SS_CACHE_FUSED=1,
+    read once per process) against the oracle: the cache parity tests and the
+    request-group pipelines re-run in a subprocess."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SS_CACHE_FUSED="0")
+    env = dict(os.environ, SS_CACHE_FUSED="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(root, "tests", "test_gpu_parity.py"),
                         os.path.join(root, "tests", "test_gpu_pipeline.py"),
-                        "-k", "(cache or request_groups) and not three_kernel"],
+                        "-k", "(cache or request_groups) and not fused_form"],
                        env=env, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
