@@ -251,7 +251,7 @@ __device__ void p1_item(const CacheArgs& a, int item, int* sw, int64_t t) {
     }
 }
 
-// Programmatic dependent launch (PDL) between the three kernels: K1 lets K2's
+// Programmatic dependent launch (PDL, SS_CACHE_PDL=1) between the three kernels: K1 lets K2's
 // CTAs launch at once (they take their SM slots while K1 runs and block in
 // griddepcontrol.wait until K1 has completed and its writes are visible), and
 // K2 does the same for K3 -- inside a decode step the next kernel no longer
@@ -519,9 +519,12 @@ ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int3
         cache_fused_kernel<<<grid, kCacheThreads, 0, stream>>>(a);
     } else {
         cache_lookup_count_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
-        // K2, K3: programmatic dependent launches (SS_CACHE_PDL=0: plain launches;
-        // griddepcontrol.wait is then a no-op)
-        static const int pdl = getenv("SS_CACHE_PDL") ? atoi(getenv("SS_CACHE_PDL")) : 1;
+        // K2, K3: plain launches (default) or programmatic dependent launches
+        // (SS_CACHE_PDL=1; griddepcontrol.wait is a no-op without).  Measured in
+        // the C2 step: PDL makes the call faster (34 vs 39 us alone, 52 vs 57 in
+        // the step) but the step slower (11.85 vs 11.0 ms median): the early-
+        // resident K2/K3 CTAs take SM slots from the other groups' select.
+        static const int pdl = getenv("SS_CACHE_PDL") ? atoi(getenv("SS_CACHE_PDL")) : 0;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
