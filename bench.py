@@ -167,7 +167,8 @@ def setup_engine(args, rank: int, world: int):
                        max_blk=W["max_blk"], topk=W["topk"], slots_per_layer=W["slots"],
                        num_requests=W["batch"], dtype=torch.bfloat16, groups=args.groups,
                        h2d_streams=args.h2d_streams, select_priority=args.select_priority,
-                       cache_per_group=args.cache_per_group, h2d_server=bool(args.h2d_server))
+                       cache_per_group=args.cache_per_group, h2d_server=bool(args.h2d_server),
+                       split_attn=bool(args.split_attn))
     eng = DecodeEngine(cfg)
     # physical host pool: a prime number of max_blk runs (aliasing, R15)
     runs = args.host_runs if cfg.max_blk <= 4096 else max(1, (args.host_runs * 4096) // cfg.max_blk)
@@ -218,7 +219,7 @@ class StepTimers:
     stream (each request group's own stream)."""
 
     def __init__(self, external=False, only=None):
-        self.ev = {"select": [], "cache": [], "gather": [], "attn": [], "allgather": []}
+        self.ev = {"select": [], "cache": [], "gather": [], "attn": [], "attn_miss": [], "allgather": []}
         self.only = only          # time only these ops (None: all)
         self.trace = []          # (name, group, layer, start_event, end_event) in issue order
         self.external = external  # record nodes inside a captured CUDA graph
@@ -613,7 +614,8 @@ def bench_ours(args):
     attn_bytes = (k_hits + k_miss) * c.block_bytes + c.num_q_heads * c.batch * 128 * 4 * c.layers * n_kt
     miss_bytes_kt = k_miss * c.block_bytes
     sel_gbs = sel_bytes / (tot["select"] * 1e-3) / 1e9
-    attn_gbs = attn_bytes / (tot["attn"] * 1e-3) / 1e9
+    attn_ms = tot["attn"] + tot.get("attn_miss", 0.0)     # split form: hit part + miss part & merge
+    attn_gbs = attn_bytes / (attn_ms * 1e-3) / 1e9
     if eng.server and graph is not None:
         # one server launch per step: its own pass (above)
         tot["gather"], nlaunch["gather"], miss_bytes_kt, k_miss_g = srv_ms, n_kt, srv_miss * c.block_bytes, srv_miss
@@ -627,7 +629,8 @@ def bench_ours(args):
                              "bytes_per_launch": int(sel_bytes / n_sel)},
         "sparse_decode_attn": {"bound": "hbm", "achieved": round(attn_gbs, 1), "peak": hbm_peak,
                                 "unit": "GB/s", "frac": round(attn_gbs / hbm_peak, 4),
-                                "us_per_launch": round(tot["attn"] * 1e3 / max(1, nlaunch["attn"]), 2),
+                                "us_per_launch": round(attn_ms * 1e3 / max(1, nlaunch["attn"]), 2),
+                                "split": bool(getattr(eng.cfg, "split_attn", False) and eng.server),
                                 "bytes_per_launch": int(attn_bytes / max(1, nlaunch["attn"]))},
         "flash_h2d_gather": {"bound": "host-link", "achieved": round(h2d_gbs, 2),
                               "peak": round(h2d_peak, 2), "unit": "GB/s",
@@ -702,7 +705,7 @@ def bench_ours(args):
                        "topk_blocks": c.topk, "hbm_cache_slots_per_layer": c.slots_per_layer,
                        "host_pool_blocks": eng.host_blocks, "host_kv": "pinned DRAM, zero-copy (UVA)",
                        "parallelism": f"kv-heads/{world} per GPU" if world > 1 else "1 GPU",
-                       "request_groups": len(eng.groups), "h2d_server": eng.server, "h2d_streams": args.h2d_streams, "select_priority": args.select_priority, "cache_per_group": args.cache_per_group,
+                       "request_groups": len(eng.groups), "h2d_server": eng.server, "split_attn": bool(eng.server and eng.cfg.split_attn), "h2d_streams": args.h2d_streams, "select_priority": args.select_priority, "cache_per_group": args.cache_per_group,
                        "cuda_graph": graph is not None,
                        "cache_settle_steps": args.settle,
                        "l2": f"no flush needed: inputs larger than L2 ({meta_gib:.0f} GiB metadata streamed per step)",
@@ -718,7 +721,8 @@ def bench_ours(args):
                           "h2d_gbs_over_step": round(n_miss * c.block_bytes / (ms * 1e-3) / 1e9, 2)},
             "roofline": roofline, "kernels": kernels, "kernels_solo": kernels_solo,
             "cold_step_ms": round(cold_ms, 2) if cold_ms else None,
-            "e2e": e2e, "gpu_launches": int(args.steps * (c.layers * 6 * len(eng.groups) + (1 if eng.server else 0))),
+            "e2e": e2e, "gpu_launches": int(args.steps * (c.layers * (8 if eng.server and eng.cfg.split_attn else 6) * len(eng.groups)
+                                                 + (1 if eng.server else 0))),
             "cpu_baseline": cpu, "clocks": clocks, "setup_s": round(setup_s, 1),
             "errors_in_timed_region": n_err,
         }
@@ -808,6 +812,9 @@ def main():
                     help="1: the step's FlashH2D gathers are served by one persistent launch "
                          "(flash_h2d_serve); 0: one flash_h2d_gather launch per layer and group "
                          "(use 0 under ncu, which serialises kernels)")
+    ap.add_argument("--split-attn", type=int, default=1,
+                    help="1 (with the server): attend each group's cache hits while FlashH2D loads its "
+                         "misses, then the misses, then a log-sum-exp merge; 0: one attention after the gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gather-alone", action="store_true",
                     help="skip the FlashH2D-alone ceiling measurement (profiling runs: keeps launch counts fixed)")

@@ -271,6 +271,34 @@ ss_status sparse_decode_attn(const void* q, const void* pool_kv, const int32_t* 
                              ss_dtype dt, float softmax_scale, const int32_t* counts,
                              float* out, void* ws, size_t ws_bytes, void* stream);
 
+/* S5, split form -- the same attention over a SUBSET of the token set, plus
+ * its log-sum-exp, so the part over the cache hits can run while FlashH2D
+ * still loads the misses.  Softmax over disjoint token sets
+ * combines exactly by log-sum-exp (PAPER.md:71-72 restated per subset):
+ *   O = (O_a 2^lse_a + O_b 2^lse_b) / (2^lse_a + 2^lse_b).
+ *   hit    device uint8 [B][Hkv][k] (hit_out of S3); required for mode 1/2.
+ *   mode   0: every selected block + tail (= sparse_decode_attn)
+ *          1: blocks with hit != 0 + tail    2: blocks with hit == 0 only.
+ *   out    device float32 [Hq][B][d]: the subset's normalised output (0 if
+ *          the subset is empty).
+ *   lse    device float32 [Hq][B]: log2-domain log-sum-exp of the subset's
+ *          scaled logits (z * log2(e) with z = q.k * softmax_scale): m + log2(l);
+ *          -inf for an empty subset.
+ *   Other arguments as sparse_decode_attn (same workspace size). */
+ss_status sparse_decode_attn_part(const void* q, const void* pool_kv, const int32_t* slot,
+                                  const uint8_t* hit, int32_t mode, int32_t k, const void* tail_kv,
+                                  const int32_t* tail_len, ss_dims dims, ss_dtype dt,
+                                  float softmax_scale, const int32_t* counts, float* out, float* lse,
+                                  void* ws, size_t ws_bytes, void* stream);
+
+/* Merge two split-form results over disjoint token sets (rows = Hq * B rows of
+ * d = 128 floats): out = (out_a 2^lse_a + out_b 2^lse_b) / (2^lse_a + 2^lse_b),
+ * 0 when both are empty.  out may alias out_a or out_b.  No-op if counts is
+ * non-null and counts[3] != 0 (as the attention calls). */
+ss_status sparse_attn_merge(const float* out_a, const float* lse_a, const float* out_b,
+                            const float* lse_b, int64_t rows, const int32_t* counts, float* out,
+                            void* stream);
+
 /* ---------------------------------------------------------------------------
  * NEXT-1: decode KV append + save path (PAPER.md:151-153 §3.2.2, :125).
  * Per decode step: kv_append for every layer (advance = 1 on the first layer

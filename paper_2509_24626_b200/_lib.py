@@ -21,7 +21,8 @@ EXPORTS = ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert", "fl
            "ss_status_string", "ss_version", "kv_append", "kv_seal_blocks", "kv_commit",
            "ss_d2h_create", "ss_d2h_destroy", "flash_d2h_save", "ws_track", "ss_admit", "prefill_layer_save",
            "block_meta_update_mean", "ss_block_select_mean", "flash_h2d_serve", "ss_flag_signal",
-           "ss_flag_wait", "ss_preload_kernels")
+           "ss_flag_wait", "ss_preload_kernels",
+           "sparse_decode_attn_part", "sparse_attn_merge")
 
 
 class SSDims(ctypes.Structure):
@@ -71,6 +72,8 @@ def load() -> ctypes.CDLL:
     L.ss_flag_signal.argtypes = [P, P]
     L.ss_flag_wait.argtypes = [P, P]
     L.ss_preload_kernels.argtypes = []
+    L.sparse_decode_attn_part.argtypes = [P, P, P, P, I32, I32, P, P, SSDims, I32, F, P, P, P, P, SZ, P]
+    L.sparse_attn_merge.argtypes = [P, P, P, P, I64, P, P, P]
     L.sparse_decode_attn.argtypes = [P, P, P, I32, P, P, SSDims, I32, F, P, P, P, SZ, P]
     L.ss_workspace_size.argtypes = [I32, SSDims, I32, I32, I32]
     L.ss_workspace_size.restype = SZ
@@ -95,7 +98,8 @@ def load() -> ctypes.CDLL:
                  "flash_h2d_gather", "sparse_decode_attn", "ss_host_device_pointer", "kv_append",
                  "kv_seal_blocks", "kv_commit", "ss_d2h_create", "ss_d2h_destroy",
                  "flash_d2h_save", "block_meta_update_mean", "ss_block_select_mean", "flash_h2d_serve",
-                 "ss_flag_signal", "ss_flag_wait", "ss_preload_kernels"):
+                 "ss_flag_signal", "ss_flag_wait", "ss_preload_kernels",
+           "sparse_decode_attn_part", "sparse_attn_merge"):
         getattr(L, name).restype = I32
     _lib = L
     return L

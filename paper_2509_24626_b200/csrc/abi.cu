@@ -28,7 +28,10 @@ ss_status launch_flag_wait(const int32_t* flag, cudaStream_t stream);
 ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* slot, int k,
                              const void* tail_kv, const int32_t* tail_len, const ss_dims& d,
                              ss_dtype dt, float scale, const int32_t* counts, float* out, void* ws,
-                             cudaStream_t stream);
+                             cudaStream_t stream, const uint8_t* hit = nullptr, int mode = 0,
+                             float* lse = nullptr);
+ss_status launch_attn_merge(const float* oa, const float* la, const float* ob, const float* lb,
+                            int64_t rows, const int32_t* counts, float* out, cudaStream_t stream);
 size_t attn_ws_bytes(const ss_dims& d, int k, ss_dtype dt);
 ss_status launch_kv_append(const void* new_kv, void* tail_kv, int32_t* tail_len, int advance,
                            const ss_dims& d, ss_dtype dt, cudaStream_t stream);
@@ -201,6 +204,34 @@ ss_status sparse_decode_attn(const void* q, const void* pool_kv, const int32_t* 
     if (!ws || ws_bytes < need) return SS_ERR_INVALID_ARG;
     return ss::launch_sparse_attn(q, pool_kv, slot, k, tail_kv, tail_len, dims, dt, softmax_scale,
                                   counts, out, ws, (cudaStream_t)stream);
+}
+
+ss_status sparse_decode_attn_part(const void* q, const void* pool_kv, const int32_t* slot,
+                                  const uint8_t* hit, int32_t mode, int32_t k, const void* tail_kv,
+                                  const int32_t* tail_len, ss_dims dims, ss_dtype dt,
+                                  float softmax_scale, const int32_t* counts, float* out, float* lse,
+                                  void* ws, size_t ws_bytes, void* stream) {
+    if (!q || !pool_kv || !slot || !tail_kv || !tail_len || !out || !lse || !dt_ok(dt) || !dims_ok(dims))
+        return SS_ERR_INVALID_ARG;
+    if (mode < 0 || mode > 2 || (mode != 0 && !hit) || k < 1) return SS_ERR_INVALID_ARG;
+    if (!aligned16(q) || !aligned16(pool_kv) || !aligned16(tail_kv) || !aligned16(out))
+        return SS_ERR_INVALID_ARG;
+    ss_status st = dims_supported(dims);
+    if (st != SS_OK) return st;
+    size_t need = ss::attn_ws_bytes(dims, k, dt);
+    if (!ws || ws_bytes < need) return SS_ERR_INVALID_ARG;
+    return ss::launch_sparse_attn(q, pool_kv, slot, k, tail_kv, tail_len, dims, dt, softmax_scale,
+                                  counts, out, ws, (cudaStream_t)stream, hit, mode, lse);
+}
+
+ss_status sparse_attn_merge(const float* out_a, const float* lse_a, const float* out_b,
+                            const float* lse_b, int64_t rows, const int32_t* counts, float* out,
+                            void* stream) {
+    if (rows < 0) return SS_ERR_INVALID_ARG;
+    if (rows == 0) return SS_OK;
+    if (!out_a || !lse_a || !out_b || !lse_b || !out) return SS_ERR_INVALID_ARG;
+    if (!aligned16(out_a) || !aligned16(out_b) || !aligned16(out)) return SS_ERR_INVALID_ARG;
+    return ss::launch_attn_merge(out_a, lse_a, out_b, lse_b, rows, counts, out, (cudaStream_t)stream);
 }
 
 ss_status kv_append(const void* new_kv, void* tail_kv, int32_t* tail_len, int32_t advance,

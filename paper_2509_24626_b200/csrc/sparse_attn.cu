@@ -87,6 +87,12 @@ struct AttnArgs {
     int32_t* tickets;
     int k, B, Hq, Hkv;
     float scale_log2;
+    // split form (sparse_decode_attn_part): mode 0 = every selected block + tail,
+    // 1 = hit blocks (hit[] != 0) + tail, 2 = missed blocks only; lse (or null)
+    // receives log2-domain log-sum-exp per (hq, b): m + log2(l), -inf if empty
+    const uint8_t* hit;
+    int mode;
+    float* lse;
     int64_t U;  // pairs * (k + 1)
     int W;      // total warps
     unsigned long long* trace;  // debug (SS_ATTN_TRACE=1): per warp globaltimer at entry / last unit / exit / merge start / merge end
@@ -240,6 +246,8 @@ __device__ __forceinline__ void finish_partial(const AttnArgs& a, int64_t p, int
             const float lsum = warp_sum(lt[g]);
             const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
             const int hq = h * G + g0 + g;
+            if (a.lse != nullptr && lane == 0)
+                a.lse[(int64_t)hq * a.B + b] = lsum > 0.f ? mt[g] + log2f(lsum) : -INFINITY;
             *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) =
                 make_float4(oo[g][0] * inv, oo[g][1] * inv, oo[g][2] * inv, oo[g][3] * inv);
         }
@@ -287,11 +295,12 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
             const int64_t p = u / Ku;
             const int r = (int)(u % Ku);
             if (r < a.k) {
-                const int32_t sl = __ldg(a.slot + p * a.k + r);
+                int32_t sl = __ldg(a.slot + p * a.k + r);
+                if (a.mode != 0 && ((__ldg(a.hit + p * a.k + r) != 0) != (a.mode == 1))) sl = -1;
                 wkind = sl >= 0 ? 1 : 0;
                 widx = sl;
             } else {
-                wkind = __ldg(a.tail_len + p / a.Hkv) > 0 ? 2 : 0;
+                wkind = (a.mode != 2 && __ldg(a.tail_len + p / a.Hkv) > 0) ? 2 : 0;
                 widx = p;
             }
         }
@@ -508,6 +517,8 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
                 const int hq = h * G + g;
                 *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) =
                     make_float4(o[g][0] * inv, o[g][1] * inv, o[g][2] * inv, o[g][3] * inv);
+                if (a.lse != nullptr && lane == 0)
+                    a.lse[(int64_t)hq * a.B + b] = l[g] > 0.f ? m[g] + log2f(l[g]) : -INFINITY;
             }
             continue;
         }
@@ -643,11 +654,12 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
             const int rr = (int)(u - p * Ku);
             wpair = (int)p;
             if (rr < a.k) {
-                const int32_t sl = __ldg(a.slot + p * a.k + rr);
+                int32_t sl = __ldg(a.slot + p * a.k + rr);
+                if (a.mode != 0 && ((__ldg(a.hit + p * a.k + rr) != 0) != (a.mode == 1))) sl = -1;
                 wkind = sl >= 0 ? 1 : 0;
                 wrow = sl * 64;
             } else {
-                wkind = __ldg(a.tail_len + p / a.Hkv) > 0 ? 2 : 0;
+                wkind = (a.mode != 2 && __ldg(a.tail_len + p / a.Hkv) > 0) ? 2 : 0;
                 wrow = (int)p * 64;
             }
         }
@@ -860,6 +872,8 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
                 if (2 * c + e < G) {
                     const float inv = l[e] > 0.f ? 1.f / l[e] : 0.f;
                     float* op = a.out + ((int64_t)(h * G + 2 * c + e) * a.B + b) * kHeadDim + r;
+                    if (a.lse != nullptr && r == 0)
+                        a.lse[(int64_t)(h * G + 2 * c + e) * a.B + b] = l[e] > 0.f ? m[e] + log2f(l[e]) : -INFINITY;
 #pragma unroll
                     for (int md = 0; md < 8; ++md) {
                         op[16 * md] = o[md][e] * inv;
@@ -987,11 +1001,53 @@ static ss_status launch_attn_t(AttnArgs a, cudaStream_t stream) {
     return SS_OK;
 }
 
+// Split-form merge: out = (O_a 2^lse_a + O_b 2^lse_b) / (2^lse_a + 2^lse_b) per
+// (hq, b) row (the standard log-sum-exp combination of two disjoint token sets'
+// softmax-normalised outputs); both empty -> 0.  One warp per row.
+__global__ void __launch_bounds__(256) attn_merge_kernel(const float* __restrict__ oa,
+                                                         const float* __restrict__ la,
+                                                         const float* __restrict__ ob,
+                                                         const float* __restrict__ lb, int64_t rows,
+                                                         const int32_t* counts, float* __restrict__ out) {
+    if (counts != nullptr && counts[3] != 0) return;
+    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (row >= rows) return;
+    const int lane = lane_id();
+    const float xa = la[row], xb = lb[row];
+    const float mx = fmaxf(xa, xb);
+    float wa = 0.f, wb = 0.f;
+    if (mx != -INFINITY) {
+        wa = exp2f(xa - mx);
+        wb = exp2f(xb - mx);
+    }
+    const float inv = (wa + wb) > 0.f ? 1.f / (wa + wb) : 0.f;
+    const float4 va = reinterpret_cast<const float4*>(oa + row * kHeadDim)[lane];
+    const float4 vb = reinterpret_cast<const float4*>(ob + row * kHeadDim)[lane];
+    float4 r;
+    r.x = (va.x * wa + vb.x * wb) * inv;
+    r.y = (va.y * wa + vb.y * wb) * inv;
+    r.z = (va.z * wa + vb.z * wb) * inv;
+    r.w = (va.w * wa + vb.w * wb) * inv;
+    reinterpret_cast<float4*>(out + row * kHeadDim)[lane] = r;
+}
+
+ss_status launch_attn_merge(const float* oa, const float* la, const float* ob, const float* lb,
+                            int64_t rows, const int32_t* counts, float* out, cudaStream_t stream) {
+    if (rows <= 0) return SS_OK;
+    const int64_t threads = rows * 32;
+    attn_merge_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(oa, la, ob, lb, rows, counts, out);
+    SS_LAUNCH_CHECK();
+    return SS_OK;
+}
+
 ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* slot, int k,
                              const void* tail_kv, const int32_t* tail_len, const ss_dims& d,
                              ss_dtype dt, float scale, const int32_t* counts, float* out, void* ws,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, const uint8_t* hit, int mode, float* lse) {
     AttnArgs a;
+    a.hit = hit;
+    a.mode = mode;
+    a.lse = lse;
     a.q = q;
     a.pool = pool_kv;
     a.slot = slot;
@@ -1034,7 +1090,7 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
 }
 
 bool preload_attn() {
-    bool ok = true;
+    bool ok = preload_fn(attn_merge_kernel);
 #define SS_PL(GG)                                              \
     ok &= preload_fn(sparse_attn_mma_kernel<GG>);             \
     ok &= preload_fn(sparse_attn_kernel<true, GG>);           \

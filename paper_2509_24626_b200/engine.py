@@ -45,6 +45,7 @@ class EngineConfig:
     select_priority: bool = False  # run select on a high-priority per-group stream
     cache_per_group: bool = False  # per-group cache streams, ordered per layer only
     h2d_server: bool = False   # one persistent FlashH2D launch per step (flash_h2d_serve)
+    split_attn: bool = False   # server mode: attend the hits while FlashH2D loads the misses
 
     @property
     def group(self) -> int:
@@ -95,6 +96,13 @@ class RequestGroup:
         self.ws_cache = ops.alloc_workspace(SS_WS_CACHE, self.dims, c.max_blk, c.topk,
                                             c.slots_per_layer, device=dev)
         self.ws_attn = ops.alloc_workspace(SS_WS_ATTN, self.dims, c.max_blk, c.topk, device=dev)
+        if c.split_attn:
+            # split attention (EngineConfig.split_attn): hit-part and miss-part
+            # outputs / log-sum-exps, merged into out[l]
+            self.out_h = torch.empty(c.num_q_heads, nb, HEAD_DIM, dtype=torch.float32, device=dev)
+            self.out_m = torch.empty_like(self.out_h)
+            self.lse_h = torch.empty(c.num_q_heads, nb, dtype=torch.float32, device=dev)
+            self.lse_m = torch.empty_like(self.lse_h)
         pair_elems = c.max_blk * 2 * HEAD_DIM
         self.meta = [m[b0 * c.num_kv_heads * pair_elems:b1 * c.num_kv_heads * pair_elems]
                      for m in eng.meta]
@@ -282,6 +290,23 @@ class DecodeEngine:
             with torch.cuda.stream(cs):
                 _cache()
                 g.ev_cache[l].record(cs)
+            if gather and self.server and c.split_attn:
+                # the hits (and the tail) are attended while the server loads the
+                # misses; then the misses, then the log-sum-exp merge
+                j = l * len(self.groups) + gi
+                ops.flag_signal(self.h2d_flags[j:j + 1], stream=cs)
+                g.stream.wait_event(g.ev_cache[l])
+                timed("attn", lambda: ops.sparse_decode_attn_part(
+                    q, self.pool_kv[l], g.slot[l], g.hit[l], 1, c.topk, g.tail_kv[l], g.tail_len, g.dims,
+                    self.scale, g.out_h, g.lse_h, g.ws_attn, counts=g.counts[l]))
+                ops.flag_wait(self.h2d_flags[self.njobs + j:self.njobs + j + 1], stream=g.stream)
+                timed("attn_miss", lambda: (
+                    ops.sparse_decode_attn_part(q, self.pool_kv[l], g.slot[l], g.hit[l], 2, c.topk,
+                                                g.tail_kv[l], g.tail_len, g.dims, self.scale, g.out_m,
+                                                g.lse_m, g.ws_attn, counts=g.counts[l]),
+                    ops.sparse_attn_merge(g.out_h, g.lse_h, g.out_m, g.lse_m, g.out[l], counts=g.counts[l])))
+                g.ev_attn[l].record(g.stream)
+                return
             if gather and self.server:
                 j = l * len(self.groups) + gi
                 ops.flag_signal(self.h2d_flags[j:j + 1], stream=cs)

@@ -220,6 +220,28 @@ def sparse_decode_attn(q: torch.Tensor, pool_kv: torch.Tensor, slot: torch.Tenso
           "sparse_decode_attn")
 
 
+def sparse_decode_attn_part(q: torch.Tensor, pool_kv: torch.Tensor, slot: torch.Tensor,
+                            hit: Optional[torch.Tensor], mode: int, k: int, tail_kv: torch.Tensor,
+                            tail_len: torch.Tensor, d: SSDims, scale: float, out: torch.Tensor,
+                            lse: torch.Tensor, ws: torch.Tensor, counts: Optional[torch.Tensor] = None,
+                            stream=None) -> None:
+    """S5 over a subset (mode 0 all, 1 hits + tail, 2 misses) with its log2-domain LSE."""
+    assert out.dtype == torch.float32 and lse.dtype == torch.float32 and slot.dtype == torch.int32
+    check(_lib.load().sparse_decode_attn_part(_ptr(q), _ptr(pool_kv), _ptr(slot), _ptr(hit), mode, k,
+                                              _ptr(tail_kv), _ptr(tail_len), d, _dt(q), float(scale),
+                                              _ptr(counts), _ptr(out), _ptr(lse), _ptr(ws), ws.numel(),
+                                              _stream(stream)), "sparse_decode_attn_part")
+
+
+def sparse_attn_merge(out_a: torch.Tensor, lse_a: torch.Tensor, out_b: torch.Tensor,
+                      lse_b: torch.Tensor, out: torch.Tensor, counts: Optional[torch.Tensor] = None,
+                      stream=None) -> None:
+    """out = log-sum-exp combination of two disjoint-subset attention results."""
+    rows = lse_a.numel()
+    check(_lib.load().sparse_attn_merge(_ptr(out_a), _ptr(lse_a), _ptr(out_b), _ptr(lse_b), rows,
+                                        _ptr(counts), _ptr(out), _stream(stream)), "sparse_attn_merge")
+
+
 # ---------------------------------------------------------------------------
 # NEXT-1: decode KV append + save path (FlashD2H)
 # ---------------------------------------------------------------------------

@@ -48,7 +48,7 @@ def test_fullsize_layer17_three_steps(name):
     cfg = EngineConfig(batch=wl.batch, layers=wl.layers, num_q_heads=wl.num_q_heads,
                        num_kv_heads=wl.num_kv_heads, max_blk=wl.max_blk, topk=wl.topk,
                        slots_per_layer=slots, num_requests=wl.batch,
-                       dtype=torch.bfloat16, groups=3, h2d_server=True)
+                       dtype=torch.bfloat16, groups=3, h2d_server=True, split_attn=True)
     eng = DecodeEngine(cfg)
     assert eng.server and len(eng.groups) == 3
     hb = runs * cfg.max_blk                             # physical host pool (C2 832 MiB, C3 1 GiB)

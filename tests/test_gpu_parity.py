@@ -421,3 +421,56 @@ def test_cache_fused_form_bit_exact(ops):
                         "-k", "(cache or request_groups) and not fused_form"],
                        env=env, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("dt", [synth.DT_BF16, synth.DT_F32])
+@pytest.mark.parametrize("G", [1, 4])
+def test_attention_split_hits_misses_merge(ops, dt, G):
+    """Split form (sparse_decode_attn_part + sparse_attn_merge): the hit part
+    (+ tail) and the miss part each equal the oracle's attention over that
+    subset, and their log-sum-exp merge equals the oracle's attention over the
+    whole set (PAPER.md:71-72 over disjoint token sets); empty subsets give 0."""
+    B, Hkv, k, S = 3, 8 // G, 48, 500
+    Hq = Hkv * G
+    rng = synth.rng_for(1000, 6, G + 10 * dt)
+    pool = synth.encode(synth.kv_blocks(rng, S, D, synth.channel_scales(rng)), dt)
+    tail = synth.encode(synth.kv_blocks(rng, B * Hkv, D).reshape(B, Hkv, 2, 32, D), dt)
+    qs = synth.encode(rng.standard_normal((B, Hq, D)).astype(np.float32), dt)
+    slot = np.full((B, Hkv, k), -1, np.int32)
+    for b in range(B):
+        for h in range(Hkv):
+            kk = int(rng.integers(1, k + 1))
+            slot[b, h, :kk] = rng.choice(S, size=kk, replace=False)
+    hit = (rng.random((B, Hkv, k)) < 0.9).astype(np.uint8)
+    hit[0, 0, :] = 1          # a pair without misses: empty miss part
+    hit[1, 0, :] = 0          # a pair without hits: hit part = tail only
+    tl = np.array([0, 17, 31], np.int32)
+    scale = 1.0 / math.sqrt(D)
+    slot_h = np.where(hit == 1, slot, -1).astype(np.int32)
+    slot_m = np.where(hit == 0, slot, -1).astype(np.int32)
+    exp_all = oracle.attention(qs, pool, slot, tail, tl, scale)
+    exp_h = oracle.attention(qs, pool, slot_h, tail, tl, scale)
+    exp_m = oracle.attention(qs, pool, slot_m, tail, np.zeros(B, np.int32), scale)
+    d = ops.dims(B, Hq, Hkv)
+    ws = ops.alloc_workspace(2, d, 32, k)
+    T = lambda x: to_torch(x)
+    o_h = torch.full((Hq, B, D), float("nan"), dtype=torch.float32, device="cuda")
+    o_m, o = torch.full_like(o_h, float("nan")), torch.full_like(o_h, float("nan"))
+    l_h = torch.full((Hq, B), float("nan"), dtype=torch.float32, device="cuda")
+    l_m = torch.full_like(l_h, float("nan"))
+    ops.sparse_decode_attn_part(T(qs), T(pool), T(slot), T(hit), 1, k, T(tail), T(tl), d, scale, o_h, l_h, ws)
+    ops.sparse_decode_attn_part(T(qs), T(pool), T(slot), T(hit), 2, k, T(tail), T(tl), d, scale, o_m, l_m, ws)
+    ops.sparse_attn_merge(o_h, l_h, o_m, l_m, o)
+    torch.cuda.synchronize()
+    for got, exp in ((o_h, exp_h), (o_m, exp_m), (o, exp_all)):
+        g = got.cpu().numpy()
+        assert np.isfinite(g).all()
+        assert np.abs(g - exp).max() <= TOL[dt]
+    lm = l_m.cpu().numpy()
+    assert np.isneginf(lm[0:G, 0]).all()                         # pair (0, 0): no misses
+    assert np.isfinite(l_h.cpu().numpy()).all()                   # every hit part has a tail or hits
+    # mode 0 = the one-call attention
+    o0, l0 = torch.empty_like(o_h), torch.empty_like(l_h)
+    ops.sparse_decode_attn_part(T(qs), T(pool), T(slot), T(hit), 0, k, T(tail), T(tl), d, scale, o0, l0, ws)
+    torch.cuda.synchronize()
+    assert np.abs(o0.cpu().numpy() - exp_all).max() <= TOL[dt]

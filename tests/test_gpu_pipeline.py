@@ -132,14 +132,16 @@ def test_f32_pipeline():
                   steps=8, rho=0.9, seed=3)
 
 
-@pytest.mark.parametrize("graph_after,server,ngroups", [(None, False, 2), (4, False, 2), (None, True, 2),
-                                                        (4, True, 2), (4, True, 3)])
-def test_request_groups_pipeline_two_streams(graph_after, server, ngroups):
+@pytest.mark.parametrize("graph_after,server,ngroups,split", [
+    (None, False, 2, False), (4, False, 2, False), (None, True, 2, False), (4, True, 2, False),
+    (4, True, 3, False), (None, True, 2, True), (4, True, 3, True)])
+def test_request_groups_pipeline_two_streams(graph_after, server, ngroups, split):
     """groups=2: the two request groups run on separate streams; per layer the
     oracle makes the same two cache calls (group order, same stamp).  With
     graph_after=4 the steps from 4 on are replays of one captured CUDA graph
     whose LRU stamps come from the pools' device clocks.  server=True: the
-    step's gathers are jobs of one persistent flash_h2d_serve launch."""
+    step's gathers are jobs of one persistent flash_h2d_serve launch; split=True:
+    each group attends its hits while the misses load, then merges."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     from paper_2509_24626_b200.engine import DecodeEngine, EngineConfig
@@ -151,7 +153,7 @@ def test_request_groups_pipeline_two_streams(graph_after, server, ngroups):
     S = B * Hkv * k * 2
     cfg = EngineConfig(batch=B, layers=L, num_q_heads=Hq, num_kv_heads=Hkv, max_blk=max_blk, topk=k,
                        slots_per_layer=S, num_requests=B, dtype=torch.bfloat16, groups=ngroups,
-                       h2d_server=server)
+                       h2d_server=server, split_attn=split)
     eng = DecodeEngine(cfg)
     assert len(eng.groups) == ngroups and eng.server == server
     rng = synth.rng_for(2000, 9)
