@@ -812,9 +812,10 @@ def main():
                     help="1: the step's FlashH2D gathers are served by one persistent launch "
                          "(flash_h2d_serve); 0: one flash_h2d_gather launch per layer and group "
                          "(use 0 under ncu, which serialises kernels)")
-    ap.add_argument("--split-attn", type=int, default=1,
+    ap.add_argument("--split-attn", type=int, default=0,
                     help="1 (with the server): attend each group's cache hits while FlashH2D loads its "
-                         "misses, then the misses, then a log-sum-exp merge; 0: one attention after the gather")
+                         "misses, then the misses, then a log-sum-exp merge (measured slower at C2: "
+                         "11.42 vs 11.03 ms median step); 0: one attention after the gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gather-alone", action="store_true",
                     help="skip the FlashH2D-alone ceiling measurement (profiling runs: keeps launch counts fixed)")

@@ -432,7 +432,7 @@ def test_attention_split_hits_misses_merge(ops, dt, G):
     whole set (PAPER.md:71-72 over disjoint token sets); empty subsets give 0."""
     B, Hkv, k, S = 3, 8 // G, 48, 500
     Hq = Hkv * G
-    rng = synth.rng_for(1000, 6, G + 10 * dt)
+    rng = synth.rng_for(1000, 6, G + (10 if dt == synth.DT_F32 else 0))
     pool = synth.encode(synth.kv_blocks(rng, S, D, synth.channel_scales(rng)), dt)
     tail = synth.encode(synth.kv_blocks(rng, B * Hkv, D).reshape(B, Hkv, 2, 32, D), dt)
     qs = synth.encode(rng.standard_normal((B, Hq, D)).astype(np.float32), dt)
