@@ -168,7 +168,7 @@ def setup_engine(args, rank: int, world: int):
                        num_requests=W["batch"], dtype=torch.bfloat16, groups=args.groups,
                        h2d_streams=args.h2d_streams, select_priority=args.select_priority,
                        cache_per_group=args.cache_per_group, h2d_server=bool(args.h2d_server),
-                       split_attn=bool(args.split_attn))
+                       split_attn=bool(args.split_attn), pool_per_group=bool(args.pool_per_group))
     eng = DecodeEngine(cfg)
     # physical host pool: a prime number of max_blk runs (aliasing, R15)
     runs = args.host_runs if cfg.max_blk <= 4096 else max(1, (args.host_runs * 4096) // cfg.max_blk)
@@ -277,7 +277,7 @@ def solo_pass(eng, q_src, layers, hbm_peak, h2d_peak, stamp):
     t = {"select": [], "cache": [], "gather": [], "attn": []}
     sel_b = attn_b = miss_b = 0
     for l in range(layers):
-        for g in eng.groups:
+        for gi, g in enumerate(eng.groups):
             q = q_src[l, g.b0:g.b1]
 
             def timed(name, fn):
@@ -294,12 +294,12 @@ def solo_pass(eng, q_src, layers, hbm_peak, h2d_peak, stamp):
             timed("select", lambda: ops.ss_block_select(q, g.meta[l], g.n_blk, c.max_blk, c.topk, g.dims,
                                                         g.sel[l], g.ws_select))
             timed("cache", lambda: ops.kv_cache_lookup_insert(
-                eng.pools[l], g.sel[l], g.req_ids, l, c.layers, c.max_blk, c.topk, g.dims, stamp,
+                eng.pool_of(l, gi), g.sel[l], g.req_ids, l, c.layers, c.max_blk, c.topk, g.dims, stamp,
                 g.slot[l], g.hit[l], g.miss_keys[l], g.miss_slots[l], g.counts[l], g.ws_cache))
             timed("gather", lambda: ops.flash_h2d_gather(eng.host_ptr, eng.host_blocks, g.miss_keys[l],
-                                                         g.miss_slots[l], g.counts[l], g.E, eng.pool_kv[l],
+                                                         g.miss_slots[l], g.counts[l], g.E, eng.pool_kv_of(l, gi),
                                                          c.block_bytes))
-            timed("attn", lambda: ops.sparse_decode_attn(q, eng.pool_kv[l], g.slot[l], c.topk, g.tail_kv[l],
+            timed("attn", lambda: ops.sparse_decode_attn(q, eng.pool_kv_of(l, gi), g.slot[l], c.topk, g.tail_kv[l],
                                                          g.tail_len, g.dims, eng.scale, g.out[l], g.ws_attn,
                                                          counts=g.counts[l]))
             hits, miss = [int(x) for x in g.counts[l, :2].tolist()]
@@ -705,7 +705,7 @@ def bench_ours(args):
                        "topk_blocks": c.topk, "hbm_cache_slots_per_layer": c.slots_per_layer,
                        "host_pool_blocks": eng.host_blocks, "host_kv": "pinned DRAM, zero-copy (UVA)",
                        "parallelism": f"kv-heads/{world} per GPU" if world > 1 else "1 GPU",
-                       "request_groups": len(eng.groups), "h2d_server": eng.server, "split_attn": bool(eng.server and eng.cfg.split_attn), "h2d_streams": args.h2d_streams, "select_priority": args.select_priority, "cache_per_group": args.cache_per_group,
+                       "request_groups": len(eng.groups), "h2d_server": eng.server, "split_attn": bool(eng.server and eng.cfg.split_attn), "pool_per_group": eng.per_group_pools, "h2d_streams": args.h2d_streams, "select_priority": args.select_priority, "cache_per_group": args.cache_per_group,
                        "cuda_graph": graph is not None,
                        "cache_settle_steps": args.settle,
                        "l2": f"no flush needed: inputs larger than L2 ({meta_gib:.0f} GiB metadata streamed per step)",
@@ -816,6 +816,9 @@ def main():
                     help="1 (with the server): attend each group's cache hits while FlashH2D loads its "
                          "misses, then the misses, then a log-sum-exp merge (measured slower at C2: "
                          "11.42 vs 11.03 ms median step); 0: one attention after the gather")
+    ap.add_argument("--pool-per-group", type=int, default=0,
+                    help="1: each layer's cache slots split evenly into one LRU pool per request group "
+                         "(independent cache calls, 1/groups of the per-call bookkeeping); 0: one pool per layer")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gather-alone", action="store_true",
                     help="skip the FlashH2D-alone ceiling measurement (profiling runs: keeps launch counts fixed)")

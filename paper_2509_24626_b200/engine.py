@@ -46,6 +46,7 @@ class EngineConfig:
     cache_per_group: bool = False  # per-group cache streams, ordered per layer only
     h2d_server: bool = False   # one persistent FlashH2D launch per step (flash_h2d_serve)
     split_attn: bool = False   # server mode: attend the hits while FlashH2D loads the misses
+    pool_per_group: bool = False  # one LRU pool per (layer, request group) of slots/groups slots
 
     @property
     def group(self) -> int:
@@ -136,9 +137,23 @@ class DecodeEngine:
         self.meta: List[torch.Tensor] = [torch.zeros(meta_elems, dtype=c.dtype, device=dev)
                                          for _ in range(c.layers)]
         self.fwd = torch.full((c.fwd_len,), -1, dtype=torch.int32, device=dev)
-        self.pools = [ops.CachePool(c.slots_per_layer, self.fwd, dev) for _ in range(c.layers)]
-        self.pool_kv = [torch.zeros(c.slots_per_layer * c.block_elems, dtype=c.dtype, device=dev)
-                        for _ in range(c.layers)]
+        ng0 = max(1, min(c.groups, c.batch))
+        # pool_per_group (reading R11b): the slots of a layer are split evenly
+        # between the request groups, each group's requests run their own batch
+        # LRU over their share, and the groups' cache calls are independent (no
+        # cross-group order, 1/groups of the O(S) bookkeeping per call)
+        self.per_group_pools = c.pool_per_group and ng0 > 1
+        if self.per_group_pools:
+            sg = c.slots_per_layer // ng0
+            self.gpools = [[ops.CachePool(sg, self.fwd, dev) for _ in range(ng0)] for _ in range(c.layers)]
+            self.gpool_kv = [[torch.zeros(sg * c.block_elems, dtype=c.dtype, device=dev) for _ in range(ng0)]
+                             for _ in range(c.layers)]
+            self.pools = [gp[0] for gp in self.gpools]
+            self.pool_kv = [gk[0] for gk in self.gpool_kv]
+        else:
+            self.pools = [ops.CachePool(c.slots_per_layer, self.fwd, dev) for _ in range(c.layers)]
+            self.pool_kv = [torch.zeros(c.slots_per_layer * c.block_elems, dtype=c.dtype, device=dev)
+                            for _ in range(c.layers)]
         self.tail_kv = torch.zeros(c.layers, c.batch, c.num_kv_heads, 2, BLOCK_TOKENS, HEAD_DIM,
                                    dtype=c.dtype, device=dev)
         self.tail_len = torch.zeros(c.batch, dtype=torch.int32, device=dev)
@@ -170,7 +185,7 @@ class DecodeEngine:
                 g.h2d_stream = h2d[i % len(h2d)]
             self.h2d_streams = h2d
         self.cache_stream = torch.cuda.Stream(dev, priority=-1) if ng > 1 else None
-        if ng > 1 and c.cache_per_group:
+        if ng > 1 and (c.cache_per_group or self.per_group_pools):
             # a layer's pool orders its calls group 0, 1, ...; calls of different
             # layers (different pools) need no order, so one shared cache stream
             # would add false cross-layer dependencies
@@ -186,8 +201,10 @@ class DecodeEngine:
         self.server = ng > 1 and c.h2d_server
         if self.server:
             self.njobs = c.layers * ng
-            self.h2d_jobs = ops.h2d_jobs([(g.miss_keys[l], g.miss_slots[l], g.counts[l], self.pool_kv[l], g.E)
-                                          for l in range(c.layers) for g in self.groups], device=dev)
+            self.h2d_jobs = ops.h2d_jobs([(g.miss_keys[l], g.miss_slots[l], g.counts[l],
+                                           self.pool_kv_of(l, gi), g.E)
+                                          for l in range(c.layers) for gi, g in enumerate(self.groups)],
+                                         device=dev)
             self.h2d_flags = ops.h2d_flags(self.njobs, device=dev)
             ops.preload_kernels()      # no lazy kernel load while the server spins
         self._capturing = False
@@ -197,6 +214,13 @@ class DecodeEngine:
         self.miss_keys, self.miss_slots, self.counts, self.out = (g0.miss_keys, g0.miss_slots,
                                                                   g0.counts, g0.out)
         self.E = g0.E
+
+    def pool_of(self, l: int, gi: int) -> "ops.CachePool":
+        """The LRU pool request group gi uses at layer l."""
+        return self.gpools[l][gi] if self.per_group_pools else self.pools[l]
+
+    def pool_kv_of(self, l: int, gi: int) -> torch.Tensor:
+        return self.gpool_kv[l][gi] if self.per_group_pools else self.pool_kv[l]
 
     # ------------------------------------------------------------------ setup
     def set_host_kv(self, host_kv: torch.Tensor, host_blocks: int) -> None:
@@ -259,13 +283,13 @@ class DecodeEngine:
 
         def _cache():
             timed("cache", lambda: ops.kv_cache_lookup_insert(
-                self.pools[l], g.sel[l], g.req_ids, l, c.layers, c.max_blk, c.topk, g.dims, stamp,
+                self.pool_of(l, gi), g.sel[l], g.req_ids, l, c.layers, c.max_blk, c.topk, g.dims, stamp,
                 g.slot[l], g.hit[l], g.miss_keys[l], g.miss_slots[l], g.counts[l], g.ws_cache))
 
         def _gather():
             timed("gather", lambda: ops.flash_h2d_gather(self.host_ptr, self.host_blocks,
                                                          g.miss_keys[l], g.miss_slots[l], g.counts[l],
-                                                         g.E, self.pool_kv[l], c.block_bytes))
+                                                         g.E, self.pool_kv_of(l, gi), c.block_bytes))
         if not multi:
             _cache()
             if gather:
@@ -280,9 +304,9 @@ class DecodeEngine:
                 g.ev_sel[l].record(g.stream)
             cs = g.cache_stream if g.cache_stream is not None else self.cache_stream
             cs.wait_event(g.ev_sel[l])
-            if g.cache_stream is not None and gi > 0:
+            if g.cache_stream is not None and gi > 0 and not self.per_group_pools:
                 cs.wait_event(self.groups[gi - 1].ev_cache[l])   # same layer pool: in group order
-            if gi == 0 and not self._capturing:
+            if gi == 0 and not self._capturing and not self.per_group_pools:
                 # (inside a captured graph, successive replays are serialised,
                 # which already orders step t+1 after all of step t)
                 for other in self.groups[1:]:
@@ -297,11 +321,11 @@ class DecodeEngine:
                 ops.flag_signal(self.h2d_flags[j:j + 1], stream=cs)
                 g.stream.wait_event(g.ev_cache[l])
                 timed("attn", lambda: ops.sparse_decode_attn_part(
-                    q, self.pool_kv[l], g.slot[l], g.hit[l], 1, c.topk, g.tail_kv[l], g.tail_len, g.dims,
+                    q, self.pool_kv_of(l, gi), g.slot[l], g.hit[l], 1, c.topk, g.tail_kv[l], g.tail_len, g.dims,
                     self.scale, g.out_h, g.lse_h, g.ws_attn, counts=g.counts[l]))
                 ops.flag_wait(self.h2d_flags[self.njobs + j:self.njobs + j + 1], stream=g.stream)
                 timed("attn_miss", lambda: (
-                    ops.sparse_decode_attn_part(q, self.pool_kv[l], g.slot[l], g.hit[l], 2, c.topk,
+                    ops.sparse_decode_attn_part(q, self.pool_kv_of(l, gi), g.slot[l], g.hit[l], 2, c.topk,
                                                 g.tail_kv[l], g.tail_len, g.dims, self.scale, g.out_m,
                                                 g.lse_m, g.ws_attn, counts=g.counts[l]),
                     ops.sparse_attn_merge(g.out_h, g.lse_h, g.out_m, g.lse_m, g.out[l], counts=g.counts[l])))
@@ -319,7 +343,7 @@ class DecodeEngine:
                 g.stream.wait_event(g.ev_gather[l])
             else:
                 g.stream.wait_event(g.ev_cache[l])
-        timed("attn", lambda: ops.sparse_decode_attn(q, self.pool_kv[l], g.slot[l], c.topk,
+        timed("attn", lambda: ops.sparse_decode_attn(q, self.pool_kv_of(l, gi), g.slot[l], c.topk,
                                                      g.tail_kv[l], g.tail_len, g.dims, self.scale,
                                                      g.out[l], g.ws_attn, counts=g.counts[l]))
         if len(self.groups) > 1:
@@ -422,7 +446,7 @@ class DecodeEngine:
         if getattr(self, "clock", None) is None:
             self.clock = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.clock.fill_(start)
-        for p in self.pools:
+        for p in (sum(self.gpools, []) if self.per_group_pools else self.pools):
             p.clock = self.clock
 
     def advance_clock(self) -> None:

@@ -46,7 +46,9 @@ def _run_pipeline(dt, B, L, Hq, Hkv, n_blk, k, S, tails, steps, rho, seed):
 
     # oracle side: its own metadata, pools and pipeline
     host_u8 = host_np.view(np.uint8).reshape(host_blocks, -1)
-    pools = [oracle.Pool(S, cfg.fwd_len, cfg.block_bytes) for _ in range(L)]
+    Sg = S // ngroups if ppg else S
+    gpools = [[oracle.Pool(Sg, cfg.fwd_len, cfg.block_bytes) for _ in range(ngroups if ppg else 1)]
+              for _ in range(L)]
     metas = []
     for l in range(L):
         m = np.zeros((B, Hkv, max_blk, 2, D), dtype=host_np.dtype)
@@ -132,16 +134,18 @@ def test_f32_pipeline():
                   steps=8, rho=0.9, seed=3)
 
 
-@pytest.mark.parametrize("graph_after,server,ngroups,split", [
-    (None, False, 2, False), (4, False, 2, False), (None, True, 2, False), (4, True, 2, False),
-    (4, True, 3, False), (None, True, 2, True), (4, True, 3, True)])
-def test_request_groups_pipeline_two_streams(graph_after, server, ngroups, split):
+@pytest.mark.parametrize("graph_after,server,ngroups,split,ppg", [
+    (None, False, 2, False, False), (4, False, 2, False, False), (None, True, 2, False, False),
+    (4, True, 2, False, False), (4, True, 3, False, False), (None, True, 2, True, False),
+    (4, True, 3, True, False), (None, True, 2, False, True), (4, True, 3, False, True)])
+def test_request_groups_pipeline_two_streams(graph_after, server, ngroups, split, ppg):
     """groups=2: the two request groups run on separate streams; per layer the
     oracle makes the same two cache calls (group order, same stamp).  With
     graph_after=4 the steps from 4 on are replays of one captured CUDA graph
     whose LRU stamps come from the pools' device clocks.  server=True: the
     step's gathers are jobs of one persistent flash_h2d_serve launch; split=True:
-    each group attends its hits while the misses load, then merges."""
+    each group attends its hits while the misses load, then merges.  ppg=True:
+    one LRU pool per (layer, group) of S / groups slots (reading R11b)."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     from paper_2509_24626_b200.engine import DecodeEngine, EngineConfig
@@ -153,7 +157,7 @@ def test_request_groups_pipeline_two_streams(graph_after, server, ngroups, split
     S = B * Hkv * k * 2
     cfg = EngineConfig(batch=B, layers=L, num_q_heads=Hq, num_kv_heads=Hkv, max_blk=max_blk, topk=k,
                        slots_per_layer=S, num_requests=B, dtype=torch.bfloat16, groups=ngroups,
-                       h2d_server=server, split_attn=split)
+                       h2d_server=server, split_attn=split, pool_per_group=ppg)
     eng = DecodeEngine(cfg)
     assert len(eng.groups) == ngroups and eng.server == server
     rng = synth.rng_for(2000, 9)
@@ -175,7 +179,9 @@ def test_request_groups_pipeline_two_streams(graph_after, server, ngroups, split
                 k0 = eng.key0(b, l, h)
                 m[b, h, :n_blk[b]] = oracle.block_meta(blocks[k0:k0 + n_blk[b]], key_stride=2 * 32 * D)
         metas.append(m)
-    pools = [oracle.Pool(S, cfg.fwd_len, cfg.block_bytes) for _ in range(L)]
+    Sg = S // ngroups if ppg else S
+    gpools = [[oracle.Pool(Sg, cfg.fwd_len, cfg.block_bytes) for _ in range(ngroups if ppg else 1)]
+              for _ in range(L)]
     qs = synth.encode(synth.queries(rng, steps, (L, B, Hq, D), 0.95), dt)
     host_u8 = host_np.view(np.uint8).reshape(hb, -1)
     nbk = np.array(n_blk, np.int32)
@@ -194,10 +200,11 @@ def test_request_groups_pipeline_two_streams(graph_after, server, ngroups, split
             eng.step(to_torch(qs[t]), stamp=t + 1)
         torch.cuda.synchronize()
         for l in range(L):
-            for g in eng.groups:
+            for gi, g in enumerate(eng.groups):
                 b0, b1 = g.b0, g.b1
+                op = gpools[l][gi if ppg else 0]
                 r = oracle.decode_layer(np.ascontiguousarray(qs[t, l, b0:b1]), np.ascontiguousarray(metas[l][b0:b1]),
-                                        nbk[b0:b1], k, pools[l], np.arange(b0, b1, dtype=np.int32), l, L,
+                                        nbk[b0:b1], k, op, np.arange(b0, b1, dtype=np.int32), l, L,
                                         max_blk, t + 1, host_u8, hb, np.ascontiguousarray(tail_np[l, b0:b1]),
                                         tl[b0:b1], 1.0 / math.sqrt(D))
                 np.testing.assert_array_equal(g.sel[l].cpu().numpy(), r["sel"])
@@ -205,7 +212,11 @@ def test_request_groups_pipeline_two_streams(graph_after, server, ngroups, split
                 np.testing.assert_array_equal(g.slot[l].cpu().numpy(), r["slot"])
                 err = float(np.abs(g.out[l].cpu().numpy() - r["out"]).max())
                 assert err <= TOL[dt], f"step {t} layer {l} group {b0}: {err}"
-            np.testing.assert_array_equal(eng.pools[l].slot_stamp.cpu().numpy(), pools[l].slot_stamp)
-            np.testing.assert_array_equal(eng.pools[l].slot_key.cpu().numpy(), pools[l].slot_key)
+            for gi in range(ngroups if ppg else 1):
+                p_dev, p_or = eng.pool_of(l, gi), gpools[l][gi]
+                np.testing.assert_array_equal(p_dev.slot_stamp.cpu().numpy(), p_or.slot_stamp)
+                np.testing.assert_array_equal(p_dev.slot_key.cpu().numpy(), p_or.slot_key)
     for l in range(L):
-        np.testing.assert_array_equal(to_numpy(eng.pool_kv[l]).view(np.uint8).reshape(S, -1), pools[l].kv)
+        for gi in range(ngroups if ppg else 1):
+            np.testing.assert_array_equal(
+                to_numpy(eng.pool_kv_of(l, gi)).view(np.uint8).reshape(Sg, -1), gpools[l][gi].kv)
