@@ -28,6 +28,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
+# more hardware work queues than CUDA's default 8: the step runs ~12 streams
+# (request groups, their cache streams, the FlashH2D server), and two of its
+# kernels spin on flags (the server, ss_flag_wait) -- with too few queues an
+# unrelated stream's work can be queued behind a spinning kernel (set before
+# the CUDA context exists)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import torch  # noqa: E402
 
 import synth  # noqa: E402
@@ -800,7 +806,7 @@ def main():
     ap.add_argument("--timeline", default=None, help="write one step's op timeline (json, timing pass)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch kernels eagerly instead of replaying a captured CUDA graph per step")
-    ap.add_argument("--groups", type=int, default=3,
+    ap.add_argument("--groups", type=int, default=5,
                     help="request groups pipelined on separate streams (PCIe of one overlaps HBM work of another)")
     ap.add_argument("--h2d-streams", type=int, default=1,
                     help="FlashH2D streams shared by the request groups (1: the link serves one group at a time)")
@@ -816,7 +822,7 @@ def main():
                     help="1 (with the server): attend each group's cache hits while FlashH2D loads its "
                          "misses, then the misses, then a log-sum-exp merge (measured slower at C2: "
                          "11.42 vs 11.03 ms median step); 0: one attention after the gather")
-    ap.add_argument("--pool-per-group", type=int, default=0,
+    ap.add_argument("--pool-per-group", type=int, default=1,
                     help="1: each layer's cache slots split evenly into one LRU pool per request group "
                          "(independent cache calls, 1/groups of the per-call bookkeeping); 0: one pool per layer")
     ap.add_argument("--no-cpu-baseline", action="store_true")

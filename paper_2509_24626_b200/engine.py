@@ -200,6 +200,12 @@ class DecodeEngine:
         # waits on done[j] (flash_h2d_serve in include/sparseserve.h)
         self.server = ng > 1 and c.h2d_server
         if self.server:
+            import os
+            import warnings
+            if int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8")) < 2 * ng + 2:
+                warnings.warn("FlashH2D server with %d request groups: set CUDA_DEVICE_MAX_CONNECTIONS "
+                              ">= %d before CUDA starts (a spinning kernel can otherwise sit in front of "
+                              "another stream's work until the 3 s timeout)" % (ng, 2 * ng + 2))
             self.njobs = c.layers * ng
             self.h2d_jobs = ops.h2d_jobs([(g.miss_keys[l], g.miss_slots[l], g.counts[l],
                                            self.pool_kv_of(l, gi), g.E)

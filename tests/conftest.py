@@ -3,6 +3,10 @@ import sys
 
 import pytest
 
+# as bench.py: enough hardware work queues for the multi-stream step (spinning
+# server / flag-wait kernels must not sit in front of unrelated streams' work)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

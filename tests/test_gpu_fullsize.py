@@ -41,16 +41,17 @@ def test_fullsize_layer17_three_steps(name):
         pytest.skip(f"needs ~{need_gb} GB of free HBM")
     from paper_2509_24626_b200.engine import DecodeEngine, EngineConfig
     import bench
-    # the launch configuration bench.py times: 3 request groups on streams, the
+    # the launch configuration bench.py times: 5 request groups on streams with
+    # one LRU pool per (layer, group), the
     # FlashH2D server, steps after the first replayed from one captured CUDA
     # graph with device-clock stamps, and (C2) the HBM-filling cache size
     slots = bench.auto_slots(None, wl, wl.batch, 1) if name == "C2" else wl.slots_per_layer
     cfg = EngineConfig(batch=wl.batch, layers=wl.layers, num_q_heads=wl.num_q_heads,
                        num_kv_heads=wl.num_kv_heads, max_blk=wl.max_blk, topk=wl.topk,
                        slots_per_layer=slots, num_requests=wl.batch,
-                       dtype=torch.bfloat16, groups=3, h2d_server=True, split_attn=True)
+                       dtype=torch.bfloat16, groups=5, h2d_server=True, pool_per_group=True)
     eng = DecodeEngine(cfg)
-    assert eng.server and len(eng.groups) == 3
+    assert eng.server and eng.per_group_pools and len(eng.groups) == min(5, wl.batch)
     hb = runs * cfg.max_blk                             # physical host pool (C2 832 MiB, C3 1 GiB)
     rng = synth.rng_for(8000, 1)
     scales = synth.channel_scales(rng)
@@ -78,7 +79,8 @@ def test_fullsize_layer17_three_steps(name):
                 p0 = eng.key0(b, l, h) % hb
                 m[b, h] = oracle.block_meta(host_np[p0:p0 + wl.n_blk], key_stride=2 * 32 * D)
         metas[l] = m
-        pools[l] = oracle.Pool(cfg.slots_per_layer, cfg.fwd_len, cfg.block_bytes)
+        ng = len(eng.groups)
+        pools[l] = [oracle.Pool(cfg.slots_per_layer // ng, cfg.fwd_len, cfg.block_bytes) for _ in range(ng)]
     host_u8 = host_np.view(np.uint8).reshape(hb, -1)
     tails = np.zeros((cfg.batch, cfg.num_kv_heads, 2, 32, D), np.uint16)
     tl = np.zeros(cfg.batch, np.int32)
@@ -95,11 +97,11 @@ def test_fullsize_layer17_three_steps(name):
             graph.replay()
         torch.cuda.synchronize()
         for l in CHECK_LAYERS:
-            for g in eng.groups:
+            for gi, g in enumerate(eng.groups):
                 b0, b1 = g.b0, g.b1
                 r = oracle.decode_layer(np.ascontiguousarray(qs[t, l, b0:b1]),
                                         np.ascontiguousarray(metas[l][b0:b1]),
-                                        np.array(nbk[b0:b1], np.int32), cfg.topk, pools[l],
+                                        np.array(nbk[b0:b1], np.int32), cfg.topk, pools[l][gi],
                                         np.arange(b0, b1, dtype=np.int32), l, cfg.layers, cfg.max_blk,
                                         t + 1, host_u8, hb, tails[b0:b1], tl[b0:b1], 1.0 / math.sqrt(D))
                 np.testing.assert_array_equal(g.sel[l].cpu().numpy(), r["sel"])
@@ -108,15 +110,17 @@ def test_fullsize_layer17_three_steps(name):
                 np.testing.assert_array_equal(g.hit[l].cpu().numpy(), r["hit"])
                 err = float(np.abs(g.out[l].cpu().numpy() - r["out"]).max())
                 assert err <= 2e-3, f"step {t} layer {l} group {b0}: max abs err {err}"
-            p = eng.pools[l]
-            np.testing.assert_array_equal(p.slot_key.cpu().numpy(), pools[l].slot_key)
-            np.testing.assert_array_equal(p.slot_stamp.cpu().numpy(), pools[l].slot_stamp)
-            np.testing.assert_array_equal(
-                p.order.cpu().numpy(),
-                np.lexsort((np.arange(cfg.slots_per_layer), pools[l].slot_stamp)).astype(np.int32))
+            for gi in range(len(eng.groups)):
+                p, po = eng.pool_of(l, gi), pools[l][gi]
+                np.testing.assert_array_equal(p.slot_key.cpu().numpy(), po.slot_key)
+                np.testing.assert_array_equal(p.slot_stamp.cpu().numpy(), po.slot_stamp)
+                np.testing.assert_array_equal(
+                    p.order.cpu().numpy(),
+                    np.lexsort((np.arange(len(po.slot_stamp)), po.slot_stamp)).astype(np.int32))
     # bytes of every cached block of the checked layers
     for l in CHECK_LAYERS:
-        used = np.nonzero(pools[l].slot_key >= 0)[0]
-        gpu = eng.pool_kv[l].view(torch.int16).view(cfg.slots_per_layer, -1)[torch.from_numpy(used).cuda()]
-        np.testing.assert_array_equal(gpu.cpu().numpy().view(np.uint8).reshape(len(used), -1),
-                                      pools[l].kv[used])
+        for gi in range(len(eng.groups)):
+            po = pools[l][gi]
+            used = np.nonzero(po.slot_key >= 0)[0]
+            gpu = eng.pool_kv_of(l, gi).view(torch.int16).view(len(po.slot_key), -1)[torch.from_numpy(used).cuda()]
+            np.testing.assert_array_equal(gpu.cpu().numpy().view(np.uint8).reshape(len(used), -1), po.kv[used])
