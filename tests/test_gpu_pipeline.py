@@ -46,9 +46,7 @@ def _run_pipeline(dt, B, L, Hq, Hkv, n_blk, k, S, tails, steps, rho, seed):
 
     # oracle side: its own metadata, pools and pipeline
     host_u8 = host_np.view(np.uint8).reshape(host_blocks, -1)
-    Sg = S // ngroups if ppg else S
-    gpools = [[oracle.Pool(Sg, cfg.fwd_len, cfg.block_bytes) for _ in range(ngroups if ppg else 1)]
-              for _ in range(L)]
+    pools = [oracle.Pool(S, cfg.fwd_len, cfg.block_bytes) for _ in range(L)]
     metas = []
     for l in range(L):
         m = np.zeros((B, Hkv, max_blk, 2, D), dtype=host_np.dtype)
