@@ -422,6 +422,7 @@ def bench_ours(args):
     t_e2e = t_timed + args.steps
     t_kt = t_e2e + e2e_steps
     t_srv = t_kt + n_kt                               # server-only timing pass (h2d_server)
+    srv_err = 0
     qs = gen_queries(eng, t_srv + n_kt + 1, W["rho"], seed=5000 + rank)
     gathered = None
     if world > 1:
@@ -597,6 +598,7 @@ def bench_ours(args):
                 srv_ms += timers_s.totals_ms()["gather"]
             del sgraph
             srv_miss = int(srv_cnt[1])
+            srv_err = int(srv_cnt[3])
     else:
         timers = StepTimers()
         k_s = torch.cuda.Event(True)
@@ -622,10 +624,13 @@ def bench_ours(args):
     sel_gbs = sel_bytes / (tot["select"] * 1e-3) / 1e9
     attn_ms = tot["attn"] + tot.get("attn_miss", 0.0)     # split form: hit part + miss part & merge
     attn_gbs = attn_bytes / (attn_ms * 1e-3) / 1e9
-    if eng.server and graph is not None:
+    if eng.server and graph is not None and srv_err == 0:
         # one server launch per step: its own pass (above)
         tot["gather"], nlaunch["gather"], miss_bytes_kt, k_miss_g = srv_ms, n_kt, srv_miss * c.block_bytes, srv_miss
     else:
+        # (a server-pass step that aborted -- counts[3] set by the server's
+        # timeout -- is not a measurement: the server launch of the per-op
+        # timing pass above is used instead)
         k_miss_g = k_miss
     h2d_gbs = miss_bytes_kt / (tot["gather"] * 1e-3) / 1e9 if tot["gather"] > 0 else 0.0
     kernels = {
@@ -731,6 +736,7 @@ def bench_ours(args):
                                                  + (1 if eng.server else 0))),
             "cpu_baseline": cpu, "clocks": clocks, "setup_s": round(setup_s, 1),
             "errors_in_timed_region": n_err,
+            "errors_in_timing_passes": int(kcnt[3]) + (srv_err if eng.server and graph is not None else 0),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
