@@ -106,10 +106,11 @@ ss_status launch_flash_h2d(const void* host_kv, int64_t host_blocks, const int64
 // FlashH2D server (flash_h2d_serve): ONE persistent launch serves the ordered
 // sequence of gathers ("jobs") of a whole decode step -- one job per (layer,
 // request group) -- so the PCIe link does not drain and refill at every layer
-// boundary.  Warps walk the jobs in order; job j's inputs are valid once
-// ready[j] != 0 (ss_flag_signal after its kv_cache_lookup_insert); its work
-// units are handed out by an atomic cursor, so warps done with job j start
-// job j+1's loads while others still finish job j.  The warp that completes
+// boundary.  Job j's inputs are valid once ready[j] != 0 (ss_flag_signal
+// after its kv_cache_lookup_insert); its work units are handed out by an
+// atomic cursor, and a warp always takes a unit of the lowest-numbered ready
+// job with units left, so warps done with job j start the next job's loads
+// while others still finish job j, and a late job never blocks ready ones.  The warp that completes
 // job j's last unit publishes done[j] = 1 (release), which ss_flag_wait turns
 // into a stream dependency for that job's attention.
 //
@@ -147,34 +148,73 @@ flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
     const int lane = lane_id();
     constexpr int64_t kBatch = 32 * kU;
     const int upb = (int)((vpb + kBatch - 1) / kBatch);  // units per block
-    int j = 0;
+    // Out-of-order service: lane 0 of a warp takes a unit of the LOWEST-numbered
+    // ready job that still has units left (jobs below `lo` are fully handed
+    // out), so a job whose producer is late never holds up later ready jobs --
+    // nor, through their consumers, the hardware queues the late producer may be
+    // waiting in.
+    int lo = 0;
     bool aborted = false;
-    for (; j < njobs; ++j) {
-        int ok = 1;
+    uint64_t t_idle = gtimer_ns();
+    const uint4* hsrc = host;
+    while (true) {
+        int pj = -1, pu = 0, pnu = 0;
         if (lane == 0) {
-            const uint64_t t0 = gtimer_ns();
-            while (ld_acquire_gpu(ready + j) == 0) {
-                if (*(volatile int32_t*)abort_flag) { ok = 0; break; }
-                if (gtimer_ns() - t0 > timeout_ns) { atomicExch(abort_flag, 1); ok = 0; break; }
-                __nanosleep(64);
+            for (int jj = lo; jj < njobs; ++jj) {
+                if (ld_acquire_gpu(ready + jj) == 0) continue;
+                const int32_t* cnt = jobs[jj].counts;
+                const int err = __ldcg(cnt + 3);
+                const int n = err ? 0 : min(__ldcg(cnt + 1), jobs[jj].max_misses);
+                const int nu = n * upb;
+                const int peek = *(volatile int32_t*)(cursor + jj);
+                if (nu == 0) {  // nothing to load: the first warp here publishes done
+                    if (peek == 0 && atomicAdd(cursor + jj, 1) == 0) st_release_gpu(done + jj, 1);
+                    if (jj == lo) ++lo;
+                    continue;
+                }
+                if (peek >= nu) {
+                    if (jj == lo) ++lo;
+                    continue;
+                }
+                const int u = atomicAdd(cursor + jj, 1);
+                if (u >= nu) {
+                    if (jj == lo) ++lo;
+                    continue;
+                }
+                pj = jj;
+                pu = u;
+                pnu = nu;
+                break;
             }
         }
-        if (!__shfl_sync(0xffffffffu, ok, 0)) { aborted = true; break; }
-        const ss_h2d_job jb = jobs[j];
-        const int err = __ldcg(jb.counts + 3);
-        const int n = err ? 0 : min(__ldcg(jb.counts + 1), jb.max_misses);
-        const int nu = n * upb;
-        int u = 0;
-        if (lane == 0) u = atomicAdd(cursor + j, 1);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (nu == 0) {
-            if (u == 0 && lane == 0) st_release_gpu(done + j, 1);
+        pj = __shfl_sync(0xffffffffu, pj, 0);
+        lo = __shfl_sync(0xffffffffu, lo, 0);
+        if (pj < 0) {
+            if (lo >= njobs) break;  // every job handed out
+            int stop = 0;
+            if (lane == 0) {
+                if (*(volatile int32_t*)abort_flag) {
+                    stop = 1;
+                } else if (gtimer_ns() - t_idle > timeout_ns) {
+                    atomicExch(abort_flag, 1);
+                    stop = 1;
+                } else {
+                    __nanosleep(64);
+                }
+            }
+            if (__shfl_sync(0xffffffffu, stop, 0)) {
+                aborted = true;
+                break;
+            }
             continue;
         }
-        const uint4* hsrc = host;
+        pu = __shfl_sync(0xffffffffu, pu, 0);
+        pnu = __shfl_sync(0xffffffffu, pnu, 0);
+        if (lane == 0) t_idle = gtimer_ns();
+        const ss_h2d_job jb = jobs[pj];
         uint4* pool = (uint4*)jb.pool_kv;
-        while (u < nu) {
-            const int i = u / upb, part = u - i * upb;
+        {
+            const int i = pu / upb, part = pu - i * upb;
             const int64_t phys = __ldcg(jb.miss_keys + i) % host_blocks;
             const uint4* src = hsrc + phys * vpb;
             uint4* dst = pool + (int64_t)__ldcg(jb.miss_slots + i) * vpb;
@@ -197,21 +237,19 @@ flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
                 for (int64_t v = v0; v < min(vpb, (int64_t)(part + 1) * kBatch); v += 32)
                     stg_v4(dst + v, ldg_stream(src + v));
             }
-            __threadfence();  // this lane's pool stores are visible GPU-wide ...
-            __syncwarp();
-            if (lane == 0) {  // ... before the unit is counted
-                const int f = atomicAdd(fin + j, 1);
-                if (f == nu - 1) {
-                    __threadfence();
-                    st_release_gpu(done + j, 1);
-                }
-                u = atomicAdd(cursor + j, 1);
+        }
+        __threadfence();  // this lane's pool stores are visible GPU-wide ...
+        __syncwarp();
+        if (lane == 0) {  // ... before the unit is counted
+            const int f = atomicAdd(fin + pj, 1);
+            if (f == pnu - 1) {
+                __threadfence();
+                st_release_gpu(done + pj, 1);
             }
-            u = __shfl_sync(0xffffffffu, u, 0);
         }
     }
     if (aborted && lane == 0) {
-        for (int jj = j; jj < njobs; ++jj) {
+        for (int jj = 0; jj < njobs; ++jj) {
             if (ld_acquire_gpu(done + jj) == 0) {
                 atomicExch(jobs[jj].counts + 3, (int)SS_ERR_CUDA);
                 __threadfence();

@@ -319,12 +319,17 @@ class DecodeEngine:
                     cs.wait_event(other.ev_attn[l])
             with torch.cuda.stream(cs):
                 _cache()
+                if gather and self.server:
+                    # job j's ready signal, then the event the group's stream waits on:
+                    # the done-flag wait below is ordered after its own job's signal in
+                    # the graph's edges, so it can never sit in a hardware queue in
+                    # front of the signal it depends on
+                    j = l * len(self.groups) + gi
+                    ops.flag_signal(self.h2d_flags[j:j + 1], stream=cs)
                 g.ev_cache[l].record(cs)
             if gather and self.server and c.split_attn:
                 # the hits (and the tail) are attended while the server loads the
                 # misses; then the misses, then the log-sum-exp merge
-                j = l * len(self.groups) + gi
-                ops.flag_signal(self.h2d_flags[j:j + 1], stream=cs)
                 g.stream.wait_event(g.ev_cache[l])
                 timed("attn", lambda: ops.sparse_decode_attn_part(
                     q, self.pool_kv_of(l, gi), g.slot[l], g.hit[l], 1, c.topk, g.tail_kv[l], g.tail_len, g.dims,
@@ -338,8 +343,7 @@ class DecodeEngine:
                 g.ev_attn[l].record(g.stream)
                 return
             if gather and self.server:
-                j = l * len(self.groups) + gi
-                ops.flag_signal(self.h2d_flags[j:j + 1], stream=cs)
+                g.stream.wait_event(g.ev_cache[l])
                 ops.flag_wait(self.h2d_flags[self.njobs + j:self.njobs + j + 1], stream=g.stream)
             elif gather:
                 g.h2d_stream.wait_event(g.ev_cache[l])
