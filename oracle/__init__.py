@@ -57,6 +57,9 @@ def lib():
         L.or_d2h_scatter.argtypes = [P, I64, P, P, I64, I64]
         L.or_prefill_save.argtypes = [P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P,
                                       P, I64]
+        L.or_ws_estimate.argtypes = [P, I32, I32, I32, I32, I32, I32, I32, P]
+        L.or_admit.argtypes = [P, I32, I64, P]
+        L.or_admit.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -278,3 +281,20 @@ def prefill_save(k_nhd: np.ndarray, v_nhd: np.ndarray, b: int, req: int, layer: 
     lib().or_prefill_save(_p(k_nhd), _p(v_nhd), n, b, req, layer, num_layers, max_blk, Hkv, d,
                           _dt(k_nhd), _p(meta), _p(tail), _p(n_blk), _p(tail_len), _p(host_kv_u8),
                           int(host_blocks))
+
+
+def ws_estimate(hist: np.ndarray, max_blk: int, w: int) -> np.ndarray:
+    """NEXT-2: hist int32 [T][L][B][Hkv][k] -> ws int64 [T][B] (blocks)."""
+    hist = np.ascontiguousarray(hist, dtype=np.int32)
+    T, L, B, Hkv, k = hist.shape
+    ws = np.zeros((T, B), np.int64)
+    lib().or_ws_estimate(_p(hist), T, L, B, Hkv, k, max_blk, w, _p(ws))
+    return ws
+
+
+def admit(m_req, m_avl: int) -> list:
+    """Algorithm 1 lines 6-14: per request, True = added, False = reset."""
+    m = np.ascontiguousarray(np.asarray(m_req, dtype=np.int64).reshape(-1))
+    out = np.zeros(max(len(m), 1), np.uint8)
+    lib().or_admit(_p(m), len(m), int(m_avl), _p(out))
+    return [bool(x) for x in out[:len(m)]]

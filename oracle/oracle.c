@@ -29,6 +29,11 @@
  *                       score exactly like the min/max bound (M = m = mu)
  *   or_attention    S5  pinned: torch scaled_dot_product_attention (fp64, CPU)
  *                       when k covers all blocks; masked-dense equivalence
+ *   or_ws_estimate  NEXT-2 pinned: closed forms (constant selections -> k per
+ *                       head, disjoint selections -> min(t+1, w) k, w = 1 ->
+ *                       |sel|), monotone in w, brute-force Python set unions
+ *   or_admit        NEXT-2 pinned: hand-traced Algorithm 1 cases (greedy in
+ *                       order, later small requests still admitted, M_avl = 0)
  */
 #include <math.h>
 #include <stdint.h>
@@ -453,4 +458,56 @@ void or_prefill_save(const void* k, const void* v, int n_tok, int b, int req, in
     n_blk[b] = nb;
     tail_len[b] = rem;
     free(blk);
+}
+
+/* ------------------------------------------------------------------------
+ * NEXT-2  decoding working set (§3.3: "tracks the KV blocks
+ * selected over the past w decoding steps (with w = 12 by default) and regards
+ * their union as the decoding working set"; per-head selection).
+ *   hist: [T][L][B][Hkv][k] int32 selections of steps 0..T-1 (-1 = none).
+ *   ws:   [T][B] out: ws[t][b] = sum over l, h of
+ *         | union over s = max(0, t-w+1) .. t of hist[s][l][b][h][:] |  (blocks).
+ * Written straight from the definition: a mark array per (t, b, l, h).
+ * ---------------------------------------------------------------------- */
+void or_ws_estimate(const int32_t* hist, int T, int L, int B, int Hkv, int k, int max_blk, int w,
+                    int64_t* ws) {
+    unsigned char* mark = (unsigned char*)malloc((size_t)(max_blk > 0 ? max_blk : 1));
+    for (int t = 0; t < T; ++t)
+        for (int b = 0; b < B; ++b) {
+            int64_t tot = 0;
+            for (int l = 0; l < L; ++l)
+                for (int h = 0; h < Hkv; ++h) {
+                    memset(mark, 0, (size_t)(max_blk > 0 ? max_blk : 1));
+                    int s0 = t - w + 1 < 0 ? 0 : t - w + 1;
+                    for (int s = s0; s <= t; ++s)
+                        for (int i = 0; i < k; ++i) {
+                            int32_t j = hist[((((int64_t)s * L + l) * B + b) * Hkv + h) * k + i];
+                            if (j >= 0 && j < max_blk && !mark[j]) { mark[j] = 1; ++tot; }
+                        }
+                }
+            ws[(int64_t)t * B + b] = tot;
+        }
+    free(mark);
+}
+
+/* ------------------------------------------------------------------------
+ * NEXT-2  Algorithm 1 lines 6-14: B_res <- {}, M_used <- 0;
+ * for req in B_init (in order): M_req <- estimateWS(req); if M_used + M_req <=
+ * M_avl then B_res.add(req), M_used += M_req else S.reset(req).
+ *   m_req [n] (estimateWS results), admit [n] out (1 added / 0 reset).
+ *   Returns |B_res|.
+ * ---------------------------------------------------------------------- */
+int or_admit(const int64_t* m_req, int n, int64_t m_avl, uint8_t* admit) {
+    int64_t m_used = 0;
+    int cnt = 0;
+    for (int i = 0; i < n; ++i) {
+        if (m_used + m_req[i] <= m_avl) {
+            admit[i] = 1;
+            m_used += m_req[i];
+            ++cnt;
+        } else {
+            admit[i] = 0;
+        }
+    }
+    return cnt;
 }

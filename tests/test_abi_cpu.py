@@ -92,7 +92,9 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
 
 
 def test_ss_admit_matches_algorithm1(lib):
-    # PAPER.md:159-183 Algorithm 1 lines 6-14, restated in Python as the check
+    # PAPER.md:159-183 Algorithm 1 lines 6-14: host logic vs the oracle's or_admit
+    # (pinned by hand-traced cases in test_oracle_pins.py) and a Python restatement
+    import oracle
     from paper_2509_24626_b200 import ops
     import random
     rnd = random.Random(5)
@@ -106,4 +108,4 @@ def test_ss_admit_matches_algorithm1(lib):
                 used += m
             else:
                 exp.append(False)
-        assert ops.ss_admit(ws, m_avl) == exp
+        assert ops.ss_admit(ws, m_avl) == exp == oracle.admit(ws, m_avl)

@@ -1,10 +1,13 @@
 """NEXT-2 parity: the incremental working-set tracker (union
-of the blocks selected over the past w = 12 decoding steps) against Python set
-unions of the same selections, over many steps, several layers and heads."""
+of the blocks selected over the past w = 12 decoding steps) against the oracle's
+or_ws_estimate (the union written from its definition, pinned in
+tests/test_oracle_pins.py) on the same selections, over many steps, several
+layers and heads."""
 import numpy as np
 import pytest
 import torch
 
+import oracle
 from layout import to_torch
 
 pytestmark = pytest.mark.gpu
@@ -18,9 +21,10 @@ def test_ws_track_equals_set_union():
     L, B, Hkv, k, max_blk, w = 3, 4, 2, 16, 200, 12
     st = ops.WorkingSetState(L, B, Hkv, max_blk, k, w)
     d = ops.dims(B, Hkv, Hkv)
-    hist = {}                          # (l, b, h) -> list of selected sets
+    steps = []                         # [t] -> [L][B][Hkv][k] selections
     prev = {}
     for t in range(40):
+        step = np.full((L, B, Hkv, k), -1, np.int32)
         for l in range(L):
             sel = np.full((B, Hkv, k), -1, np.int32)
             for b in range(B):
@@ -33,10 +37,10 @@ def test_ws_track_equals_set_union():
                     s = sorted(keep)[:kk]
                     sel[b, h, :len(s)] = s
                     prev[(l, b, h)] = s
-                    hist.setdefault((l, b, h), []).append(set(s))
+            step[l] = sel
             ops.ws_track(st, l, to_torch(sel), k, d, max_blk, t)
+        steps.append(step)
         torch.cuda.synchronize()
         got = st.ws_count.cpu().numpy()
-        for b in range(B):
-            exp = sum(len(set().union(*hist[(l, b, h)][-w:])) for l in range(L) for h in range(Hkv))
-            assert got[b] == exp, (t, b, got[b], exp)
+        exp = oracle.ws_estimate(np.stack(steps), max_blk, w)[t]
+        assert (got == exp).all(), (t, got, exp)

@@ -511,3 +511,55 @@ def test_mean_score_of_identical_tokens_equals_minmax_score():
     s_mean = oracle.block_score_mean(qs, mu, np.array([6], np.int32))
     s_mm = oracle.block_score(qs, _meta_from_blocks(ks, 1, 1, 6), np.array([6], np.int32))
     np.testing.assert_array_equal(s_mean, s_mm)
+
+
+# ----------------------------------------------------------------------------
+# NEXT-2 decoding working set (§3.3) and Algorithm 1
+# ----------------------------------------------------------------------------
+def test_ws_estimate_closed_forms():
+    T, L, B, Hkv, k, mb = 20, 2, 3, 2, 5, 400
+    # the same k blocks every step: the union never grows past k per head
+    const = np.broadcast_to(np.arange(k, dtype=np.int32), (T, L, B, Hkv, k))
+    for w in (1, 4, 12):
+        assert (oracle.ws_estimate(const, mb, w) == L * Hkv * k).all()
+    # disjoint selections every step: the union is min(t+1, w) * k per head
+    disj = (np.arange(T, dtype=np.int32)[:, None, None, None, None] * k
+            + np.arange(k, dtype=np.int32)) * np.ones((1, L, B, Hkv, 1), np.int32)
+    for w in (1, 3, 12):
+        ws = oracle.ws_estimate(disj, mb, w)
+        for t in range(T):
+            assert (ws[t] == L * Hkv * min(t + 1, w) * k).all()
+    # empty selections count nothing; -1 entries are not blocks
+    assert (oracle.ws_estimate(np.full((T, L, B, Hkv, k), -1, np.int32), mb, 12) == 0).all()
+
+
+def test_ws_estimate_brute_force_and_monotone_in_w():
+    rng = np.random.default_rng(3)
+    T, L, B, Hkv, k, mb = 16, 2, 2, 3, 6, 40
+    hist = rng.integers(-1, mb, size=(T, L, B, Hkv, k)).astype(np.int32)
+    prev = None
+    for w in (1, 2, 5, 12, 16):
+        ws = oracle.ws_estimate(hist, mb, w)
+        for t in range(T):
+            for b in range(B):
+                exp = sum(len({int(j) for s in range(max(0, t - w + 1), t + 1)
+                               for j in hist[s, l, b, h] if j >= 0})
+                          for l in range(L) for h in range(Hkv))
+                assert ws[t, b] == exp
+        if w == 1:   # w = 1: the working set is this step's distinct selections
+            assert (ws == np.array([[sum(len(set(hist[t, l, b, h][hist[t, l, b, h] >= 0].tolist()))
+                                         for l in range(L) for h in range(Hkv))
+                                     for b in range(B)] for t in range(T)])).all()
+        if prev is not None:  # Fig. 8: a longer window never shrinks the union
+            assert (ws >= prev).all()
+        prev = ws
+
+
+def test_admit_hand_traced_algorithm1():
+    # M_avl = 10: 4 (used 4) add; 7 (11 > 10) reset; 6 (10) add; 1 (11) reset; 0 (10) add
+    assert oracle.admit([4, 7, 6, 1, 0], 10) == [True, False, True, False, True]
+    # a large request early is reset, later small ones still fit (no early stop)
+    assert oracle.admit([20, 3, 3, 3], 9) == [False, True, True, True]
+    assert oracle.admit([1, 2], 0) == [False, False]
+    assert oracle.admit([0, 0], 0) == [True, True]
+    assert oracle.admit([], 5) == []
