@@ -116,7 +116,7 @@ class ClockSampler:
 # ----------------------------------------------------------------------------
 # workload
 # ----------------------------------------------------------------------------
-HOST_AHEAD_CYCLES = 10_000_000   # ~5 ms at 1.965 GHz (torch.cuda._sleep spins SM cycles)
+HOST_AHEAD_CYCLES = int(os.environ.get("SS_HOST_AHEAD_CYCLES", 40_000_000))  # ~20 ms at 1.965 GHz (torch.cuda._sleep spins SM cycles)
 
 
 def workload_cfg(args, world: int):
