@@ -39,7 +39,8 @@ namespace ss {
 
 constexpr int kSelThreads = 256;
 constexpr int kSelWarps = kSelThreads / 32;
-constexpr int kSelChunkMax = 2048;  // blocks per CTA (upper bound; smem sizing)
+constexpr int kSelChunkMax = 4096;  // blocks per CTA (upper bound; smem sizing)
+constexpr int kSelChunkGqa = 2048;  // measured best at C3 (tools/kbench.py)
 constexpr int kSelChunkDefault = 1024;  // measured best at C2 (tools/kbench.py)
 constexpr int kSelMaxMerge = 8192;
 
@@ -548,7 +549,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
 // the top-k).  Measured (tools/kbench.py, C2 / C3 full batch and one request
 // group): a chooser that sized chunks to fill whole waves of resident CTAs lost
 // to these fixed sizes everywhere (smaller chunks pay more top-k and merge work
-// than the wave tail costs).  SS_SEL_CHUNK (multiple of 32, <= 2048) overrides.
+// than the wave tail costs).  SS_SEL_CHUNK (multiple of 32, <= 4096) overrides.
 static int sel_chunk_env() {
     static const int env = [] {
         const char* e = getenv("SS_SEL_CHUNK");
@@ -560,9 +561,12 @@ static int sel_chunk_env() {
 }
 constexpr int kSelChunkMin = 512;  // workspace sizing bound (SS_SEL_CHUNK may go lower)
 
-static int sel_chunk(int G, size_t, int, int, int) {
-    if (sel_chunk_env()) return sel_chunk_env();
-    return G > 1 ? kSelChunkMax : kSelChunkDefault;
+// The chunk a call uses; doubled (up to kSelChunkMax) while the candidate merge
+// of the pair's chunks would exceed kSelMaxMerge keys (its shared-memory bound).
+static int sel_chunk(int G, int max_blk, int k) {
+    int ch = sel_chunk_env() ? sel_chunk_env() : (G > 1 ? kSelChunkGqa : kSelChunkDefault);
+    while ((size_t)((max_blk + ch - 1) / ch) * k > kSelMaxMerge && ch < kSelChunkMax) ch *= 2;
+    return ch;
 }
 
 // Workspace: tickets [pairs] first (fixed place: they must stay zero between
@@ -584,8 +588,7 @@ static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_
                               int k, const ss_dims& d, int32_t* sel, double* scores, void* ws,
                               cudaStream_t stream) {
     size_t pairs = (size_t)d.batch * d.num_kv_heads;
-    constexpr int kCtasPerSm = (G > 1 && !MEAN && TT == 1) ? 3 : 2;  // = __launch_bounds__
-    const int CH = sel_chunk(G, pairs, max_blk, k, kCtasPerSm * kNumSMs);
+    const int CH = sel_chunk(G, max_blk, k);
     int nchunks = (max_blk + CH - 1) / CH;
     size_t nc = pairs * nchunks * k;
     int32_t* tickets = (int32_t*)ws;
@@ -615,7 +618,7 @@ ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_
                               void* ws, cudaStream_t stream, bool mean) {
     int G = d.num_q_heads / d.num_kv_heads;
     {   // the largest chunk must keep the candidate merge within kSelMaxMerge keys
-        const int ch = sel_chunk_env() ? sel_chunk_env() : kSelChunkMax;
+        const int ch = sel_chunk(G, max_blk, k);  // the chunk the launch will use
         const int nchunks = (max_blk + ch - 1) / ch;
         if ((size_t)nchunks * k > kSelMaxMerge && nchunks > 1) return SS_ERR_UNSUPPORTED;
     }

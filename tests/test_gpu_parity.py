@@ -117,6 +117,14 @@ def test_select_ties_and_k_edges(ops, k):
     _select_case(ops, synth.DT_BF16, 2, 4, 4, [300, 96], k, seed=20 + k, ties=True)
 
 
+@pytest.mark.parametrize("G", [1, 4])
+def test_select_large_k_many_chunks_merge_bound(ops, G):
+    # 1M-token context (32768 blocks) with k = 300: at the default chunk the pair's
+    # candidates (32 x 300 for G = 1, 16 x 300 for G = 4) would exceed the merge's
+    # 8192-key shared-memory bound, so the call must widen its chunk, not overflow
+    _select_case(ops, synth.DT_BF16, 1, G, 1, [32768], 300, seed=40 + G)
+
+
 def test_select_needles_selected(ops):
     sel = _select_case(ops, synth.DT_BF16, 2, 8, 8, [700, 64], 4, seed=30, needle=True)
     assert (sel[:, :, 0] >= 0).all()
