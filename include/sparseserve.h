@@ -110,7 +110,9 @@ ss_status block_meta_update(const void* keys, int64_t key_stride, const int64_t*
  *            written in ascending j, -1 padded.
  *   scores   device float64 [B][Hkv][max_blk] out (j < n_blk only), or NULL.
  *   ws       device workspace of ss_workspace_size(SS_WS_SELECT, ...) bytes,
- *            ZERO-FILLED ONCE before first use; every call leaves it zeroed. */
+ *            ZERO-FILLED ONCE before first use; every call leaves it zeroed.
+ * Returns SS_ERR_UNSUPPORTED (nothing launched) when ceil(max_blk / 4096) * k >
+ * 8192: the per-pair candidate merge would exceed its shared-memory bound. */
 ss_status ss_block_select(const void* q, const void* meta, const int32_t* n_blk,
                           int32_t max_blk, int32_t k, ss_dims dims, ss_dtype dt, int32_t* sel,
                           double* scores, void* ws, size_t ws_bytes, void* stream);
