@@ -9,8 +9,14 @@ KV in pinned host DRAM).  Attention-path only: no QKV/O projections or FFN.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (the
-reference arm of this tier) on a bounded sample of the same workload.
+Prints ONE JSON line (rank 0).  `--gpus N` (N > 1) without a torchrun
+environment re-launches itself under `torch.distributed.run` with N ranks (one
+process per GPU, NCCL), failing loudly if fewer than N GPUs are visible.  Each
+rank owns Hkv/N KV heads of 16*N requests (weak scaling: the per-GPU work is
+the N = 1 workload), runs the N = 1 launch configuration (request groups,
+FlashH2D server, one CUDA graph per step) and all-gathers every layer's
+per-head outputs (S6) inside that graph.  `--impl reference` times the CPU
+oracle (the reference arm of this tier) on the box's host cores.
 """
 from __future__ import annotations
 
@@ -124,11 +130,13 @@ def workload_cfg(args, world: int):
     # (configs[2], Llama-3-8B GQA 1M-context FlashH2D stress) with --config C3
     wl = synth.C3 if args.config == "C3" else synth.C2
     batch = wl.batch * world                     # weak scaling: per-GPU batch fixed
-    assert wl.num_kv_heads % world == 0, "KV heads must divide across ranks"
+    if wl.num_kv_heads % world:
+        raise SystemExit(f"{wl.num_kv_heads} KV heads do not split over {world} ranks")
+    rho = wl.rho if args.rho is None else args.rho
     return dict(name=wl.name, batch=batch, layers=wl.layers, num_q_heads=wl.num_q_heads,
                 num_kv_heads=wl.num_kv_heads, n_blk=wl.n_blk, max_blk=wl.max_blk, topk=wl.topk,
                 slots=auto_slots(args, wl, batch, world) if args.slots < 0 and wl is synth.C2
-                else (args.slots if args.slots > 0 else wl.slots_per_layer), rho=wl.rho, context=wl.context)
+                else (args.slots if args.slots > 0 else wl.slots_per_layer), rho=rho, context=wl.context)
 
 
 def auto_slots(args, wl, batch, world, reserve_gib=12):
@@ -143,6 +151,26 @@ def auto_slots(args, wl, batch, world, reserve_gib=12):
     s = (free - meta - fwd - (reserve_gib << 30)) // per_slot
     s = min(s, batch * hkv * wl.n_blk)
     return max(wl.slots_per_layer, int(s) // 4096 * 4096)
+
+
+def _is_prime(n):
+    return n > 1 and all(n % p for p in range(2, int(n ** 0.5) + 1))
+
+
+def host_runs_for(args, max_blk, block_bytes, world):
+    """Physical host pool = runs x max_blk blocks (logical blocks alias onto it,
+    DESIGN.md R15).  --host-runs, capped so that all ranks' pinned pools stay
+    within 60 % of the host's RAM; a prime number of runs spreads the aliasing."""
+    want = args.host_runs if max_blk <= 4096 else max(1, (args.host_runs * 4096) // max_blk)
+    try:
+        mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+        cap = int(0.6 * mem / world) // (max_blk * block_bytes)
+    except (ValueError, OSError):
+        cap = want
+    r = max(1, min(want, cap))
+    while r > 2 and not _is_prime(r):
+        r -= 1
+    return r
 
 
 def gen_host_blocks_on_gpu(engine, host_t, phys_blocks, seed, meta_phys, chunk_blocks=16384):
@@ -162,9 +190,11 @@ def gen_host_blocks_on_gpu(engine, host_t, phys_blocks, seed, meta_phys, chunk_b
         ops.block_meta_update(xb, meta_phys[s * 2 * 128:], n, key_stride=be)
         host_t[s * be:(s + n) * be].copy_(xb.view(-1), non_blocking=False)
         del x, xb
+    torch.cuda.synchronize()
 
 
-def setup_engine(args, rank: int, world: int):
+def setup_engine(args, rank: int, world: int, local: int):
+    from paper_2509_24626_b200 import ops
     from paper_2509_24626_b200.engine import DecodeEngine, EngineConfig
     W = workload_cfg(args, world)
     hkv = W["num_kv_heads"] // world
@@ -176,13 +206,16 @@ def setup_engine(args, rank: int, world: int):
                        cache_per_group=args.cache_per_group, h2d_server=bool(args.h2d_server),
                        split_attn=bool(args.split_attn), pool_per_group=bool(args.pool_per_group))
     eng = DecodeEngine(cfg)
-    # physical host pool: a prime number of max_blk runs (aliasing, R15)
-    runs = args.host_runs if cfg.max_blk <= 4096 else max(1, (args.host_runs * 4096) // cfg.max_blk)
+    # this rank's physical host pool: pinned, device-mapped, on its GPU's NUMA
+    # node (ss_host_alloc); logical blocks alias onto it (R15)
+    runs = host_runs_for(args, cfg.max_blk, cfg.block_bytes, world)
     phys = runs * cfg.max_blk
-    host_t = torch.empty(phys * cfg.block_elems, dtype=torch.bfloat16, pin_memory=True)
+    hp = ops.HostPool(phys * cfg.block_bytes, device=local)
+    host_t = hp.tensor.view(torch.bfloat16)
     meta_phys = torch.empty(phys * 2 * 128, dtype=torch.bfloat16, device="cuda")
     gen_host_blocks_on_gpu(eng, host_t, phys, seed=4000 + rank, meta_phys=meta_phys)
-    eng.set_host_kv(host_t, phys)
+    eng.set_host_kv(host_t, phys, dev_ptr=hp.dev_ptr)
+    eng.host_pool = hp                          # keeps the pinned pool alive
     # logical metadata of (b, l, h, j) = metadata of physical block key % phys:
     # whole 32-block tiles move together (key0 % phys is a multiple of max_blk)
     tiles_per_pair = cfg.max_blk // 32
@@ -198,6 +231,9 @@ def setup_engine(args, rank: int, world: int):
     eng.n_blk.fill_(W["n_blk"])
     eng.tail_len.zero_()
     torch.cuda.synchronize()
+    W["host_pool"] = {"blocks": phys, "gib": round(phys * cfg.block_bytes / 2**30, 2),
+                      "logical_gib": round(cfg.batch * cfg.layers * hkv * W["n_blk"] * cfg.block_bytes / 2**30, 1),
+                      "numa_node": hp.numa_node, "numa_bound": hp.numa_bound}
     return eng, W
 
 
@@ -250,25 +286,6 @@ class StepTimers:
 
     def counts(self):
         return {k: len(v) for k, v in self.ev.items()}
-
-
-def run_step(eng, q_step, stamp, timers=None, pgs=None, world=1, gathered=None):
-    """One decode step of every layer through the engine (S1..S5 per layer and
-    request group); with N > 1 ranks, S6 = all-gather of each layer's per-head
-    outputs on the group's stream right after its attention."""
-    hook = None
-    if world > 1:
-        from paper_2509_24626_b200.shard import gather_outputs
-
-        def hook(gi, g, l):
-            if timers is None:
-                gather_outputs(g.out[l], gathered[gi][l], group=pgs[gi])
-            else:
-                s, e = timers.mark("allgather")
-                s.record()
-                gather_outputs(g.out[l], gathered[gi][l], group=pgs[gi])
-                e.record()
-    eng.step(q_step, stamp, timers=timers, post_attn=hook)
 
 
 def solo_pass(eng, q_src, layers, hbm_peak, h2d_peak, stamp):
@@ -372,49 +389,131 @@ def measure_h2d_peak(nbytes=1 << 30):
     return gbs
 
 
-def cpu_sample(eng, W, q_np_step, n_req=1, n_layers=1):
-    """Time the oracle (as it stands, single thread) on a bounded sample of the
-    same workload: n_req requests x n_layers layers x all KV heads of one step
-    (S1..S5 from an empty pool; the metadata of the sampled blocks is built
-    first, untimed -- S0 runs once per 32 steps).  Returns (tokens/s
-    extrapolated to all layers, seconds timed, description)."""
-    import oracle
+# ----------------------------------------------------------------------------
+# the oracle on the host cores (cpu_baseline and the reference arm)
+# ----------------------------------------------------------------------------
+def cpu_info():
+    cores = len(os.sched_getaffinity(0))
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return cores, model
+
+
+class OracleDecoder:
+    """The oracle (oracle/, as it stands) decoding whole steps of a workload on
+    the host cores.  One task = one request's layer call, S1..S5 over its Hkv
+    KV heads (oracle.decode_layer).  Requests are independent: each has its own
+    batch-LRU pool over all layers (slots = 4 x one call's demand; the pools
+    share one key->slot table, their keys never collide), so a layer's tasks
+    run on `threads` host threads at once (ctypes releases the GIL).  The
+    metadata of the physical host pool is built by the oracle too (S0, untimed:
+    it runs once per 32 steps); logical block (b, l, h, j) aliases physical
+    block key % phys exactly as on the GPU (R15)."""
+
+    def __init__(self, blocks_u16, phys, W, hkv, hq, threads):
+        import oracle
+        from concurrent.futures import ThreadPoolExecutor
+        self.oracle = oracle
+        self.phys, self.L, self.B = phys, W["layers"], W["batch"]
+        self.Hkv, self.Hq, self.max_blk, self.n_blk, self.k = hkv, hq, W["max_blk"], W["n_blk"], W["topk"]
+        self.threads = max(1, threads)
+        self.ex = ThreadPoolExecutor(self.threads)
+        self.host_u8 = blocks_u16.view(np.uint8).reshape(phys, -1)
+        meta = np.empty((phys, 2, 128), np.uint16)
+        step = (phys + self.threads - 1) // self.threads
+
+        def s0(s):
+            meta[s:s + step] = oracle.block_meta(blocks_u16[s:s + step], key_stride=2 * 32 * 128)
+        list(self.ex.map(s0, range(0, phys, step)))
+        self.meta = meta
+        self.fwd = np.full(self.B * self.L * hkv * self.max_blk, -1, np.int32)
+        self.pools = {}
+        self.tail = np.zeros((1, hkv, 2, 32, 128), np.uint16)
+        self.tail_len = np.zeros(1, np.int32)
+        self.scale = 1.0 / math.sqrt(128)
+
+    def pool(self, b):
+        if b not in self.pools:
+            p = self.oracle.Pool(4 * self.Hkv * self.k, 1, 16384)
+            p.fwd = self.fwd
+            self.pools[b] = p
+        return self.pools[b]
+
+    def call(self, b, l, q_bl, stamp):
+        M = self.max_blk
+        start = (((b * self.L + l) * self.Hkv) * M) % self.phys
+        if start + self.Hkv * M <= self.phys:       # the Hkv runs are contiguous: a view
+            meta = self.meta[start:start + self.Hkv * M].reshape(1, self.Hkv, M, 2, 128)
+        else:
+            meta = np.stack([self.meta[(start + h * M) % self.phys:(start + h * M) % self.phys + M]
+                             for h in range(self.Hkv)])[None]
+        self.oracle.decode_layer(q_bl[None], meta, np.array([self.n_blk], np.int32), self.k, self.pool(b),
+                                 np.array([b], np.int32), l, self.L, M, stamp, self.host_u8, self.phys,
+                                 self.tail, self.tail_len, self.scale)
+
+    def run(self, q_step, stamp, layers, requests, threads=None):
+        """q_step: uint16 [L][B][Hq][128].  Layers in order; a layer's requests in
+        parallel (or one by one with threads=1).  Returns wall seconds."""
+        t0 = time.perf_counter()
+        for l in layers:
+            if (threads or self.threads) == 1:
+                for b in requests:
+                    self.call(b, l, q_step[l, b], stamp)
+            else:
+                list(self.ex.map(lambda b: self.call(b, l, q_step[l, b], stamp), requests))
+        return time.perf_counter() - t0
+
+
+def cpu_baseline_sample(eng, W, q_np_step, layers_multi=6, tasks_single=8):
+    """cpu_baseline: the oracle on a bounded sample of this run's workload and
+    host pool, single-threaded and on every allowed core.  Returns the dict for
+    the JSON line (tokens/s extrapolated from the sampled layers to whole steps;
+    labelled)."""
     c = eng.cfg
-    host_np = eng.host_kv.view(torch.int16).numpy().view(np.uint16)
-    blocks = host_np.reshape(eng.host_blocks, 2, 32, 128)
-    metas = []
-    for l in range(n_layers):
-        meta = np.empty((n_req, c.num_kv_heads, c.max_blk, 2, 128), np.uint16)
-        for b in range(n_req):
-            for h in range(c.num_kv_heads):
-                p0 = eng.key0(b, l, h) % eng.host_blocks
-                meta[b, h, :W["n_blk"]] = oracle.block_meta(blocks[p0:p0 + W["n_blk"]], key_stride=2 * 32 * 128)
-        metas.append(meta)
-    t0 = time.perf_counter()
-    for l in range(n_layers):
-        pool = oracle.Pool(n_req * c.num_kv_heads * c.topk, c.fwd_len, c.block_bytes)
-        oracle.decode_layer(q_np_step[l, :n_req], metas[l], np.full(n_req, W["n_blk"], np.int32), c.topk,
-                            pool, np.arange(n_req, dtype=np.int32), l, c.layers, c.max_blk, 1,
-                            host_np.view(np.uint8).reshape(eng.host_blocks, -1), eng.host_blocks,
-                            np.zeros((n_req, c.num_kv_heads, 2, 32, 128), np.uint16),
-                            np.zeros(n_req, np.int32), eng.scale)
-    dt = time.perf_counter() - t0
-    per_step_s = dt / n_layers * c.layers / n_req        # seconds per request-step, all layers
-    desc = (f"{n_req} request(s) x {n_layers} layer(s) x {c.num_kv_heads} KV heads of one {W['name']} decode step "
-            f"(S1..S5 from an empty pool, metadata prebuilt), extrapolated x{c.layers} layers")
-    return 1.0 / per_step_s, dt, desc
+    cores, model = cpu_info()
+    blocks = eng.host_kv.view(torch.int16).numpy().view(np.uint16).reshape(eng.host_blocks, 2, 32, 128)
+    t_setup = time.perf_counter()
+    od = OracleDecoder(blocks, eng.host_blocks, W, c.num_kv_heads, c.num_q_heads, cores)
+    setup_s = time.perf_counter() - t_setup
+    reqs = list(range(c.batch))
+    # single thread: `tasks_single` request-layer calls of layer 0
+    t1 = od.run(q_np_step, 1, [0], reqs[:tasks_single], threads=1)
+    tok1 = (tasks_single / c.batch) / (t1 * c.layers) * c.batch     # request-steps per second
+    # all cores: layers 1..layers_multi, every request of each layer in parallel
+    tm = od.run(q_np_step, 1, list(range(1, 1 + layers_multi)), reqs)
+    tokm = c.batch / (tm * c.layers / layers_multi)
+    od.ex.shutdown()
+    return {"value": round(tokm, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "cpu_model": model,
+            "sample": (f"oracle S1..S5 (oracle.decode_layer) on {layers_multi} of {c.layers} layers x all {c.batch} "
+                       f"requests x {c.num_kv_heads} KV heads of one {W['name']} decode step, the layer's requests "
+                       f"on {cores} host threads; tokens/s extrapolated x{c.layers}/{layers_multi} layers"),
+            "seconds": round(tm, 3), "cpu_seconds_approx": round(tm * cores, 1),
+            "single_thread": {"value": round(tok1, 4), "unit": "tokens/s", "cores": 1,
+                              "sample": f"{tasks_single} request-layer calls (layer 0), extrapolated to whole steps",
+                              "seconds": round(t1, 3)},
+            "metadata_setup_s": round(setup_s, 2)}
 
 
 def bench_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # under torchrun (any world size, 1 included) the step runs the multi-GPU
+    # path: NCCL process group, S6 all-gather of every layer's outputs
+    dist_on = "WORLD_SIZE" in os.environ
     torch.cuda.set_device(local)
-    pgs = None
-    if world > 1:
+    if dist_on:
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     t_setup = time.time()
-    eng, W = setup_engine(args, rank, world)
+    eng, W = setup_engine(args, rank, world, local)
     c = eng.cfg
     e2e_steps = max(3, args.steps // 2)
     n_kt = max(3, min(args.steps, 8))                 # eager per-kernel timing pass
@@ -423,27 +522,37 @@ def bench_ours(args):
     t_kt = t_e2e + e2e_steps
     t_srv = t_kt + n_kt                               # server-only timing pass (h2d_server)
     srv_err = 0
-    qs = gen_queries(eng, t_srv + n_kt + 1, W["rho"], seed=5000 + rank)
-    gathered = None
-    if world > 1:
-        # one communicator per request group (their all-gathers run on different streams)
-        pgs = [torch.distributed.new_group(list(range(world))) for _ in eng.groups]
-        gathered = [torch.empty(c.layers, c.num_q_heads * world, g.nb, 128, dtype=torch.float32,
-                                device="cuda") for g in eng.groups]
+    t_stats = t_srv + n_kt                            # server statistics pass
+    qs = gen_queries(eng, t_stats + n_kt + 1, W["rho"], seed=5000 + rank)
+    gatherer = None
+    if dist_on:
+        # S6: one communicator per request group (their all-gathers run on the
+        # groups' streams), captured into the step graph with everything else
+        from paper_2509_24626_b200.shard import OutputGather
+        gatherer = OutputGather(eng, world)
     h2d_peak = measure_h2d_peak()
     gather_alone = None if args.no_gather_alone else measure_flash_h2d_alone(eng)
     setup_s = time.time() - t_setup
 
     def barrier():
-        if world > 1:
+        if dist_on:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    def allgather_hook():
-        if world == 1:
-            return None
-        from paper_2509_24626_b200.shard import gather_outputs
-        return lambda gi, g, l: gather_outputs(g.out[l], gathered[gi][l], group=pgs[gi])
+    def max_over_ranks(x):
+        if not dist_on:
+            return x
+        tt = torch.tensor([x], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        return float(tt.item())
+
+    def sum_over_ranks(t):
+        if dist_on:
+            torch.distributed.all_reduce(t)
+        return t
+
+    def allgather_hook(timers=None):
+        return None if gatherer is None else gatherer.hook(timers)
 
     # settle + warm-up (eager, host stamps 1..settle+W).  The first step is cold
     # (every block misses); the `settle` steps before the W warm-up steps bring
@@ -457,7 +566,7 @@ def bench_ours(args):
     for t in range(args.settle + args.warmup - n_gw):
         s, e = torch.cuda.Event(True), torch.cuda.Event(True)
         s.record()
-        run_step(eng, qs[t], stamp=t + 1, pgs=pgs, world=world, gathered=gathered)
+        eng.step(qs[t], t + 1, post_attn=allgather_hook())
         e.record()
         torch.cuda.synchronize()
         if t == 0:
@@ -481,7 +590,7 @@ def bench_ours(args):
         if graph is not None:
             graph.replay()
         else:
-            run_step(eng, q_static, stamp=t + 1, pgs=pgs, world=world, gathered=gathered)
+            eng.step(q_static, t + 1, post_attn=allgather_hook())
 
     def counts_sum(acc):
         for g in eng.groups:
@@ -514,24 +623,22 @@ def bench_ours(args):
     end.record()
     barrier()
     clocks = sampler.stop()
-    ms = start.elapsed_time(end)
-    if world > 1:
-        tt = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(start.elapsed_time(end))
     ms_step = ms / args.steps
     raw_steps = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
     per_step = sorted(raw_steps)
-    n_hits, n_miss, n_evict, n_err = cnt.cpu().tolist()
+    n_hits, n_miss, n_evict, n_err = sum_over_ranks(cnt).cpu().tolist()
     lookups = n_hits + n_miss
     hit_rate = n_hits / lookups if lookups else 0.0
-    value = c.batch * args.steps / (ms * 1e-3)        # batch counts every rank's requests
+    # whole-job throughput: c.batch counts every rank's requests (each rank
+    # holds Hkv/N heads of all of them), so this is tokens/s over the N GPUs
+    value = c.batch * args.steps / (ms * 1e-3)
 
     # ---- e2e through the public API with host buffers (right after the timed
     # region, so both see a comparable, warmed cache): every step copies its q
     # in from pinned host memory and its outputs out ----
     q_host = qs[t_e2e:t_e2e + e2e_steps].cpu().pin_memory()
-    outs = gathered if world > 1 else eng.outputs()
+    outs = gatherer.outputs() if gatherer is not None else eng.outputs()
     out_host = [torch.empty(o.shape, dtype=torch.float32, pin_memory=True) for o in outs]
     barrier()
     e_s, e_e = torch.cuda.Event(True), torch.cuda.Event(True)
@@ -545,11 +652,8 @@ def bench_ours(args):
         counts_sum(e2e_cnt)
     e_e.record()
     barrier()
-    e_ms = e_s.elapsed_time(e_e)
-    if world > 1:
-        tt = torch.tensor([e_ms], device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        e_ms = float(tt.item())
+    e_ms = max_over_ranks(e_s.elapsed_time(e_e))
+    sum_over_ranks(e2e_cnt)
     e2e = {"value": round(c.batch * e2e_steps / (e_ms * 1e-3), 2), "unit": "tokens/s",
            "h2d_bytes_per_step": int(q_host[0].numel() * q_host.element_size()),
            "d2h_bytes_per_step": int(sum(o.numel() * o.element_size() for o in out_host)),
@@ -562,10 +666,11 @@ def bench_ours(args):
     # copy of the step graph (event-record nodes), so the launch times are those
     # of the replayed step, free of host launch latency; eager otherwise ----
     kcnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    server_stats = None
     barrier()
     if graph is not None:
         timers = StepTimers(external=True)
-        tgraph = eng.capture_graph(q_static, post_attn=allgather_hook(), timers=timers)
+        tgraph = eng.capture_graph(q_static, post_attn=allgather_hook(timers), timers=timers)
         tgraph.replay()                  # untimed: the first launch uploads the graph
         torch.cuda.synchronize()
         tot = {k: 0.0 for k in timers.ev}
@@ -599,13 +704,37 @@ def bench_ours(args):
             del sgraph
             srv_miss = int(srv_cnt[1])
             srv_err = int(srv_cnt[3])
+            # the server's own statistics (include/sparseserve.h flash_h2d_serve
+            # stats): link idle time between its first and last unit, per step
+            eng.collect_h2d_stats = True
+            stgraph = eng.capture_graph(q_static, post_attn=allgather_hook())
+            stgraph.replay()
+            torch.cuda.synchronize()
+            idle, span, wait, warps = 0, 0, 0, 0
+            for t in range(t_stats, t_stats + n_kt):
+                q_static.copy_(qs[t], non_blocking=True)
+                stgraph.replay()
+                torch.cuda.synchronize()
+                st = eng.h2d_stats.cpu().tolist()
+                idle += st[4]
+                span += st[3] - st[2]
+                wait += st[0]
+                warps = st[1]
+            eng.collect_h2d_stats = False
+            del stgraph
+            server_stats = {"link_idle_frac": round(idle / max(1, span), 4),
+                            "busy_span_ms_per_step": round(span / n_kt / 1e6, 3),
+                            "warp_wait_frac": round(wait / max(1, warps * span), 4),
+                            "warps": warps, "steps": n_kt,
+                            "note": "flash_h2d_serve statistics (globaltimer): fraction of the span from the "
+                                    "step's first to its last 8 KiB unit during which no server warp was copying"}
     else:
         timers = StepTimers()
         k_s = torch.cuda.Event(True)
         k_s.record()
         for t in range(t_kt, t_kt + n_kt):
             q_static.copy_(qs[t], non_blocking=True)
-            run_step(eng, q_static, stamp=t + 1, timers=timers, pgs=pgs, world=world, gathered=gathered)
+            eng.step(q_static, t + 1, timers=timers, post_attn=allgather_hook(timers))
             counts_sum(kcnt)
         barrier()
         if args.timeline and rank == 0:
@@ -658,8 +787,12 @@ def bench_ours(args):
                                  "eager launches") + " on each kernel's launching stream; kernels of "
                                 "different request groups overlap, so a launch's time includes co-running work"},
     }
-    if world > 1:
-        kernels["nccl_all_gather"] = {"us_per_launch": round(tot["allgather"] * 1e3 / max(1, nlaunch["allgather"]), 2)}
+    if gatherer is not None:
+        kernels["nccl_all_gather"] = {"us_per_launch": round(tot["allgather"] * 1e3 / max(1, nlaunch["allgather"]), 2),
+                                      "launches_per_step": c.layers * len(eng.groups),
+                                      "bytes_per_launch_per_rank": int(c.num_q_heads * eng.groups[0].nb * 128 * 4),
+                                      "note": "NCCL all-gather of one request group's layer outputs, captured in "
+                                              "the step graph on the group's stream (time includes co-running work)"}
     # dominant kernel = the largest share of the step at each kernel's own roofline
     # (algorithmic bytes / peak).  The event times above are taken while request
     # groups overlap (a launch's time includes co-running kernels and waits for
@@ -690,20 +823,22 @@ def bench_ours(args):
     # ---- each kernel alone (its own roofline fraction, no co-running group) ----
     if graph is not None:
         eng.advance_clock()
-    q_static.copy_(qs[t_srv + n_kt])
-    kernels_solo = solo_pass(eng, q_static, min(4, c.layers), hbm_peak, h2d_peak, stamp=t_srv + n_kt + 1)
+    q_static.copy_(qs[t_stats + n_kt])
+    kernels_solo = solo_pass(eng, q_static, min(4, c.layers), hbm_peak, h2d_peak, stamp=t_stats + n_kt + 1)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         q_np = qs[0].view(torch.int16).cpu().numpy().view(np.uint16)
-        v, secs, desc = cpu_sample(eng, W, q_np, n_req=args.cpu_req, n_layers=args.cpu_layers)
-        cpu = {"value": round(v, 4), "unit": "tokens/s", "cores": 1, "kind": "oracle",
-               "sample": desc, "seconds": round(secs, 2)}
+        cpu = cpu_baseline_sample(eng, W, q_np)
+    errors = n_err + int(kcnt[3]) + (srv_err if eng.server and graph is not None else 0)
 
     meta_gib = c.layers * c.batch * c.num_kv_heads * c.max_blk * 2 * 128 * 2 / 2**30
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world,
+            "value_per_gpu": round(value / world, 2),
+            "value_note": "value = whole-job tokens/s over all ranks (bench contract); value_per_gpu = "
+                          "the metric's tokens/s/GPU",
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
             "step_ms_min_median_max": [round(per_step[0], 3), round(statistics.median(per_step), 3),
                                        round(per_step[-1], 3)],
@@ -714,8 +849,11 @@ def bench_ours(args):
                        "layers": c.layers, "q_heads": W["num_q_heads"], "kv_heads": W["num_kv_heads"],
                        "head_dim": 128, "context": W["context"], "block_tokens": 32,
                        "topk_blocks": c.topk, "hbm_cache_slots_per_layer": c.slots_per_layer,
-                       "host_pool_blocks": eng.host_blocks, "host_kv": "pinned DRAM, zero-copy (UVA)",
-                       "parallelism": f"kv-heads/{world} per GPU" if world > 1 else "1 GPU",
+                       "host_pool_blocks": eng.host_blocks, "host_pool": W["host_pool"],
+                       "host_kv": (f"pinned DRAM, zero-copy (UVA); {W['host_pool']['logical_gib']} GiB of logical KV "
+                                   f"aliased onto a {W['host_pool']['gib']} GiB physical pool per GPU (DESIGN.md R15)"),
+                       "parallelism": (f"kv-heads/{world} per GPU, NCCL all-gather per layer" if dist_on
+                                       else "1 GPU"),
                        "request_groups": len(eng.groups), "h2d_server": eng.server, "split_attn": bool(eng.server and eng.cfg.split_attn), "pool_per_group": eng.per_group_pools, "h2d_streams": args.h2d_streams, "select_priority": args.select_priority, "cache_per_group": args.cache_per_group,
                        "cuda_graph": graph is not None,
                        "cache_settle_steps": args.settle,
@@ -734,60 +872,94 @@ def bench_ours(args):
             "cold_step_ms": round(cold_ms, 2) if cold_ms else None,
             "e2e": e2e, "gpu_launches": int(args.steps * (c.layers * (8 if eng.server and eng.cfg.split_attn else 6) * len(eng.groups)
                                                  + (1 if eng.server else 0))),
+            "flash_h2d_server": server_stats,
             "cpu_baseline": cpu, "clocks": clocks, "setup_s": round(setup_s, 1),
             "errors_in_timed_region": n_err,
             "errors_in_timing_passes": int(kcnt[3]) + (srv_err if eng.server and graph is not None else 0),
         }
+        if errors:
+            # a device-side error (capacity, invalid key, aborted FlashH2D job)
+            # made some layer calls no-ops: the numbers are not a measurement
+            line["valid"] = False
+            line["invalid_reason"] = f"{errors} device-side error status(es) in the timed/timing passes"
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+    if errors:
+        sys.exit(3)
 
 
 # ----------------------------------------------------------------------------
-# reference arm: the CPU oracle on a bounded sample of the same workload
+# reference arm: the CPU oracle (this tier's reference) on the host cores
 # ----------------------------------------------------------------------------
 def bench_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    import oracle
+    """Whole decode steps of the workload by the oracle (OracleDecoder) on every
+    allowed host core: each timed step is one full N = 1 step -- all layers x all
+    requests x all KV heads -- so ms_per_step is a real measured time.  The
+    host pool is generated on the CPU (seeded, the recipe of DESIGN.md §4) and
+    aliased harder than the GPU run's (the work per block is the same)."""
     wl = synth.C3 if args.config == "C3" else synth.C2
-    G = wl.num_q_heads // wl.num_kv_heads
-    # bounded sample per step: 1 request x hkv KV heads (x G query heads) x 1 layer
-    n_req, hkv, n_blk, k = 1, (4 if G == 1 else 1), wl.n_blk, wl.topk
-    max_blk = wl.max_blk
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    W = dict(name=wl.name, batch=wl.batch, layers=wl.layers, n_blk=wl.n_blk, max_blk=wl.max_blk, topk=wl.topk)
+    rho = wl.rho if args.rho is None else args.rho
+    cores, model = cpu_info()
+    t0 = time.perf_counter()
+    runs = max(1, (11 * 4096) // wl.max_blk)          # 11 runs at C2 (704 MiB), 1 at C3
+    phys = runs * wl.max_blk
     rng = synth.rng_for(6000, 1)
     scales = synth.channel_scales(rng)
-    blocks = synth.encode(synth.kv_blocks(rng, hkv * n_blk, 128, scales), synth.DT_BF16)
-    host_u8 = blocks.view(np.uint8).reshape(hkv * n_blk, -1)
-    qs = synth.encode(synth.queries(rng, args.warmup + args.steps, (n_req, hkv * G, 128), wl.rho), synth.DT_BF16)
-    fwd_len = n_req * 1 * hkv * max_blk
-    pool = oracle.Pool(4 * hkv * k, fwd_len, 16384)
-    meta = oracle.block_meta(blocks, key_stride=2 * 32 * 128).reshape(n_req, hkv, n_blk, 2, 128)
-    times = []
-    for t in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        oracle.decode_layer(qs[t], meta, np.array([n_blk], np.int32), k, pool, np.zeros(1, np.int32), 0, 1,
-                            max_blk, t + 1, host_u8, hkv * n_blk, np.zeros((1, hkv, 2, 32, 128), np.uint16),
-                            np.zeros(1, np.int32), 1.0 / math.sqrt(128))
-        if t >= args.warmup:
-            times.append(time.perf_counter() - t0)
+    blocks = np.empty((phys, 2, 32, 128), np.uint16)
+    for s0 in range(0, phys, 8192):
+        n = min(8192, phys - s0)
+        blocks[s0:s0 + n] = synth.encode(synth.kv_blocks(rng, n, 128, scales), synth.DT_BF16)
+    od = OracleDecoder(blocks, phys, W, wl.num_kv_heads, wl.num_q_heads, cores)
+    qs = synth.encode(synth.queries(rng, args.warmup + args.steps,
+                                    (wl.layers, wl.batch, wl.num_q_heads, 128), rho), synth.DT_BF16)
+    setup_s = time.perf_counter() - t0
+    layers, reqs = list(range(wl.layers)), list(range(wl.batch))
+    for t in range(args.warmup):
+        od.run(qs[t], t + 1, layers, reqs)
+    times = [od.run(qs[args.warmup + i], args.warmup + i + 1, layers, reqs) for i in range(args.steps)]
+    od.ex.shutdown()
     sec = sum(times)
-    # one sampled step = 1 request x hkv of 32 KV heads x 1 of 32 layers
-    frac = (hkv / wl.num_kv_heads) / wl.layers
-    tok_s = args.steps * frac / sec
-    desc = (f"oracle S1..S5 on 1 request x {hkv} of {wl.num_kv_heads} KV heads x 1 of {wl.layers} layers "
-            f"of {wl.name} per step (metadata prebuilt), scaled to whole decode steps")
-    line = {"impl": "reference", "metric": METRIC, "value": round(tok_s, 5), "unit": "tokens/s",
-            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1e3 / tok_s * 1, 2), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": {"workload": wl.name},
-            "cpu_baseline": {"value": round(tok_s, 5), "unit": "tokens/s", "cores": 1, "kind": "oracle",
-                             "sample": desc},
-            "e2e": {"value": round(tok_s, 5), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+    tok_s = wl.batch * args.steps / sec
+    desc = (f"full {wl.name} decode steps by the oracle (S1..S5, oracle.decode_layer per request-layer, "
+            f"{wl.batch} requests x {wl.layers} layers x {wl.num_kv_heads} KV heads), a layer's requests on "
+            f"{cores} host threads; one LRU pool per request; host pool {phys} blocks (aliased)")
+    if world > 1:
+        desc += f"; at N={world} the oracle's rate per token is the same: each step samples 16 of the {16 * world} requests"
+    line = {"impl": "reference", "metric": METRIC, "value": round(tok_s, 4), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * sec / args.steps, 1),
+            "step_ms_min_median_max": [round(1e3 * min(times), 1), round(1e3 * statistics.median(times), 1),
+                                       round(1e3 * max(times), 1)],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": wl.name, "global_batch": wl.batch * world,
+                                            "layers": wl.layers, "rho": rho},
+            "timed_seconds": round(sec, 2), "setup_s": round(setup_s, 1),
+            "cpu_baseline": {"value": round(tok_s, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "cpu_model": model, "sample": desc},
+            "e2e": {"value": round(tok_s, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def relaunch_distributed(args) -> int:
+    """--gpus N > 1 outside torchrun: start N ranks (one per GPU) with
+    torch.distributed.run on 127.0.0.1 and return their exit code."""
+    import socket
+    n_vis = torch.cuda.device_count()
+    if n_vis < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {n_vis} CUDA device(s) are visible\n")
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -807,8 +979,8 @@ def main():
                          "stress size; 0: the workload's SURVEY size)")
     ap.add_argument("--hit-trace", action="store_true",
                     help="print each settle/warm-up step's hit rate and time to stderr")
-    ap.add_argument("--cpu-req", type=int, default=2)
-    ap.add_argument("--cpu-layers", type=int, default=4)
+    ap.add_argument("--rho", type=float, default=None,
+                    help="query drift rho of q_{t+1} = rho q_t + sqrt(1-rho^2) xi (default: the workload's)")
     ap.add_argument("--timeline", default=None, help="write one step's op timeline (json, timing pass)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch kernels eagerly instead of replaying a captured CUDA graph per step")
@@ -836,15 +1008,17 @@ def main():
                     help="skip the FlashH2D-alone ceiling measurement (profiling runs: keeps launch counts fixed)")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        # multi-GPU: one request group per rank and eager launches (the TP
-        # all-gather goes on the single compute stream; no NCCL inside a graph)
-        args.groups = 1
-        args.graph = False
     if args.impl == "reference":
-        bench_reference(args)
-    else:
-        bench_ours(args)
+        # under torchrun (N > 1) rank 0 alone times the oracle; the other ranks exit
+        if int(os.environ.get("RANK", "0")) == 0:
+            bench_reference(args)
+        return
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        sys.exit(relaunch_distributed(args))
+    if world_env is not None and int(world_env) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
+    bench_ours(args)
 
 
 if __name__ == "__main__":

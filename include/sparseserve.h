@@ -210,22 +210,35 @@ ss_status flash_h2d_gather(const void* host_kv, int64_t host_blocks, const int64
 /* S4, pipelined form -- the same FlashH2D copy (§3.2.1) for
  * every gather of a decode step, served by ONE persistent launch so the host
  * link does not drain at each layer boundary.  Each job is one
- * flash_h2d_gather's arguments; jobs are served in array order.
+ * flash_h2d_gather's arguments; a warp always serves the lowest-numbered
+ * ready job with blocks left.
  *   jobs      device array of njobs ss_h2d_job (read-only except counts[3],
  *             see abort below).  pool_kv / max_misses / block_bytes as above.
- *   flags     device int32 [4*njobs + 1], ZEROED by the caller before the
- *             launch: [0,nj) ready, [nj,2nj) done, [2nj,4nj) server scratch,
- *             [4nj] abort.  Job j starts once ready[j] != 0 (set it with
- *             ss_flag_signal, stream-ordered after the job's
- *             kv_cache_lookup_insert); done[j] becomes 1 (release, GPU scope)
- *             after all of job j's blocks are in HBM -- wait for it with
- *             ss_flag_wait before reading the pool.
- *   Errors: a job not ready within 3 s (SS_SERVE_TIMEOUT_MS) aborts the
- *   server; every job not yet done then gets counts[3] = SS_ERR_CUDA and
- *   done = 1 (no waiter hangs; downstream attention becomes a no-op).  The
- *   launch never completes before every ready job is served, so a job whose
- *   producer runs only after the server (e.g. a profiler serialising kernels)
- *   aborts: use flash_h2d_gather there. */
+ *   flags     device int32 [SS_H2D_FLAGS(njobs)], ZEROED by the caller before
+ *             the launch: [0,nj) ready, [nj,2nj) done, [2nj,4nj) server
+ *             scratch, [4nj] abort.  Job j starts once ready[j] != 0 (set it
+ *             with ss_flag_signal, stream-ordered after the job's
+ *             kv_cache_lookup_insert); done[j] becomes SS_H2D_DONE_SERVED
+ *             (release, GPU scope) after all of job j's blocks are in HBM --
+ *             wait for it with ss_flag_wait before reading the pool.
+ *   timeout_us  abort after this long with no ready job (<= 0: 3 s).
+ *   stats_or_null  device uint64 [SS_H2D_STATS], zeroed by the caller, or
+ *             NULL: [0] sum over the server's warps of ns with nothing to
+ *             serve, [1] warps, [2] first unit start / [3] last unit end
+ *             (globaltimer ns), [4] ns between them with NO warp copying
+ *             (link idle), [5] 1 + the job found not ready at an abort (0:
+ *             none); [6..7] scratch.
+ *   Errors: on abort every job not yet done gets done = SS_H2D_DONE_ABORTED
+ *   (and counts[3] = SS_ERR_CUDA); its ss_flag_wait, which runs after the
+ *   job's producer, then sets counts[3] = SS_ERR_CUDA again so a producer
+ *   that ran late cannot clear it: the attention becomes a no-op and the
+ *   error stays visible.  The launch never completes before every ready job
+ *   is served, so a job whose producer runs only after the server (e.g. a
+ *   profiler serialising kernels) aborts: use flash_h2d_gather there. */
+#define SS_H2D_FLAGS(njobs) (4 * (njobs) + 1)
+#define SS_H2D_STATS 8
+#define SS_H2D_DONE_SERVED 1
+#define SS_H2D_DONE_ABORTED 2
 typedef struct {
     const int64_t* miss_keys;
     const int32_t* miss_slots;
@@ -236,22 +249,27 @@ typedef struct {
 } ss_h2d_job;
 
 ss_status flash_h2d_serve(const void* host_kv, int64_t host_blocks, const ss_h2d_job* jobs,
-                          int32_t njobs, int64_t block_bytes, int32_t* flags, void* stream);
+                          int32_t njobs, int64_t block_bytes, int32_t* flags, int64_t timeout_us,
+                          uint64_t* stats_or_null, void* stream);
 
 /* Stream-ordered flag signal / wait for flash_h2d_serve.
  *   ss_flag_signal: *flag = 1 (device int32 that was 0), after all prior work
  *                   on `stream` (a 1-byte memset: no kernel).
  *   ss_flag_wait:   later work on `stream` starts only after *flag != 0
- *                   (acquire, GPU scope), observed by a one-thread kernel;
- *                   gives up after the same timeout. */
+ *                   (acquire, GPU scope), observed by a one-thread kernel.
+ *                   If the flag reads SS_H2D_DONE_ABORTED, or nothing is
+ *                   signalled within timeout_us (<= 0: 3 s), it sets
+ *                   counts_or_null[3] = SS_ERR_CUDA (when given) so the job's
+ *                   downstream calls become no-ops and the failure is
+ *                   reported, never silent. */
 ss_status ss_flag_signal(int32_t* flag, void* stream);
+ss_status ss_flag_wait(const int32_t* flag, int32_t* counts_or_null, int64_t timeout_us, void* stream);
 
 /* Load every kernel of the library now (CUDA lazy module loading would load
  * each one at its first launch; a first launch that has to wait behind a
  * spinning flash_h2d_serve can stall it).  flash_h2d_serve calls it itself on
  * its first call outside stream capture.  Idempotent; SS_ERR_CUDA on failure. */
 ss_status ss_preload_kernels(void);
-ss_status ss_flag_wait(const int32_t* flag, void* stream);
 
 /* S5  sparse_decode_attn -- PAPER.md:71-72 §2.1 (S = QK^T/sqrt(d), P =
  * softmax(S), O = PV) restricted to the selected blocks.
@@ -416,6 +434,24 @@ size_t ss_workspace_size(int32_t which, ss_dims dims, int32_t max_blk, int32_t k
 
 /* Device address of pinned host memory (cudaHostGetDevicePointer). */
 ss_status ss_host_device_pointer(void* host, void** dev);
+
+/* Host KV pool memory (§3.1: DRAM holds every KV block;
+ * PAPER.md:143-149 §3.2.1: FlashH2D reads it zero-copy over UVA; SURVEY.md
+ * §8(e): each rank's partition on its GPU's NUMA node).
+ *   ss_device_numa_node: NUMA node of CUDA device `device`'s PCIe root from
+ *     sysfs, or -1 when unknown (single-node or virtualised hosts).
+ *   ss_host_alloc: `bytes` of page-locked, device-mapped host memory; when
+ *     numa_node >= 0 its pages are bound to that node before first touch
+ *     (mbind), *bound_out (may be NULL) = 1 if that binding took effect.
+ *     *host_out = host address (caller owns it: free with ss_host_free with
+ *     the same bytes), *dev_out = its device address (for flash_h2d_*).
+ *     SS_ERR_CAPACITY if the mapping fails, SS_ERR_CUDA if registration does
+ *     (nothing is left allocated on error).  Contents are zero.
+ *   ss_host_free: unregisters and unmaps; NULL is a no-op. */
+int32_t ss_device_numa_node(int32_t device);
+ss_status ss_host_alloc(size_t bytes, int32_t numa_node, void** host_out, void** dev_out,
+                        int32_t* bound_out);
+ss_status ss_host_free(void* host, size_t bytes);
 
 const char* ss_status_string(ss_status s);
 const char* ss_version(void);

@@ -10,10 +10,15 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libsparseserve.so")
+# SS_LIB_VARIANT=debug loads libsparseserve_debug.so (built with -DSS_DEBUG_KNOBS:
+# the development A/B environment knobs; tools/ and a few subprocess tests only)
+LIB_PATH = os.path.join(PKG, "libsparseserve_debug.so" if os.environ.get("SS_LIB_VARIANT") == "debug"
+                        else "libsparseserve.so")
 
 SS_OK, SS_ERR_INVALID_ARG, SS_ERR_UNSUPPORTED, SS_ERR_CAPACITY, SS_ERR_CUDA = range(5)
 SS_BF16, SS_F32 = 0, 1
+SS_H2D_STATS = 8
+SS_H2D_DONE_SERVED, SS_H2D_DONE_ABORTED = 1, 2
 SS_WS_SELECT, SS_WS_CACHE, SS_WS_ATTN, SS_WS_SEAL, SS_WS_PREFILL = 0, 1, 2, 3, 4
 
 EXPORTS = ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert", "flash_h2d_gather",
@@ -22,7 +27,8 @@ EXPORTS = ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert", "fl
            "ss_d2h_create", "ss_d2h_destroy", "flash_d2h_save", "ws_track", "ss_admit", "prefill_layer_save",
            "block_meta_update_mean", "ss_block_select_mean", "flash_h2d_serve", "ss_flag_signal",
            "ss_flag_wait", "ss_preload_kernels",
-           "sparse_decode_attn_part", "sparse_attn_merge")
+           "sparse_decode_attn_part", "sparse_attn_merge", "ss_device_numa_node", "ss_host_alloc",
+           "ss_host_free")
 
 
 class SSDims(ctypes.Structure):
@@ -68,9 +74,9 @@ def load() -> ctypes.CDLL:
     L.kv_cache_lookup_insert.argtypes = [SSCachePool, P, P, I32, I32, I32, I32, SSDims, I64, P, P,
                                          P, P, P, P, SZ, P]
     L.flash_h2d_gather.argtypes = [P, I64, P, P, P, I32, P, I64, P]
-    L.flash_h2d_serve.argtypes = [P, I64, P, I32, I64, P, P]
+    L.flash_h2d_serve.argtypes = [P, I64, P, I32, I64, P, I64, P, P]
     L.ss_flag_signal.argtypes = [P, P]
-    L.ss_flag_wait.argtypes = [P, P]
+    L.ss_flag_wait.argtypes = [P, P, I64, P]
     L.ss_preload_kernels.argtypes = []
     L.sparse_decode_attn_part.argtypes = [P, P, P, P, I32, I32, P, P, SSDims, I32, F, P, P, P, P, SZ, P]
     L.sparse_attn_merge.argtypes = [P, P, P, P, I64, P, P, P]
@@ -78,6 +84,13 @@ def load() -> ctypes.CDLL:
     L.ss_workspace_size.argtypes = [I32, SSDims, I32, I32, I32]
     L.ss_workspace_size.restype = SZ
     L.ss_host_device_pointer.argtypes = [P, ctypes.POINTER(ctypes.c_void_p)]
+    L.ss_device_numa_node.argtypes = [I32]
+    L.ss_device_numa_node.restype = I32
+    L.ss_host_alloc.argtypes = [SZ, I32, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
+                                ctypes.POINTER(I32)]
+    L.ss_host_alloc.restype = I32
+    L.ss_host_free.argtypes = [P, SZ]
+    L.ss_host_free.restype = I32
     L.ss_status_string.argtypes = [I32]
     L.ss_status_string.restype = ctypes.c_char_p
     L.ss_version.restype = ctypes.c_char_p

@@ -23,8 +23,9 @@ ss_status launch_flash_h2d(const void* host_kv, int64_t host_blocks, const int64
                            const int32_t* miss_slots, const int32_t* counts, int max_misses,
                            void* pool_kv, int64_t block_bytes, cudaStream_t stream);
 ss_status launch_flash_h2d_serve(const void* host_kv, int64_t host_blocks, const ss_h2d_job* jobs,
-                                 int njobs, int64_t block_bytes, int32_t* flags, cudaStream_t stream);
-ss_status launch_flag_wait(const int32_t* flag, cudaStream_t stream);
+                                 int njobs, int64_t block_bytes, int32_t* flags, int64_t timeout_us,
+                                 unsigned long long* stats, cudaStream_t stream);
+ss_status launch_flag_wait(const int32_t* flag, int32_t* counts, int64_t timeout_us, cudaStream_t stream);
 ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* slot, int k,
                              const void* tail_kv, const int32_t* tail_len, const ss_dims& d,
                              ss_dtype dt, float scale, const int32_t* counts, float* out, void* ws,
@@ -161,7 +162,8 @@ ss_status ss_preload_kernels(void) {
 }
 
 ss_status flash_h2d_serve(const void* host_kv, int64_t host_blocks, const ss_h2d_job* jobs,
-                          int32_t njobs, int64_t block_bytes, int32_t* flags, void* stream) {
+                          int32_t njobs, int64_t block_bytes, int32_t* flags, int64_t timeout_us,
+                          uint64_t* stats_or_null, void* stream) {
     if (njobs < 0) return SS_ERR_INVALID_ARG;
     if (njobs == 0) return SS_OK;
     if (!host_kv || !jobs || !flags || host_blocks < 1) return SS_ERR_INVALID_ARG;
@@ -173,7 +175,9 @@ ss_status flash_h2d_serve(const void* host_kv, int64_t host_blocks, const ss_h2d
     if (cudaStreamIsCapturing((cudaStream_t)stream, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {
         if (ss_preload_kernels() != SS_OK) return SS_ERR_CUDA;
     }
-    return ss::launch_flash_h2d_serve(host_kv, host_blocks, jobs, njobs, block_bytes, flags,
+    if (stats_or_null && (reinterpret_cast<uintptr_t>(stats_or_null) & 7)) return SS_ERR_INVALID_ARG;
+    return ss::launch_flash_h2d_serve(host_kv, host_blocks, jobs, njobs, block_bytes, flags, timeout_us,
+                                      reinterpret_cast<unsigned long long*>(stats_or_null),
                                       (cudaStream_t)stream);
 }
 
@@ -184,9 +188,9 @@ ss_status ss_flag_signal(int32_t* flag, void* stream) {
     return SS_OK;
 }
 
-ss_status ss_flag_wait(const int32_t* flag, void* stream) {
+ss_status ss_flag_wait(const int32_t* flag, int32_t* counts_or_null, int64_t timeout_us, void* stream) {
     if (!flag) return SS_ERR_INVALID_ARG;
-    return ss::launch_flag_wait(flag, (cudaStream_t)stream);
+    return ss::launch_flag_wait(flag, counts_or_null, timeout_us, (cudaStream_t)stream);
 }
 
 ss_status sparse_decode_attn(const void* q, const void* pool_kv, const int32_t* slot, int32_t k,

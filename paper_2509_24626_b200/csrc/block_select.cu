@@ -551,13 +551,9 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
 // to these fixed sizes everywhere (smaller chunks pay more top-k and merge work
 // than the wave tail costs).  SS_SEL_CHUNK (multiple of 32, <= 4096) overrides.
 static int sel_chunk_env() {
-    static const int env = [] {
-        const char* e = getenv("SS_SEL_CHUNK");
-        int v = e ? atoi(e) : 0;
-        if (e && (v < 32 || v > kSelChunkMax || (v % 32))) v = kSelChunkMax;
-        return v;
-    }();
-    return env;
+    int v = knob("SS_SEL_CHUNK", 0);  // debug build only
+    if (v != 0 && (v < 32 || v > kSelChunkMax || (v % 32))) v = kSelChunkMax;
+    return v;
 }
 constexpr int kSelChunkMin = 512;  // workspace sizing bound (SS_SEL_CHUNK may go lower)
 
@@ -603,9 +599,9 @@ static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_
     const int items = nchunks * (int)pairs;
     // (measured: both the persistent grid and the L2 tile prefetch were slower
     // than a plain one-CTA-per-item grid; kept switchable for experiments)
-    static const int persist = getenv("SS_SEL_PERSIST") ? atoi(getenv("SS_SEL_PERSIST")) : 0;
-    static const int l2pf = getenv("SS_SEL_L2PF") ? atoi(getenv("SS_SEL_L2PF")) : 0;
-    const int grid = (persist && items > 2 * kNumSMs) ? 2 * kNumSMs : items;
+    const int persist = knob("SS_SEL_PERSIST", 0);
+    const int l2pf = knob("SS_SEL_L2PF", 0);
+    const int grid = (persist && items > 2 * num_sms()) ? 2 * num_sms() : items;
     kern<<<grid, kSelThreads, smem, stream>>>(q, meta, n_blk, max_blk, k, d.num_q_heads,
                                               d.num_kv_heads, nchunks, CH, (int)pairs, l2pf, sel, scores, cand_key,
                                               cand_j, tickets);
@@ -623,9 +619,9 @@ ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_
         if ((size_t)nchunks * k > kSelMaxMerge && nchunks > 1) return SS_ERR_UNSUPPORTED;
     }
     // integer-built float64 operands (default) or F2F conversions (SS_SEL_ICV=0, A/B only)
-    static const bool icv = getenv("SS_SEL_ICV") ? atoi(getenv("SS_SEL_ICV")) != 0 : true;
+    const bool icv = knob("SS_SEL_ICV", 1) != 0;
     // GQA: one tile per warp pass at 3 CTAs / SM (SS_SEL_TT=1) vs two (default)
-    static const bool tt1 = getenv("SS_SEL_TT") && atoi(getenv("SS_SEL_TT")) == 1;
+    const bool tt1 = knob("SS_SEL_TT", 2) == 1;
 #define SS_SEL_ARGS q, meta, n_blk, max_blk, k, d, sel, scores, ws, stream
 #define SS_SEL_CASE(GG)                                                                       \
     case GG:                                                                                  \

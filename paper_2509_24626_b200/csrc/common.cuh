@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "sparseserve.h"
 
@@ -10,7 +11,35 @@ namespace ss {
 
 constexpr int kBlockTokens = 32;
 constexpr int kHeadDim = 128;
-constexpr int kNumSMs = 148;  // B200
+
+// Multiprocessor count of the current device (148 on B200), queried once per
+// device: grids of the persistent kernels are sized to it.
+inline int num_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+    if (cache[dev] == 0) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+        cache[dev] = n;
+    }
+    return cache[dev];
+}
+
+// Development A/B knobs (environment variables such as SS_SEL_CHUNK) exist only
+// in the debug build (-DSS_DEBUG_KNOBS, libsparseserve_debug.so, used by
+// tools/ and a few subprocess tests).  The shipped library ignores the
+// environment: every call does exactly what include/sparseserve.h states.
+inline int knob(const char* name, int dflt) {
+#ifdef SS_DEBUG_KNOBS
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+#else
+    (void)name;
+    return dflt;
+#endif
+}
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }

@@ -78,22 +78,18 @@ ss_status launch_flash_h2d(const void* host_kv, int64_t host_blocks, const int64
                            const int32_t* miss_slots, const int32_t* counts, int max_misses,
                            void* pool_kv, int64_t block_bytes, cudaStream_t stream) {
     if (max_misses <= 0) return SS_OK;
-    // experiment knob: SS_H2D_SKIP=1 launches nothing (the step without PCIe time)
-    static const bool skip = getenv("SS_H2D_SKIP") && atoi(getenv("SS_H2D_SKIP")) != 0;
-    if (skip) return SS_OK;
     int64_t warps_needed = (int64_t)max_misses * 2;  // ~2 units per block (bf16)
-    static const int threads = getenv("SS_H2D_THREADS") ? atoi(getenv("SS_H2D_THREADS")) : 128;
+    const int threads = knob("SS_H2D_THREADS", 128);
     int64_t grid = (warps_needed * 32 + threads - 1) / threads;
     // Few CTAs on purpose: zero-copy PCIe loads in flight on an SM slow down
     // the HBM-bound kernels co-running on that SM (measured: a select kernel
     // sharing the GPU with a 148-CTA gather ran 3.7x slower, with a 16-CTA one
     // 1.2x slower), while 16 CTAs x 4 warps x 32 lanes x 16 x 16 B = 512 KB in
     // flight cover the link's bandwidth-delay product.
-    static const int max_ctas = getenv("SS_H2D_CTAS") ? atoi(getenv("SS_H2D_CTAS")) : kH2DCtas;
+    const int max_ctas = knob("SS_H2D_CTAS", kH2DCtas);
     if (grid > max_ctas) grid = max_ctas;
     // loads in flight per lane: 16 (default) keeps 512 KB in flight on 16 SMs
-    static const int unroll = getenv("SS_H2D_UNROLL") ? atoi(getenv("SS_H2D_UNROLL")) : 16;
-    auto kern = unroll >= 16 ? flash_h2d_kernel<16> : flash_h2d_kernel<8>;
+    auto kern = knob("SS_H2D_UNROLL", 16) >= 16 ? flash_h2d_kernel<16> : flash_h2d_kernel<8>;
     kern<<<(int)grid, threads, 0, stream>>>(
         (const uint4*)host_kv, host_blocks, miss_keys, miss_slots, counts, max_misses,
         (uint4*)pool_kv, block_bytes / 16, 0u);
@@ -110,16 +106,27 @@ ss_status launch_flash_h2d(const void* host_kv, int64_t host_blocks, const int64
 // after its kv_cache_lookup_insert); its work units are handed out by an
 // atomic cursor, and a warp always takes a unit of the lowest-numbered ready
 // job with units left, so warps done with job j start the next job's loads
-// while others still finish job j, and a late job never blocks ready ones.  The warp that completes
-// job j's last unit publishes done[j] = 1 (release), which ss_flag_wait turns
-// into a stream dependency for that job's attention.
+// while others still finish job j, and a late job never blocks ready ones.  The
+// warp that completes job j's last unit publishes done[j] = 1 (release), which
+// ss_flag_wait turns into a stream dependency for that job's attention.
 //
 // flags (device int32, zeroed by the caller before each launch):
 //   [0, nj) ready   [nj, 2nj) done   [2nj, 3nj) unit cursor
 //   [3nj, 4nj) finished units        [4nj] abort
-// A job that is not ready within the timeout aborts the server: every job not
-// yet done gets counts[3] = SS_ERR_CUDA (downstream attention becomes a no-op,
-// the error is visible in the counts) and done = 1, so nothing waits forever.
+// A server that sees no ready job for `timeout` aborts: every job not yet done
+// gets done = 2 (SS_H2D_DONE_ABORTED).  The abort is sticky where it matters:
+// the job's ss_flag_wait (stream-ordered after the job's producer, so after
+// any counts[3] = 0 that producer writes) sees done == 2 and sets counts[3] =
+// SS_ERR_CUDA, which turns the attention that follows into a no-op and makes
+// the error visible in the step's counts.  A flag_wait that itself times out
+// does the same.
+//
+// stats (optional, device uint64 [8], zeroed by the caller): [0] sum over the
+// server's warps of the ns spent with no unit to serve (polling), [1] warps,
+// [2] first unit start (globaltimer ns), [3] last unit end, [4] ns from the
+// first unit start to the last unit end during which NO warp was copying
+// (link idle, from a per-warp busy count), [5] 1 + the first job found not
+// ready at an abort (0: no abort).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t gtimer_ns() {
     uint64_t t;
@@ -135,16 +142,47 @@ __device__ __forceinline__ void st_release_gpu(int32_t* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+constexpr int kDoneServed = 1;
+constexpr int kDoneAborted = 2;
+
+// Link-idle accounting: `busy` counts the warps copying right now; the warp
+// that takes it 1 -> 0 stamps the idle start, the warp that takes it 0 -> 1
+// adds the elapsed idle time.  (Approximate at the ns level: the stamp and the
+// count are two words; good enough for an idle fraction.)
+struct ServeStats {
+    unsigned long long* s;
+    __device__ __forceinline__ void busy_begin(int32_t* busy, uint64_t* idle_t0) {
+        if (s == nullptr) return;
+        const uint64_t now = gtimer_ns();
+        if (atomicAdd(busy, 1) == 0) {
+            const uint64_t t0 = atomicExch((unsigned long long*)idle_t0, 0ull);
+            if (t0 != 0 && now > t0) atomicAdd(s + 4, now - t0);
+            atomicCAS(s + 2, 0ull, (unsigned long long)now);  // first unit start
+        }
+    }
+    __device__ __forceinline__ void busy_end(int32_t* busy, uint64_t* idle_t0) {
+        if (s == nullptr) return;
+        const uint64_t now = gtimer_ns();
+        atomicMax(s + 3, now);
+        if (atomicSub(busy, 1) == 1) atomicExch((unsigned long long*)idle_t0, now);
+    }
+};
+
 template <int kU>
 __global__ void __launch_bounds__(kH2DThreadsMax)
 flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
                         const ss_h2d_job* __restrict__ jobs, int njobs, int64_t vpb,
-                        int32_t* flags, uint32_t zero, uint64_t timeout_ns) {
+                        int32_t* flags, uint32_t zero, uint64_t timeout_ns,
+                        unsigned long long* stats) {
     int32_t* ready = flags;
     int32_t* done = flags + njobs;
     int32_t* cursor = flags + 2 * njobs;
     int32_t* fin = flags + 3 * njobs;
     int32_t* abort_flag = flags + 4 * njobs;
+    // link-idle bookkeeping lives in stats[6] (busy warps) and stats[7] (idle start)
+    int32_t* busy = stats ? (int32_t*)(stats + 6) : nullptr;
+    uint64_t* idle_t0 = stats ? (uint64_t*)(stats + 7) : nullptr;
+    ServeStats st{stats};
     const int lane = lane_id();
     constexpr int64_t kBatch = 32 * kU;
     const int upb = (int)((vpb + kBatch - 1) / kBatch);  // units per block
@@ -155,7 +193,9 @@ flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
     // waiting in.
     int lo = 0;
     bool aborted = false;
-    uint64_t t_idle = gtimer_ns();
+    uint64_t t_idle = gtimer_ns();   // start of the current no-work stretch
+    uint64_t idle_sum = 0;
+    bool polling = false;
     const uint4* hsrc = host;
     while (true) {
         int pj = -1, pu = 0, pnu = 0;
@@ -168,7 +208,7 @@ flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
                 const int nu = n * upb;
                 const int peek = *(volatile int32_t*)(cursor + jj);
                 if (nu == 0) {  // nothing to load: the first warp here publishes done
-                    if (peek == 0 && atomicAdd(cursor + jj, 1) == 0) st_release_gpu(done + jj, 1);
+                    if (peek == 0 && atomicAdd(cursor + jj, 1) == 0) st_release_gpu(done + jj, kDoneServed);
                     if (jj == lo) ++lo;
                     continue;
                 }
@@ -193,10 +233,18 @@ flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
             if (lo >= njobs) break;  // every job handed out
             int stop = 0;
             if (lane == 0) {
+                if (!polling) {
+                    polling = true;
+                    t_idle = gtimer_ns();
+                }
                 if (*(volatile int32_t*)abort_flag) {
                     stop = 1;
                 } else if (gtimer_ns() - t_idle > timeout_ns) {
-                    atomicExch(abort_flag, 1);
+                    if (atomicExch(abort_flag, 1) == 0 && stats) {
+                        int first = lo;
+                        while (first < njobs && ld_acquire_gpu(ready + first) != 0) ++first;
+                        stats[5] = (unsigned long long)(first + 1);
+                    }
                     stop = 1;
                 } else {
                     __nanosleep(64);
@@ -210,7 +258,8 @@ flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
         }
         pu = __shfl_sync(0xffffffffu, pu, 0);
         pnu = __shfl_sync(0xffffffffu, pnu, 0);
-        if (lane == 0) t_idle = gtimer_ns();
+        if (lane == 0 && polling) idle_sum += gtimer_ns() - t_idle;
+        polling = false;
         const ss_h2d_job jb = jobs[pj];
         uint4* pool = (uint4*)jb.pool_kv;
         {
@@ -223,6 +272,9 @@ flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
                 uint4 r[kU];
 #pragma unroll
                 for (int k = 0; k < kU; ++k) r[k] = ldg_stream(src + v0 + 32 * k);
+                // (statistics atomics after the loads are issued: their round
+                // trip overlaps the PCIe latency instead of delaying it)
+                if (lane == 0) st.busy_begin(busy, idle_t0);
                 uint32_t fold = 0;
 #pragma unroll
                 for (int k = 0; k < kU; ++k) fold ^= r[k].w;
@@ -234,6 +286,7 @@ flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
                     stg_v4(dst + v0 + 32 * k, x);
                 }
             } else {
+                if (lane == 0) st.busy_begin(busy, idle_t0);
                 for (int64_t v = v0; v < min(vpb, (int64_t)(part + 1) * kBatch); v += 32)
                     stg_v4(dst + v, ldg_stream(src + v));
             }
@@ -241,51 +294,66 @@ flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
         __threadfence();  // this lane's pool stores are visible GPU-wide ...
         __syncwarp();
         if (lane == 0) {  // ... before the unit is counted
+            st.busy_end(busy, idle_t0);
             const int f = atomicAdd(fin + pj, 1);
             if (f == pnu - 1) {
                 __threadfence();
-                st_release_gpu(done + pj, 1);
+                st_release_gpu(done + pj, kDoneServed);
             }
         }
+    }
+    if (lane == 0 && stats) {
+        if (polling) idle_sum += gtimer_ns() - t_idle;
+        atomicAdd(stats + 0, idle_sum);
+        atomicAdd(stats + 1, 1ull);
     }
     if (aborted && lane == 0) {
         for (int jj = 0; jj < njobs; ++jj) {
             if (ld_acquire_gpu(done + jj) == 0) {
                 atomicExch(jobs[jj].counts + 3, (int)SS_ERR_CUDA);
                 __threadfence();
-                st_release_gpu(done + jj, 1);
+                st_release_gpu(done + jj, kDoneAborted);
             }
         }
     }
 }
 
-__global__ void flag_wait_kernel(const int32_t* flag, uint64_t timeout_ns) {
+// Stream-ordered wait for a done flag.  flag == 2 (the server aborted this
+// job) or a wait that times out marks the job failed in its counts word (this
+// kernel runs after the job's producer, so the mark cannot be overwritten by
+// it): the attention that follows is a no-op and the step reports the error.
+__global__ void flag_wait_kernel(const int32_t* flag, int32_t* counts, uint64_t timeout_ns) {
     const uint64_t t0 = gtimer_ns();
-    while (ld_acquire_gpu(flag) == 0) {
+    int v;
+    while ((v = ld_acquire_gpu(flag)) == 0) {
         if (gtimer_ns() - t0 > timeout_ns) break;
         __nanosleep(128);
     }
+    if (v != kDoneServed && counts != nullptr) {
+        atomicExch(counts + 3, (int)SS_ERR_CUDA);
+        __threadfence();
+    }
 }
 
-static uint64_t serve_timeout_ns() {
-    static const uint64_t t = getenv("SS_SERVE_TIMEOUT_MS") ? (uint64_t)atoll(getenv("SS_SERVE_TIMEOUT_MS")) * 1000000ull
-                                                            : 3000000000ull;  // 3 s
-    return t;
+static uint64_t timeout_ns_of(int64_t timeout_us) {
+    return timeout_us > 0 ? (uint64_t)timeout_us * 1000ull : 3000000000ull;  // default 3 s
 }
 
 ss_status launch_flash_h2d_serve(const void* host_kv, int64_t host_blocks, const ss_h2d_job* jobs,
-                                 int njobs, int64_t block_bytes, int32_t* flags, cudaStream_t stream) {
+                                 int njobs, int64_t block_bytes, int32_t* flags, int64_t timeout_us,
+                                 unsigned long long* stats, cudaStream_t stream) {
     if (njobs <= 0) return SS_OK;
-    static const int threads = getenv("SS_H2D_THREADS") ? atoi(getenv("SS_H2D_THREADS")) : 128;
-    static const int ctas = getenv("SS_H2D_CTAS") ? atoi(getenv("SS_H2D_CTAS")) : kH2DCtas;
+    const int threads = knob("SS_H2D_THREADS", 128);
+    const int ctas = knob("SS_H2D_CTAS", kH2DCtas);
     flash_h2d_server_kernel<16><<<ctas, threads, 0, stream>>>(
-        (const uint4*)host_kv, host_blocks, jobs, njobs, block_bytes / 16, flags, 0u, serve_timeout_ns());
+        (const uint4*)host_kv, host_blocks, jobs, njobs, block_bytes / 16, flags, 0u,
+        timeout_ns_of(timeout_us), stats);
     SS_LAUNCH_CHECK();
     return SS_OK;
 }
 
-ss_status launch_flag_wait(const int32_t* flag, cudaStream_t stream) {
-    flag_wait_kernel<<<1, 32, 0, stream>>>(flag, serve_timeout_ns());
+ss_status launch_flag_wait(const int32_t* flag, int32_t* counts, int64_t timeout_us, cudaStream_t stream) {
+    flag_wait_kernel<<<1, 32, 0, stream>>>(flag, counts, timeout_ns_of(timeout_us));
     SS_LAUNCH_CHECK();
     return SS_OK;
 }

@@ -512,10 +512,10 @@ ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int3
     // Measured in the C2 step: fused 54.8 us alone / 76 us in-step vs 38.7 / 56.6
     // for three kernels -- the 128-CTA grid serialises items per CTA and its
     // barriers cost more than two kernel boundaries (profiles/r01s3_cache_fused_ab.txt)
-    static const int fused = getenv("SS_CACHE_FUSED") ? atoi(getenv("SS_CACHE_FUSED")) : 0;
-    static const int fused_ctas = getenv("SS_CACHE_CTAS") ? atoi(getenv("SS_CACHE_CTAS")) : 128;
+    const int fused = knob("SS_CACHE_FUSED", 0);
+    const int fused_ctas = knob("SS_CACHE_CTAS", 128);
     if (fused) {
-        const int grid = std::max(1, std::min(a.nA + a.nS, std::min(fused_ctas, kNumSMs)));
+        const int grid = std::max(1, std::min(a.nA + a.nS, std::min(fused_ctas, num_sms())));
         cache_fused_kernel<<<grid, kCacheThreads, 0, stream>>>(a);
     } else {
         cache_lookup_count_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
@@ -524,7 +524,7 @@ ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int3
         // the C2 step: PDL makes the call faster (34 vs 39 us alone, 52 vs 57 in
         // the step) but the step slower (11.85 vs 11.0 ms median): the early-
         // resident K2/K3 CTAs take SM slots from the other groups' select.
-        static const int pdl = getenv("SS_CACHE_PDL") ? atoi(getenv("SS_CACHE_PDL")) : 0;
+        const int pdl = knob("SS_CACHE_PDL", 0);
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;

@@ -910,12 +910,11 @@ static size_t attn_smem_bytes() {
 }
 
 static int attn_total_warps(ss_dtype dt) {
-    return kNumSMs * (dt == SS_BF16 ? AttnTraits<true>::NW : AttnTraits<false>::NW);
+    return num_sms() * (dt == SS_BF16 ? AttnTraits<true>::NW : AttnTraits<false>::NW);
 }
 
 static bool attn_trace_on() {
-    static const bool on = getenv("SS_ATTN_TRACE") && atoi(getenv("SS_ATTN_TRACE")) != 0;
-    return on;
+    return knob("SS_ATTN_TRACE", 0) != 0;
 }
 
 static size_t attn_ws_bytes_core(const ss_dims& d, ss_dtype dt) {
@@ -980,9 +979,9 @@ static ss_status launch_attn_mma_t(const AttnArgs& a, const void* pool, const vo
     // dispatched into whatever SM space co-running kernels leave); warps never
     // synchronise, so the kernel is the same (warp w = warp_id * gridDim + CTA).
     // Measured: 0.89 vs 0.85 of HBM peak alone at C2, no in-step difference.
-    static const int cta_warps = getenv("SS_ATTN_CTA_WARPS") ? atoi(getenv("SS_ATTN_CTA_WARPS")) : kMmaNW;
+    const int cta_warps = knob("SS_ATTN_CTA_WARPS", kMmaNW);
     if (cta_warps == kMmaNW)
-        kern<<<kNumSMs, kMmaNW * 32, kMmaSmem, stream>>>(a, tm_pool, tm_tail);
+        kern<<<num_sms(), kMmaNW * 32, kMmaSmem, stream>>>(a, tm_pool, tm_tail);
     else
         kern<<<a.W, 32, sizeof(MmaWarpSmem) + 1024, stream>>>(a, tm_pool, tm_tail);
     SS_LAUNCH_CHECK();
@@ -996,7 +995,7 @@ static ss_status launch_attn_t(AttnArgs a, cudaStream_t stream) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return SS_ERR_CUDA;
-    kern<<<kNumSMs, AttnTraits<BF16>::NW * 32, smem, stream>>>(a);
+    kern<<<num_sms(), AttnTraits<BF16>::NW * 32, smem, stream>>>(a);
     SS_LAUNCH_CHECK();
     return SS_OK;
 }
@@ -1065,15 +1064,14 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
     // at least kMinUnitsPerWarp units (128 KiB in bf16) per warp: fewer, longer
     // ranges when the problem is small (C3: ~16 partials per pair to merge instead
     // of ~28); W <= U keeps every range non-empty
-    static const int min_units = getenv("SS_ATTN_MIN_UNITS") ? atoi(getenv("SS_ATTN_MIN_UNITS"))
-                                                              : kMinUnitsPerWarp;
+    const int min_units = knob("SS_ATTN_MIN_UNITS", kMinUnitsPerWarp);
     a.W = (int)std::max<int64_t>(1, std::min<int64_t>(attn_total_warps(dt), a.U / std::max(1, min_units)));
     size_t part = (size_t)a.W * 2 * G * kAttnPartStride * 4;
     a.part = (float*)ws;
     a.tickets = (int32_t*)((char*)ws + part);
     a.trace = attn_trace_on() ? (unsigned long long*)((char*)ws + attn_ws_bytes_core(d, dt)) : nullptr;
     // bf16: tensor-core path (SS_ATTN_MMA=0 selects the CUDA-core FMA path)
-    static const int use_mma = getenv("SS_ATTN_MMA") ? atoi(getenv("SS_ATTN_MMA")) : 1;
+    const int use_mma = knob("SS_ATTN_MMA", 1);
 #define SS_ATTN_CASE(GG)                                                                    \
     case GG:                                                                                \
         if (dt == SS_BF16 && use_mma) return launch_attn_mma_t<GG>(a, pool_kv, tail_kv, stream); \

@@ -212,6 +212,11 @@ class DecodeEngine:
                                           for l in range(c.layers) for gi, g in enumerate(self.groups)],
                                          device=dev)
             self.h2d_flags = ops.h2d_flags(self.njobs, device=dev)
+            # server statistics (link idle time; include/sparseserve.h), zeroed per
+            # step; passed to the server only when collect_h2d_stats is set (a few
+            # atomics per 8 KiB unit)
+            self.h2d_stats = ops.h2d_stats(device=dev)
+        self.collect_h2d_stats = False
             ops.preload_kernels()      # no lazy kernel load while the server spins
         self._capturing = False
         g0 = self.groups[0]
@@ -229,13 +234,13 @@ class DecodeEngine:
         return self.gpool_kv[l][gi] if self.per_group_pools else self.pool_kv[l]
 
     # ------------------------------------------------------------------ setup
-    def set_host_kv(self, host_kv: torch.Tensor, host_blocks: int) -> None:
-        """host_kv: pinned CPU tensor holding host_blocks blocks [2][32][d] (dtype)."""
-        assert host_kv.is_pinned()
+    def set_host_kv(self, host_kv: torch.Tensor, host_blocks: int, dev_ptr: Optional[int] = None) -> None:
+        """host_kv: pinned CPU tensor holding host_blocks blocks [2][32][d] (dtype);
+        dev_ptr: its device address if already known (ops.HostPool)."""
         assert host_kv.numel() * host_kv.element_size() >= host_blocks * self.cfg.block_bytes
         self.host_kv = host_kv
         self.host_blocks = host_blocks
-        self.host_ptr = ops.host_device_pointer(host_kv)
+        self.host_ptr = dev_ptr if dev_ptr is not None else ops.host_device_pointer(host_kv)
 
     def key0(self, req: int, layer: int, h: int) -> int:
         c = self.cfg
@@ -334,7 +339,8 @@ class DecodeEngine:
                 timed("attn", lambda: ops.sparse_decode_attn_part(
                     q, self.pool_kv_of(l, gi), g.slot[l], g.hit[l], 1, c.topk, g.tail_kv[l], g.tail_len, g.dims,
                     self.scale, g.out_h, g.lse_h, g.ws_attn, counts=g.counts[l]))
-                ops.flag_wait(self.h2d_flags[self.njobs + j:self.njobs + j + 1], stream=g.stream)
+                ops.flag_wait(self.h2d_flags[self.njobs + j:self.njobs + j + 1], counts=g.counts[l],
+                              stream=g.stream)
                 timed("attn_miss", lambda: (
                     ops.sparse_decode_attn_part(q, self.pool_kv_of(l, gi), g.slot[l], g.hit[l], 2, c.topk,
                                                 g.tail_kv[l], g.tail_len, g.dims, self.scale, g.out_m,
@@ -344,7 +350,8 @@ class DecodeEngine:
                 return
             if gather and self.server:
                 g.stream.wait_event(g.ev_cache[l])
-                ops.flag_wait(self.h2d_flags[self.njobs + j:self.njobs + j + 1], stream=g.stream)
+                ops.flag_wait(self.h2d_flags[self.njobs + j:self.njobs + j + 1], counts=g.counts[l],
+                              stream=g.stream)
             elif gather:
                 g.h2d_stream.wait_event(g.ev_cache[l])
                 with torch.cuda.stream(g.h2d_stream):
@@ -380,6 +387,7 @@ class DecodeEngine:
         cur = torch.cuda.current_stream(self.device)
         if self.server:
             self.h2d_flags.zero_()     # before every stream below forks off `cur`
+            self.h2d_stats.zero_()
         for g in self.groups:
             g.stream.wait_stream(cur)
         self.cache_stream.wait_stream(cur)
@@ -397,7 +405,8 @@ class DecodeEngine:
                     ts, te = timers.mark("gather", 0, 0)
                     ts.record()
                 ops.flash_h2d_serve(self.host_ptr, self.host_blocks, self.h2d_jobs, self.njobs,
-                                    c.block_bytes, self.h2d_flags)
+                                    c.block_bytes, self.h2d_flags,
+                                    stats=self.h2d_stats if self.collect_h2d_stats else None)
                 if tm:
                     te.record()
         # issue layer by layer, group by group: group A's FlashH2D (PCIe) overlaps

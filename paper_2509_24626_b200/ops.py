@@ -158,6 +158,36 @@ def host_device_pointer(host: torch.Tensor) -> int:
     return int(out.value)
 
 
+class HostPool:
+    """Page-locked, device-mapped host memory for the host KV pool, on the NUMA
+    node of `device` (ss_host_alloc; freed on close / garbage collection).
+    `tensor` is a CPU uint8 view of it, `dev_ptr` its device address."""
+
+    def __init__(self, nbytes: int, device: int = 0, numa_node: Optional[int] = None):
+        import ctypes
+        lib = _lib.load()
+        self.numa_node = int(lib.ss_device_numa_node(device)) if numa_node is None else int(numa_node)
+        h, d, bound = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int32(0)
+        check(lib.ss_host_alloc(nbytes, self.numa_node, ctypes.byref(h), ctypes.byref(d), ctypes.byref(bound)),
+              "ss_host_alloc")
+        self.host_ptr, self.dev_ptr, self.nbytes = int(h.value), int(d.value), int(nbytes)
+        self.numa_bound = bool(bound.value)
+        buf = (ctypes.c_uint8 * nbytes).from_address(self.host_ptr)
+        self.tensor = torch.frombuffer(buf, dtype=torch.uint8)
+
+    def close(self) -> None:
+        if self.host_ptr:
+            self.tensor = None
+            _lib.load().ss_host_free(self.host_ptr, self.nbytes)
+            self.host_ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def flash_h2d_gather(host_kv_dev_ptr: int, host_blocks: int, miss_keys: torch.Tensor,
                      miss_slots: torch.Tensor, counts: torch.Tensor, max_misses: int,
                      pool_kv: torch.Tensor, block_bytes: int, stream=None) -> None:
@@ -180,17 +210,27 @@ def h2d_jobs(jobs, device=None) -> torch.Tensor:
 
 
 def h2d_flags(njobs: int, device=None) -> torch.Tensor:
-    """Zeroed flag words for flash_h2d_serve ([4*njobs + 1] int32)."""
+    """Zeroed flag words for flash_h2d_serve (SS_H2D_FLAGS(njobs) = 4*njobs + 1 int32)."""
     return torch.zeros(4 * njobs + 1, dtype=torch.int32, device=device or "cuda")
 
 
+def h2d_stats(device=None) -> torch.Tensor:
+    """Zeroed server statistics words (SS_H2D_STATS uint64, held as int64)."""
+    return torch.zeros(_lib.SS_H2D_STATS, dtype=torch.int64, device=device or "cuda")
+
+
 def flash_h2d_serve(host_kv_dev_ptr: int, host_blocks: int, jobs: torch.Tensor, njobs: int,
-                    block_bytes: int, flags: torch.Tensor, stream=None) -> None:
-    """S4, pipelined: one persistent launch serves njobs gathers in order (job j
-    once flags[j] != 0; sets flags[njobs + j] = 1 when its blocks are in HBM)."""
+                    block_bytes: int, flags: torch.Tensor, timeout_us: int = 0,
+                    stats: Optional[torch.Tensor] = None, stream=None) -> None:
+    """S4, pipelined: one persistent launch serves njobs gathers (job j once
+    flags[j] != 0; sets flags[njobs + j] = 1 when its blocks are in HBM, 2 if
+    the server aborted).  timeout_us <= 0: 3 s."""
     assert flags.dtype == torch.int32 and flags.numel() >= 4 * njobs + 1
+    if stats is not None:
+        assert stats.dtype == torch.int64 and stats.numel() >= _lib.SS_H2D_STATS
     check(_lib.load().flash_h2d_serve(host_kv_dev_ptr, host_blocks, _ptr(jobs), njobs, block_bytes,
-                                      _ptr(flags), _stream(stream)), "flash_h2d_serve")
+                                      _ptr(flags), int(timeout_us), _ptr(stats), _stream(stream)),
+          "flash_h2d_serve")
 
 
 def preload_kernels() -> None:
@@ -203,9 +243,14 @@ def flag_signal(flag: torch.Tensor, stream=None) -> None:
     check(_lib.load().ss_flag_signal(flag.data_ptr(), _stream(stream)), "ss_flag_signal")
 
 
-def flag_wait(flag: torch.Tensor, stream=None) -> None:
-    """Later work on the stream waits until *flag != 0."""
-    check(_lib.load().ss_flag_wait(flag.data_ptr(), _stream(stream)), "ss_flag_wait")
+def flag_wait(flag: torch.Tensor, counts: Optional[torch.Tensor] = None, timeout_us: int = 0,
+              stream=None) -> None:
+    """Later work on the stream waits until *flag != 0; an aborted job (flag 2)
+    or a timed-out wait sets counts[3] = SS_ERR_CUDA (when counts is given)."""
+    if counts is not None:
+        assert counts.dtype == torch.int32
+    check(_lib.load().ss_flag_wait(flag.data_ptr(), _ptr(counts), int(timeout_us), _stream(stream)),
+          "ss_flag_wait")
 
 
 def sparse_decode_attn(q: torch.Tensor, pool_kv: torch.Tensor, slot: torch.Tensor, k: int,

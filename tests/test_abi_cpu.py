@@ -70,12 +70,18 @@ def test_host_validation_without_gpu(lib):
     assert lib.block_meta_update(None, 8192, None, 0, None, 0, 128, None) == SS_OK     # n == 0 no-op
     assert lib.flash_h2d_gather(16, 0, 16, 16, 16, 1, 16, 16384, None) == SS_ERR_INVALID_ARG
     assert lib.flash_h2d_gather(16, 4, 16, 16, 16, 1, 16, 100, None) == SS_ERR_INVALID_ARG
-    assert lib.flash_h2d_serve(16, 4, 16, 0, 16384, 16, None) == SS_OK               # no jobs: no-op
-    assert lib.flash_h2d_serve(16, 4, 16, -1, 16384, 16, None) == SS_ERR_INVALID_ARG
-    assert lib.flash_h2d_serve(16, 4, None, 2, 16384, 16, None) == SS_ERR_INVALID_ARG
-    assert lib.flash_h2d_serve(16, 4, 16, 2, 100, 16, None) == SS_ERR_INVALID_ARG
+    assert lib.flash_h2d_serve(16, 4, 16, 0, 16384, 16, 0, None, None) == SS_OK       # no jobs: no-op
+    assert lib.flash_h2d_serve(16, 4, 16, -1, 16384, 16, 0, None, None) == SS_ERR_INVALID_ARG
+    assert lib.flash_h2d_serve(16, 4, None, 2, 16384, 16, 0, None, None) == SS_ERR_INVALID_ARG
+    assert lib.flash_h2d_serve(16, 4, 16, 2, 100, 16, 0, None, None) == SS_ERR_INVALID_ARG
+    assert lib.flash_h2d_serve(16, 4, 16, 2, 16384, 16, 0, 12, None) == SS_ERR_INVALID_ARG  # stats misaligned
     assert lib.ss_flag_signal(None, None) == SS_ERR_INVALID_ARG
-    assert lib.ss_flag_wait(None, None) == SS_ERR_INVALID_ARG
+    assert lib.ss_flag_wait(None, None, 0, None) == SS_ERR_INVALID_ARG
+    import ctypes as _ct
+    h, dv = _ct.c_void_p(), _ct.c_void_p()
+    assert lib.ss_host_alloc(0, -1, _ct.byref(h), _ct.byref(dv), None) == SS_ERR_INVALID_ARG
+    assert lib.ss_host_alloc(4096, -1, None, None, None) == SS_ERR_INVALID_ARG
+    assert lib.ss_host_free(None, 0) == SS_OK
     assert lib.sparse_decode_attn(16, 16, 16, 64, 16, 16, d, 0, 0.1, None, 16, 16, 1, None) == SS_ERR_INVALID_ARG
     assert lib.ss_status_string(3) == b"SS_ERR_CAPACITY"
     assert lib.ss_workspace_size(0, d, 4096, 64, 0) > 0

@@ -415,14 +415,17 @@ def test_cache_device_clock_mode(ops):
 
 
 def test_cache_fused_form_bit_exact(ops):
-    """The fused one-launch form of kv_cache_lookup_insert (SS_CACHE_FUSED=1,
-    read once per process) against the oracle: the cache parity tests and the
-    request-group pipelines re-run in a subprocess."""
+    """The fused one-launch form of kv_cache_lookup_insert (SS_CACHE_FUSED=1 in
+    the debug build, libsparseserve_debug.so) against the oracle: the cache
+    parity tests and the request-group pipelines re-run in a subprocess."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SS_CACHE_FUSED="1")
+    from paper_2509_24626_b200 import build as _build
+    if not os.path.exists(_build.LIB_DEBUG):
+        pytest.skip("debug library not built (python -m paper_2509_24626_b200.build --debug)")
+    env = dict(os.environ, SS_CACHE_FUSED="1", SS_LIB_VARIANT="debug")
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(root, "tests", "test_gpu_parity.py"),
                         os.path.join(root, "tests", "test_gpu_pipeline.py"),
