@@ -216,8 +216,8 @@ class DecodeEngine:
             # step; passed to the server only when collect_h2d_stats is set (a few
             # atomics per 8 KiB unit)
             self.h2d_stats = ops.h2d_stats(device=dev)
-        self.collect_h2d_stats = False
             ops.preload_kernels()      # no lazy kernel load while the server spins
+        self.collect_h2d_stats = False
         self._capturing = False
         g0 = self.groups[0]
         # single-group aliases (tests, smoke)

@@ -115,3 +115,13 @@ def test_ss_admit_matches_algorithm1(lib):
             else:
                 exp.append(False)
         assert ops.ss_admit(ws, m_avl) == exp == oracle.admit(ws, m_avl)
+
+
+def test_python_modules_import_on_cpu():
+    """The binding, engine and multi-GPU host logic import without a GPU (syntax
+    and import-time errors surface in the CPU suite)."""
+    import importlib
+    for m in ("paper_2509_24626_b200.ops", "paper_2509_24626_b200.engine", "paper_2509_24626_b200.shard"):
+        importlib.import_module(m)
+    import ast
+    ast.parse(open(os.path.join(ROOT, "bench.py")).read())

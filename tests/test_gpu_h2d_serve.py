@@ -190,6 +190,11 @@ def test_flash_h2d_serve_stats(ops):
     jt = ops.h2d_jobs(jobs)
     flags = ops.h2d_flags(2)
     stats = ops.h2d_stats()
+    # load torch's sleep kernel now: a first launch under CUDA lazy module
+    # loading would wait for the spinning server (ss_preload_kernels covers
+    # the library's own kernels only)
+    torch.cuda._sleep(1)
+    torch.cuda.synchronize()
     side = torch.cuda.Stream()
     side.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(side):
