@@ -169,43 +169,6 @@ __device__ void cta_topk(const uint64_t* keys, int n, int k_sel, int* hist, int*
 }
 
 // ---------------------------------------------------------------------------
-// GQA operand choice by a warp-uniform switch.  For channel c, head g adds
-// q_{g,c} * (q_{g,c} >= 0 ? M_c : m_c) == max(q M, q m) (one DFMA, exact
-// product, one rounding -- the oracle's step).  The sign pattern of q over a
-// group of up to 4 heads is the same for every lane (q is per CTA), so a
-// `switch` on it selects straight-line code in which every head's operand
-// register is fixed at compile time: no per-head select instruction, one DFMA
-// per head, channel and block.
-// ---------------------------------------------------------------------------
-template <int HG, int TT, int P>
-__device__ __forceinline__ void pat_dfma(const double (&qv)[4], double xMA, double xNA, double xMB,
-                                         double xNB, double* aA, double* aB) {
-#pragma unroll
-    for (int i = 0; i < HG; ++i) {
-        aA[i] = __fma_rn(qv[i], ((P >> i) & 1) ? xMA : xNA, aA[i]);
-        if constexpr (TT == 2) aB[i] = __fma_rn(qv[i], ((P >> i) & 1) ? xMB : xNB, aB[i]);
-    }
-}
-
-template <int HG, int TT>
-__device__ __forceinline__ void sel_dfma(int pat, const double (&qv)[4], double xMA, double xNA, double xMB,
-                                         double xNB, double* aA, double* aB) {
-#define SS_PAT(P)                                                     \
-    case P:                                                           \
-        pat_dfma<HG, TT, P>(qv, xMA, xNA, xMB, xNB, aA, aB);          \
-        break;
-    if constexpr (HG == 2) {
-        switch (pat) { SS_PAT(0) SS_PAT(1) SS_PAT(2) SS_PAT(3) }
-    } else {
-        switch (pat) {
-            SS_PAT(0) SS_PAT(1) SS_PAT(2) SS_PAT(3) SS_PAT(4) SS_PAT(5) SS_PAT(6) SS_PAT(7)
-            SS_PAT(8) SS_PAT(9) SS_PAT(10) SS_PAT(11) SS_PAT(12) SS_PAT(13) SS_PAT(14) SS_PAT(15)
-        }
-    }
-#undef SS_PAT
-}
-
-// ---------------------------------------------------------------------------
 template <bool BF16, int G, bool ICV, bool MEAN, int TT>
 __global__ void __launch_bounds__(kSelThreads, (G > 1 && !MEAN && TT == 1) ? 3 : 2)
 block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
@@ -222,7 +185,8 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     // GQA bf16 (SELQ): ONE DFMA per head and channel.  The sign of q_{g,c} is
     // the same for every lane, and the min / max operands are integer-built
     // float64s whose low words are 0, so the operand of head g is the high word
-    // hN + f_g * (hM - hN) (one IMAD, f_g = [q_{g,c} >= 0]) and
+    // hN ^ (f_g & (hM ^ hN)) (one LOP3 on the integer pipe, f_g = all ones
+    // when q_{g,c} >= 0, else 0) and
     // acc + q * (q >= 0 ? M : m) == acc + max(q M, q m), rounded once.
     constexpr bool SELQ = BF16 && ICV && G > 1 && !MEAN;
     double* qs = (double*)smem_raw;                                     // [128*G] (SELQ)
@@ -327,25 +291,9 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
         if (ICV) qd *= kQScale;
         if constexpr (SELQ) {
             qs[i] = qd;                  // q * 2^896, signed
+            qf[i] = qd >= 0.0 ? -1 : 0;  // all ones: the max row M, 0: the min row m
         } else {
             qpn[i] = make_double2(qd > 0.0 ? qd : 0.0, qd < 0.0 ? qd : 0.0);
-        }
-    }
-    if constexpr (SELQ) {
-        // sign pattern of each (channel, group of <= 4 heads): bit i set when
-        // q of head 4*hg + i is >= 0 (take the max row M), clear for the min row m
-        constexpr int NHG = (G + 3) / 4, HG = G < 4 ? G : 4;
-        for (int i = tid; i < kHeadDim * NHG; i += kSelThreads) {
-            const int c = i / NHG, hg = i % NHG;
-            int pat = 0;
-            for (int t = 0; t < HG; ++t) {
-                const int g = hg * 4 + t;
-                const size_t qi = ((size_t)b * Hq + (size_t)h * G + g) * kHeadDim + c;
-                const float qv = BF16 ? __uint_as_float(((uint32_t)((const uint16_t*)q)[qi]) << 16)
-                                      : ((const float*)q)[qi];
-                pat |= (qv >= 0.f ? 1 : 0) << t;
-            }
-            qf[i] = pat;
         }
     }
     __syncthreads();
@@ -489,24 +437,37 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                 const int c = s * CPC + e;
                 if constexpr (SELQ) {
                     const int w = e >> 1;
-                    const double xNA = __hiloint2double((e & 1) ? bf16_hi_hiword(wnA[w]) : bf16_lo_hiword(wnA[w]), 0);
-                    const double xMA = __hiloint2double((e & 1) ? bf16_hi_hiword(wxA[w]) : bf16_lo_hiword(wxA[w]), 0);
-                    double xNB = 0.0, xMB = 0.0;
+                    const int32_t hNA = (e & 1) ? bf16_hi_hiword(wnA[w]) : bf16_lo_hiword(wnA[w]);
+                    const int32_t hMA = (e & 1) ? bf16_hi_hiword(wxA[w]) : bf16_lo_hiword(wxA[w]);
+                    const int32_t dA = hMA ^ hNA;   // hN ^ (d & mask) picks M or m: one LOP3
+                    int32_t hNB = 0, dB = 0;
                     if constexpr (TT == 2) {
-                        xNB = __hiloint2double((e & 1) ? bf16_hi_hiword(wnB[w]) : bf16_lo_hiword(wnB[w]), 0);
-                        xMB = __hiloint2double((e & 1) ? bf16_hi_hiword(wxB[w]) : bf16_lo_hiword(wxB[w]), 0);
+                        hNB = (e & 1) ? bf16_hi_hiword(wnB[w]) : bf16_lo_hiword(wnB[w]);
+                        dB = ((e & 1) ? bf16_hi_hiword(wxB[w]) : bf16_lo_hiword(wxB[w])) ^ hNB;
                     }
-                    constexpr int NHG = (G + 3) / 4, HG = G < 4 ? G : 4;
+                    double qv[G];
+                    int32_t fv[G];
 #pragma unroll
-                    for (int hg = 0; hg < NHG; ++hg) {
-                        double qv[4];
+                    for (int g = 0; g < G; g += 2) {
+                        const double2 t = *reinterpret_cast<const double2*>(qs + c * G + g);
+                        qv[g] = t.x;
+                        qv[g + 1] = t.y;
+                    }
 #pragma unroll
-                        for (int t = 0; t < HG; t += 2) {
-                            const double2 q2 = *reinterpret_cast<const double2*>(qs + c * G + hg * 4 + t);
-                            qv[t] = q2.x;
-                            qv[t + 1] = q2.y;
+                    for (int g = 0; g < G; g += (G >= 4 ? 4 : 2)) {
+                        if constexpr (G >= 4) {
+                            const int4 t = *reinterpret_cast<const int4*>(qf + c * G + g);
+                            fv[g] = t.x; fv[g + 1] = t.y; fv[g + 2] = t.z; fv[g + 3] = t.w;
+                        } else {
+                            const int2 t = *reinterpret_cast<const int2*>(qf + c * G + g);
+                            fv[g] = t.x; fv[g + 1] = t.y;
                         }
-                        sel_dfma<HG, TT>(qf[c * NHG + hg], qv, xMA, xNA, xMB, xNB, accA + hg * 4, accB + hg * 4);
+                    }
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        accA[g] = __fma_rn(qv[g], __hiloint2double(hNA ^ (fv[g] & dA), 0), accA[g]);
+                        if constexpr (TT == 2)
+                            accB[g] = __fma_rn(qv[g], __hiloint2double(hNB ^ (fv[g] & dB), 0), accB[g]);
                     }
                     continue;
                 }

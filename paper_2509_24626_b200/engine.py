@@ -298,6 +298,7 @@ class DecodeEngine:
                 g.slot[l], g.hit[l], g.miss_keys[l], g.miss_slots[l], g.counts[l], g.ws_cache))
 
         def _gather():
+            self._wait_saved(l, torch.cuda.current_stream(self.device))
             timed("gather", lambda: ops.flash_h2d_gather(self.host_ptr, self.host_blocks,
                                                          g.miss_keys[l], g.miss_slots[l], g.counts[l],
                                                          g.E, self.pool_kv_of(l, gi), c.block_bytes))
@@ -325,6 +326,9 @@ class DecodeEngine:
             with torch.cuda.stream(cs):
                 _cache()
                 if gather and self.server:
+                    # the job's gather may read a block sealed by an earlier step:
+                    # its ready signal waits for that layer's save (if in flight)
+                    self._wait_saved(l, cs)
                     # job j's ready signal, then the event the group's stream waits on:
                     # the done-flag wait below is ordered after its own job's signal in
                     # the graph's edges, so it can never sit in a hardware queue in
@@ -476,7 +480,7 @@ class DecodeEngine:
                          d2h_threads: int = 8) -> None:
         """Decode KV append + save: per-layer device staging for
         sealed blocks, a pinned DRAM landing buffer, the FlashD2H CPU-thread pool
-        and a side stream.  The host mirrors of tail_len / n_blk decide (without
+        and a save stream.  The host mirrors of tail_len / n_blk decide (without
         a device sync) which requests' tails fill at each step."""
         c, dev = self.cfg, self.device
         self.staging = torch.empty(c.layers, c.batch * c.num_kv_heads * c.block_elems, dtype=c.dtype,
@@ -485,12 +489,24 @@ class DecodeEngine:
                                       pin_memory=True)
         self.seal_ws = ops.alloc_workspace(3, self.dims, c.max_blk, c.topk, device=dev)
         self.fill_req = torch.empty(c.batch, dtype=torch.int32, device=dev)
+        self.fill_req_host = torch.empty(c.batch, dtype=torch.int32, pin_memory=True)
+        self.ev_fill = torch.cuda.Event()       # the last fill_req upload has been read
         self.d2h = ops.D2HEngine(d2h_threads)
         self.d2h_stream = torch.cuda.Stream(dev)
-        self.ev_save = torch.cuda.Event()
+        self.ev_sealed = torch.cuda.Event()
+        # ev_saved[l]: layer l's latest FlashD2H save is in DRAM (None: none in flight)
+        self.ev_saved: List[Optional[torch.cuda.Event]] = [None] * c.layers
         self.tail_len_host = list(tail_len_host)
         self.n_blk_host = list(n_blk_host)
         self.req_ids_host = self.req_ids.tolist()
+
+    def _wait_saved(self, l: int, stream) -> None:
+        """Order `stream` after layer l's in-flight FlashD2H save: only the
+        FlashH2D gather of a layer needs the DRAM copy of a freshly sealed
+        block (it may select and miss it); select and cache never wait."""
+        ev = getattr(self, "ev_saved", None)
+        if ev is not None and ev[l] is not None and not self._capturing:
+            stream.wait_event(ev[l])
 
     def append_kv(self, new_kv_all: torch.Tensor) -> None:
         """Append this step's token: new_kv_all [L][B][Hkv][2][d] (device).  Layer 0
@@ -501,30 +517,47 @@ class DecodeEngine:
 
     def seal_full_blocks(self) -> List[int]:
         """After the step's attention: for the requests whose tail is full, build
-        the metadata of the new block, save it to DRAM with FlashD2H on the side
-        stream, and commit (n_blk += 1, tail_len = 0).  The current stream waits
-        for the save, so the next step (which may select and miss the new block)
-        finds it in DRAM.  Returns the sealed request indices."""
+        the metadata of the new block and stage it (kv_seal_blocks), commit
+        (n_blk += 1, tail_len = 0) -- both on the current stream, a few small
+        kernels -- then save the staged blocks to DRAM with FlashD2H on the save
+        stream, fully in parallel with the next steps' work.  A
+        later step's FlashH2D gather of layer l waits for layer l's save only
+        (`_wait_saved`).  Returns the sealed request indices."""
         c = self.cfg
         fill = [b for b in range(c.batch) if self.tail_len_host[b] == BLOCK_TOKENS]
         if not fill:
             return []
         n = len(fill)
         cur = torch.cuda.current_stream(self.device)
-        self.fill_req[:n].copy_(torch.tensor(fill, dtype=torch.int32), non_blocking=False)
-        self.d2h_stream.wait_stream(cur)
+        # the staging buffers are reused: the previous save of each layer first
+        for l in range(c.layers):
+            if self.ev_saved[l] is not None:
+                cur.wait_event(self.ev_saved[l])
+        self.ev_fill.synchronize()              # the pinned upload buffer is free again
+        self.fill_req_host[:n].copy_(torch.tensor(fill, dtype=torch.int32))
+        self.fill_req[:n].copy_(self.fill_req_host[:n], non_blocking=True)
+        self.ev_fill.record(cur)
+        for l in range(c.layers):
+            ops.kv_seal_blocks(self.fill_req, n, self.tail_kv[l], self.n_blk, c.max_blk, self.meta[l],
+                               self.staging[l], self.seal_ws, self.dims)
+        ops.kv_commit(self.fill_req, n, self.n_blk, self.tail_len)
+        self.ev_sealed.record(cur)
+        self.d2h_stream.wait_event(self.ev_sealed)
         with torch.cuda.stream(self.d2h_stream):
             for l in range(c.layers):
-                ops.kv_seal_blocks(self.fill_req, n, self.tail_kv[l], self.n_blk, c.max_blk, self.meta[l],
-                                   self.staging[l], self.seal_ws, self.dims)
                 keys = [self.key0(self.req_ids_host[b], l, h) + self.n_blk_host[b]
                         for b in fill for h in range(c.num_kv_heads)]
                 ops.flash_d2h_save(self.d2h, self.staging[l], self.host_stage[l], n * c.num_kv_heads,
                                    keys, self.host_kv, self.host_blocks, c.block_bytes)
-            ops.kv_commit(self.fill_req, n, self.n_blk, self.tail_len)
-            self.ev_save.record(self.d2h_stream)
-        cur.wait_event(self.ev_save)
+                ev = torch.cuda.Event()
+                ev.record(self.d2h_stream)
+                self.ev_saved[l] = ev
         for b in fill:
             self.n_blk_host[b] += 1
             self.tail_len_host[b] = 0
         return fill
+
+    def wait_saves(self) -> None:
+        """The current stream waits for every in-flight FlashD2H save."""
+        for l in range(self.cfg.layers):
+            self._wait_saved(l, torch.cuda.current_stream(self.device))

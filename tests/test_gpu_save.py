@@ -60,15 +60,22 @@ def test_append_seal_flash_d2h_steps():
     pools = [oracle.Pool(S, cfg.fwd_len, cfg.block_bytes) for _ in range(L)]
     qs = synth.encode(synth.queries(rng, steps, (L, B, Hq, D), 0.9), dt)
     new_kvs = synth.encode(rng.standard_normal((steps, L, B, Hkv, 2, D)), dt)
-    sealed_total = 0
+    # ---- GPU: all steps back to back, no host synchronisation: each step's
+    # FlashD2H save overlaps the following steps (only a later gather of the
+    # same layer waits for it); per-step results are cloned on the stream ----
+    got = []
+    fills = []
     for t in range(steps):
-        # ---- GPU: append, step, seal ----
         eng.append_kv(to_torch(new_kvs[t]))
         for l in range(L):
             eng.layer_step(l, to_torch(qs[t, l]), stamp=t + 1)
-        fill = eng.seal_full_blocks()
-        torch.cuda.synchronize()
-        # ---- oracle ----
+        got.append([(eng.sel[l].clone(), eng.counts[l].clone(), eng.out[l].clone()) for l in range(L)])
+        fills.append(eng.seal_full_blocks())
+    eng.wait_saves()
+    torch.cuda.synchronize()
+    # ---- oracle replay, step by step ----
+    sealed_total = 0
+    for t in range(steps):
         for l in range(L):
             tl = o_tlen.copy()
             oracle.kv_append(new_kvs[t, l], o_tail[l], tl, advance=True)
@@ -77,12 +84,13 @@ def test_append_seal_flash_d2h_steps():
             r = oracle.decode_layer(qs[t, l], metas[l], o_nblk, k, pools[l], np.arange(B, dtype=np.int32),
                                     l, L, max_blk, t + 1, o_host.view(np.uint8).reshape(hb, -1), hb,
                                     o_tail[l], o_tlen, 1.0 / math.sqrt(D))
-            np.testing.assert_array_equal(eng.sel[l].cpu().numpy(), r["sel"])
-            np.testing.assert_array_equal(eng.counts[l].cpu().numpy(), r["counts"])
-            err = float(np.abs(eng.out[l].cpu().numpy() - r["out"]).max())
+            g_sel, g_cnt, g_out = got[t][l]
+            np.testing.assert_array_equal(g_sel.cpu().numpy(), r["sel"])
+            np.testing.assert_array_equal(g_cnt.cpu().numpy(), r["counts"])
+            err = float(np.abs(g_out.cpu().numpy() - r["out"]).max())
             assert err <= 2e-3, f"step {t} layer {l}: {err}"
         o_fill = [b for b in range(B) if o_tlen[b] == 32]
-        assert fill == o_fill
+        assert fills[t] == o_fill
         if o_fill:
             sealed_total += len(o_fill)
             nb_before = o_nblk.copy()
@@ -93,16 +101,16 @@ def test_append_seal_flash_d2h_steps():
                 oracle.d2h_scatter(staging.view(np.uint8).reshape(len(keys), -1), keys,
                                    o_host.view(np.uint8).reshape(hb, -1), hb)
             o_tlen, o_nblk = tl, nb
-        # ---- compare state ----
-        np.testing.assert_array_equal(eng.tail_len.cpu().numpy(), o_tlen)
-        np.testing.assert_array_equal(eng.n_blk.cpu().numpy(), o_nblk)
-        for l in range(L):
-            for b in range(B):
-                n = o_tlen[b]
-                np.testing.assert_array_equal(to_numpy(eng.tail_kv[l, b])[:, :, :n], o_tail[l, b][:, :, :n])
-            got_meta = tiled_to_logical(to_numpy(eng.meta[l]), B, Hkv, max_blk)
-            for b in range(B):
-                np.testing.assert_array_equal(got_meta[b, :, :o_nblk[b]].view(np.uint8),
-                                              metas[l][b, :, :o_nblk[b]].view(np.uint8))
+    # ---- final state ----
+    np.testing.assert_array_equal(eng.tail_len.cpu().numpy(), o_tlen)
+    np.testing.assert_array_equal(eng.n_blk.cpu().numpy(), o_nblk)
+    for l in range(L):
+        for b in range(B):
+            n = o_tlen[b]
+            np.testing.assert_array_equal(to_numpy(eng.tail_kv[l, b])[:, :, :n], o_tail[l, b][:, :, :n])
+        got_meta = tiled_to_logical(to_numpy(eng.meta[l]), B, Hkv, max_blk)
+        for b in range(B):
+            np.testing.assert_array_equal(got_meta[b, :, :o_nblk[b]].view(np.uint8),
+                                          metas[l][b, :, :o_nblk[b]].view(np.uint8))
     assert sealed_total >= 3
     np.testing.assert_array_equal(host_t.view(torch.int16).numpy().view(np.uint16), o_host.reshape(-1))
