@@ -603,6 +603,7 @@ static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_
     const int persist = knob("SS_SEL_PERSIST", 0);
     const int l2pf = knob("SS_SEL_L2PF", 0);
     const int grid = (persist && items > 2 * num_sms()) ? 2 * num_sms() : items;
+    set_carveout(kern);
     kern<<<grid, kSelThreads, smem, stream>>>(q, meta, n_blk, max_blk, k, d.num_q_heads,
                                               d.num_kv_heads, nchunks, CH, (int)pairs, l2pf, sel, scores, cand_key,
                                               cand_j, tickets);

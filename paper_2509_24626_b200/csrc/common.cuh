@@ -77,6 +77,18 @@ inline bool preload_fn(K* k) {
     return cudaFuncGetAttributes(&a, (const void*)k) == cudaSuccess;
 }
 
+// One shared-memory / L1 carve-out for every kernel of a decode step (percent
+// of the unified on-SM memory given to shared memory; < 0 leaves the driver's
+// choice).  Kernels of different request groups co-run and alternate on each
+// SM; a kernel whose preferred split differs from the SM's current one makes
+// the SM reconfigure (drain) before its CTAs can land.
+constexpr int kCarveoutDefault = -1;
+template <typename K>
+inline void set_carveout(K* k) {
+    const int v = knob("SS_CARVEOUT", kCarveoutDefault);
+    if (v >= 0) cudaFuncSetAttribute((const void*)k, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

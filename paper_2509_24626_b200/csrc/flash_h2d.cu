@@ -90,6 +90,7 @@ ss_status launch_flash_h2d(const void* host_kv, int64_t host_blocks, const int64
     if (grid > max_ctas) grid = max_ctas;
     // loads in flight per lane: 16 (default) keeps 512 KB in flight on 16 SMs
     auto kern = knob("SS_H2D_UNROLL", 16) >= 16 ? flash_h2d_kernel<16> : flash_h2d_kernel<8>;
+    set_carveout(kern);
     kern<<<(int)grid, threads, 0, stream>>>(
         (const uint4*)host_kv, host_blocks, miss_keys, miss_slots, counts, max_misses,
         (uint4*)pool_kv, block_bytes / 16, 0u);
@@ -345,6 +346,7 @@ ss_status launch_flash_h2d_serve(const void* host_kv, int64_t host_blocks, const
     if (njobs <= 0) return SS_OK;
     const int threads = knob("SS_H2D_THREADS", 128);
     const int ctas = knob("SS_H2D_CTAS", kH2DCtas);
+    set_carveout(flash_h2d_server_kernel<16>);
     flash_h2d_server_kernel<16><<<ctas, threads, 0, stream>>>(
         (const uint4*)host_kv, host_blocks, jobs, njobs, block_bytes / 16, flags, 0u,
         timeout_ns_of(timeout_us), stats);
@@ -353,6 +355,7 @@ ss_status launch_flash_h2d_serve(const void* host_kv, int64_t host_blocks, const
 }
 
 ss_status launch_flag_wait(const int32_t* flag, int32_t* counts, int64_t timeout_us, cudaStream_t stream) {
+    set_carveout(flag_wait_kernel);
     flag_wait_kernel<<<1, 32, 0, stream>>>(flag, counts, timeout_ns_of(timeout_us));
     SS_LAUNCH_CHECK();
     return SS_OK;

@@ -518,6 +518,9 @@ ss_status launch_cache(const ss_cache_pool& pool, const int32_t* sel, const int3
         const int grid = std::max(1, std::min(a.nA + a.nS, std::min(fused_ctas, num_sms())));
         cache_fused_kernel<<<grid, kCacheThreads, 0, stream>>>(a);
     } else {
+        set_carveout(cache_lookup_count_kernel);
+        set_carveout(cache_victim_kernel);
+        set_carveout(cache_assign_place_kernel);
         cache_lookup_count_kernel<<<a.nA + a.nS, kCacheThreads, 0, stream>>>(a);
         // K2, K3: plain launches (default) or programmatic dependent launches
         // (SS_CACHE_PDL=1; griddepcontrol.wait is a no-op without).  Measured in

@@ -979,6 +979,7 @@ static ss_status launch_attn_mma_t(const AttnArgs& a, const void* pool, const vo
     // dispatched into whatever SM space co-running kernels leave); warps never
     // synchronise, so the kernel is the same (warp w = warp_id * gridDim + CTA).
     // Measured: 0.89 vs 0.85 of HBM peak alone at C2, no in-step difference.
+    set_carveout(kern);
     const int cta_warps = knob("SS_ATTN_CTA_WARPS", kMmaNW);
     if (cta_warps == kMmaNW)
         kern<<<num_sms(), kMmaNW * 32, kMmaSmem, stream>>>(a, tm_pool, tm_tail);
@@ -995,6 +996,7 @@ static ss_status launch_attn_t(AttnArgs a, cudaStream_t stream) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return SS_ERR_CUDA;
+    set_carveout(kern);
     kern<<<num_sms(), AttnTraits<BF16>::NW * 32, smem, stream>>>(a);
     SS_LAUNCH_CHECK();
     return SS_OK;

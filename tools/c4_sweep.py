@@ -6,7 +6,7 @@ batch grows, the working set outgrows the cache and FlashH2D traffic per token
 rises.  LWM-7B heads (32 x d=128), 2048 blocks per request, top-64, 4 simulated
 layers (32 layers x B=256 would need 256 GiB of metadata), rho = 0.95.
 
-  python tools/c4_sweep.py [--batches 8,16,32,64,128] [--steps 12] [--cache-gib 16]
+  python tools/c4_sweep.py [--batches 8,16,32,64,128,256] [--steps 12] [--cache-gib 16] [--admission]
 """
 import argparse
 import json
@@ -32,10 +32,11 @@ def run(B, args):
                        slots_per_layer=slots, num_requests=B, dtype=torch.bfloat16, groups=1)
     eng = DecodeEngine(cfg)
     phys = 127 * n_blk                                   # 4 GiB physical host pool (aliased)
-    host_t = torch.empty(phys * cfg.block_elems, dtype=torch.bfloat16, pin_memory=True)
+    hp = ops.HostPool(phys * cfg.block_bytes)
+    host_t = hp.tensor.view(torch.bfloat16)
     meta_phys = torch.empty(phys * 2 * 128, dtype=torch.bfloat16, device="cuda")
     bench.gen_host_blocks_on_gpu(eng, host_t, phys, seed=4400, meta_phys=meta_phys)
-    eng.set_host_kv(host_t, phys)
+    eng.set_host_kv(host_t, phys, dev_ptr=hp.dev_ptr)
     tile = 32 * 2 * 128
     mp = meta_phys.view(-1, tile)
     ar = torch.arange(n_blk // 32, device="cuda")
@@ -103,13 +104,14 @@ def run(B, args):
            "working_set_over_cache": round(ws_blocks * 16384 / (args.cache_gib << 30), 3),
            "capacity_errors": errs, "last_status": status}
     del eng
+    hp.close()
     torch.cuda.empty_cache()
     return res
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--batches", default="8,16,32,64,128")
+    ap.add_argument("--batches", default="8,16,32,64,128,256")
     ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--warmup", type=int, default=14)
     ap.add_argument("--cache-gib", type=int, default=16)
