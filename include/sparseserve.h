@@ -89,7 +89,8 @@ typedef struct {
  *   keys      device, dtype dt: block i's 32 keys at keys + i*key_stride
  *             (elements), laid out [32][d].  key_stride = 32*d for packed keys,
  *             2*32*d to read the K half of [2][32][d] KV blocks in place.
- *   dst_idx   device int64 [n]: logical meta index per block, or NULL = 0..n-1.
+ *   dst_idx   device int64 [n]: logical meta index per block (< 0: block i is
+ *             skipped), or NULL = 0..n-1.
  *   n         number of blocks (0 is a no-op).
  *   meta      device, tiled layout above; per-channel min/max under the total
  *             order of the bit patterns (-0 < +0; finite inputs only). */
@@ -345,6 +346,9 @@ ss_status kv_append(const void* new_kv, void* tail_kv, int32_t* tail_len, int32_
  * head is copied to staging[i][h] (device [n_fill][Hkv][2][32][d], list order)
  * and its per-channel min/max is written to meta (tiled layout) as block
  * n_blk[b] of (b, h).  Counters are not changed (see kv_commit).
+ * Precondition: n_blk[b] < max_blk (a row is free); a request whose block
+ * table is full gets its staging copy but no metadata row (nothing out of
+ * bounds is written).
  *   ws   device, ss_workspace_size(SS_WS_SEAL, ...) bytes, no initialisation. */
 ss_status kv_seal_blocks(const int32_t* fill_req, int32_t n_fill, const void* tail_kv,
                          const int32_t* n_blk, int32_t max_blk, void* meta, void* staging,

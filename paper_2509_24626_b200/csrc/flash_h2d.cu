@@ -346,8 +346,9 @@ ss_status launch_flash_h2d_serve(const void* host_kv, int64_t host_blocks, const
     if (njobs <= 0) return SS_OK;
     const int threads = knob("SS_H2D_THREADS", 128);
     const int ctas = knob("SS_H2D_CTAS", kH2DCtas);
-    set_carveout(flash_h2d_server_kernel<16>);
-    flash_h2d_server_kernel<16><<<ctas, threads, 0, stream>>>(
+    auto kern = knob("SS_H2D_UNROLL", 16) >= 16 ? flash_h2d_server_kernel<16> : flash_h2d_server_kernel<8>;
+    set_carveout(kern);
+    kern<<<ctas, threads, 0, stream>>>(
         (const uint4*)host_kv, host_blocks, jobs, njobs, block_bytes / 16, flags, 0u,
         timeout_ns_of(timeout_us), stats);
     SS_LAUNCH_CHECK();
@@ -363,7 +364,7 @@ ss_status launch_flag_wait(const int32_t* flag, int32_t* counts, int64_t timeout
 
 bool preload_h2d() {
     return preload_fn(flash_h2d_kernel<16>) && preload_fn(flash_h2d_kernel<8>) &&
-           preload_fn(flash_h2d_server_kernel<16>) && preload_fn(flag_wait_kernel);
+           preload_fn(flash_h2d_server_kernel<16>) && preload_fn(flash_h2d_server_kernel<8>) && preload_fn(flag_wait_kernel);
 }
 
 }  // namespace ss

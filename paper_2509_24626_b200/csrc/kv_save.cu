@@ -78,7 +78,10 @@ kv_seal_copy_kernel(const int32_t* __restrict__ fill_req, const uint4* __restric
     const uint4* src = tail + ((int64_t)b * Hkv + h) * block_vecs;
     uint4* dst = staging + ((int64_t)i * Hkv + h) * block_vecs;
     for (int v = threadIdx.x; v < block_vecs; v += kSaveThreads) dst[v] = src[v];
-    if (threadIdx.x == 0) dst_idx[(int64_t)i * Hkv + h] = ((int64_t)b * Hkv + h) * max_blk + n_blk[b];
+    // a full block table (n_blk == max_blk) has no row for the new block: no
+    // metadata is written (precondition of the call; the engine checks it)
+    if (threadIdx.x == 0)
+        dst_idx[(int64_t)i * Hkv + h] = n_blk[b] < max_blk ? ((int64_t)b * Hkv + h) * max_blk + n_blk[b] : -1;
 }
 
 __global__ void kv_commit_kernel(const int32_t* __restrict__ fill_req, int n_fill, int32_t* n_blk,

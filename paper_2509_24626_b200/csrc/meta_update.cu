@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(128) meta_update_kernel(const E* __restrict__ 
             }
         }
         int64_t idx = dst_idx ? dst_idx[i] : i;
+        if (idx < 0) continue;  // no destination row (kv_seal_blocks on a full block table)
         int64_t tile = idx >> 5;
         int r = (int)(idx & 31);
         E* mt = meta + tile * (int64_t)(64 * kHeadDim);
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(128) meta_mean_kernel(const E* __restrict__ ke
         }
         const float mu = __double2float_rn(acc * (1.0 / 32.0));
         const int64_t idx = dst_idx ? dst_idx[i] : i;
+        if (idx < 0) continue;  // no destination row
         float* mt = meta + (idx >> 5) * (int64_t)(32 * kHeadDim);
         mt[((c >> 2) * 32 + (int)(idx & 31)) * 4 + (c & 3)] = mu;
     }

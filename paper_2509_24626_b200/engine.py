@@ -528,6 +528,9 @@ class DecodeEngine:
         if not fill:
             return []
         n = len(fill)
+        full = [b for b in fill if self.n_blk_host[b] >= c.max_blk]
+        if full:
+            raise ValueError(f"requests {full} have max_blk={c.max_blk} full blocks: no row for a new block")
         cur = torch.cuda.current_stream(self.device)
         # the staging buffers are reused: the previous save of each layer first
         for l in range(c.layers):

@@ -36,8 +36,10 @@ def run(mode, args):
         eng.step(qs[t], t + 1)
     torch.cuda.synchronize()
     tl0 = 31 if mode != "none" else 0
+    nb0 = W["n_blk"] - 1                 # 4095 full blocks + a 31-token tail: room for block 4096
+    eng.n_blk.fill_(nb0)
     eng.tail_len.fill_(tl0)
-    eng.enable_save_path([tl0] * c.batch, [W["n_blk"]] * c.batch, d2h_threads=8)
+    eng.enable_save_path([tl0] * c.batch, [nb0] * c.batch, d2h_threads=8)
     new_kv = torch.randn(c.layers, c.batch, c.num_kv_heads, 2, 128, device="cuda").to(torch.bfloat16)
     ev = [torch.cuda.Event(True) for _ in range(6)]
     torch.cuda.synchronize()
