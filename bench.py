@@ -289,61 +289,94 @@ class StepTimers:
 
 
 def solo_pass(eng, q_src, layers, hbm_peak, h2d_peak, stamp):
-    """Each hot-path kernel timed ALONE: one request group's select, cache,
-    FlashH2D and attention of `layers` layers, each launch bracketed by a
-    synchronize and CUDA events on the current stream (no co-running kernels).
-    This is each kernel's own roofline fraction; the in-step `kernels` numbers
-    above include the overlap with the other request group."""
+    """Each hot-path kernel timed ALONE (no co-running kernels): the launches of
+    one request group at a time for `layers` layers x all groups, phase by phase
+    -- every select, then every cache call, then every gather, then every
+    attention -- so each phase is the same kernel launched back to back on one
+    stream (inputs of different layers / groups: no L2 reuse), timed by one
+    event pair on that stream: the kernel's average launch duration.  The
+    `sync` variant brackets every launch with a synchronize (+ the launch
+    latency of an idle GPU).  These are the kernels' own roofline fractions;
+    the in-step `kernels` numbers include the overlap with other groups."""
     from paper_2509_24626_b200 import ops
     c = eng.cfg
     cur = torch.cuda.current_stream()
-    t = {"select": [], "cache": [], "gather": [], "attn": []}
-    sel_b = attn_b = miss_b = 0
-    for l in range(layers):
-        for gi, g in enumerate(eng.groups):
-            q = q_src[l, g.b0:g.b1]
+    items = [(l, gi, g) for l in range(layers) for gi, g in enumerate(eng.groups)]
 
-            def timed(name, fn):
-                torch.cuda.synchronize()
+    def launch(name, l, gi, g):
+        q = q_src[l, g.b0:g.b1]
+        if name == "select":
+            ops.ss_block_select(q, g.meta[l], g.n_blk, c.max_blk, c.topk, g.dims, g.sel[l], g.ws_select)
+        elif name == "cache":
+            ops.kv_cache_lookup_insert(eng.pool_of(l, gi), g.sel[l], g.req_ids, l, c.layers, c.max_blk, c.topk,
+                                       g.dims, stamp, g.slot[l], g.hit[l], g.miss_keys[l], g.miss_slots[l],
+                                       g.counts[l], g.ws_cache)
+        elif name == "gather":
+            ops.flash_h2d_gather(eng.host_ptr, eng.host_blocks, g.miss_keys[l], g.miss_slots[l], g.counts[l], g.E,
+                                 eng.pool_kv_of(l, gi), c.block_bytes)
+        else:
+            ops.sparse_decode_attn(q, eng.pool_kv_of(l, gi), g.slot[l], c.topk, g.tail_kv[l], g.tail_len, g.dims,
+                                   eng.scale, g.out[l], g.ws_attn, counts=g.counts[l])
+
+    names = ("select", "cache", "gather", "attn")
+    t_b2b, t_sync = {}, {k: 0.0 for k in names}
+    snap = None
+    for rep in range(2):                 # rep 0: back to back; rep 1: synchronised launches
+        for name in names:
+            if rep == 1 and name == "gather":
+                # rep 1's cache calls (same selections, same stamp) hit everything:
+                # gather / attention re-run rep 0's miss lists (still in place)
+                for (l, gi, g), cnt in zip(items, snap):
+                    g.counts[l].copy_(cnt)
+            torch.cuda.synchronize()
+            if rep == 0:
                 s, e = torch.cuda.Event(True), torch.cuda.Event(True)
-                # a 100 us device spin ahead of the start event: the launch below is
-                # enqueued before the GPU reaches `s`, so host launch latency is not timed
-                torch.cuda._sleep(200000)
+                torch.cuda._sleep(2_000_000)        # the host enqueues while the GPU spins
                 s.record(cur)
-                fn()
+                for l, gi, g in items:
+                    launch(name, l, gi, g)
                 e.record(cur)
                 torch.cuda.synchronize()
-                t[name].append(s.elapsed_time(e))
-            timed("select", lambda: ops.ss_block_select(q, g.meta[l], g.n_blk, c.max_blk, c.topk, g.dims,
-                                                        g.sel[l], g.ws_select))
-            timed("cache", lambda: ops.kv_cache_lookup_insert(
-                eng.pool_of(l, gi), g.sel[l], g.req_ids, l, c.layers, c.max_blk, c.topk, g.dims, stamp,
-                g.slot[l], g.hit[l], g.miss_keys[l], g.miss_slots[l], g.counts[l], g.ws_cache))
-            timed("gather", lambda: ops.flash_h2d_gather(eng.host_ptr, eng.host_blocks, g.miss_keys[l],
-                                                         g.miss_slots[l], g.counts[l], g.E, eng.pool_kv_of(l, gi),
-                                                         c.block_bytes))
-            timed("attn", lambda: ops.sparse_decode_attn(q, eng.pool_kv_of(l, gi), g.slot[l], c.topk, g.tail_kv[l],
-                                                         g.tail_len, g.dims, eng.scale, g.out[l], g.ws_attn,
-                                                         counts=g.counts[l]))
-            hits, miss = [int(x) for x in g.counts[l, :2].tolist()]
-            sel_b += g.nb * c.num_kv_heads * int(g.n_blk[0].item()) * 512 + q.numel() * 2
-            attn_b += (hits + miss) * c.block_bytes + c.num_q_heads * g.nb * 128 * 4
-            miss_b += miss * c.block_bytes
-    tot = {k: sum(v) * 1e-3 for k, v in t.items()}
-    n = len(t["select"])
+                t_b2b[name] = s.elapsed_time(e) * 1e-3
+                if name == "cache":
+                    snap = [g.counts[l].clone() for l, gi, g in items]
+            else:
+                for l, gi, g in items:
+                    torch.cuda.synchronize()
+                    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+                    torch.cuda._sleep(200000)
+                    s.record(cur)
+                    launch(name, l, gi, g)
+                    e.record(cur)
+                    torch.cuda.synchronize()
+                    t_sync[name] += s.elapsed_time(e) * 1e-3
+    sel_b = attn_b = miss_b = 0
+    for (l, gi, g), cnt in zip(items, snap):
+        hits, miss = [int(x) for x in cnt[:2].tolist()]
+        sel_b += g.nb * c.num_kv_heads * int(g.n_blk[0].item()) * 512 + g.nb * c.num_q_heads * 128 * 2
+        attn_b += (hits + miss) * c.block_bytes + c.num_q_heads * g.nb * 128 * 4
+        miss_b += miss * c.block_bytes
+    n = len(items)
 
     def ent(bound, byts, sec, peak):
         gbs = byts / sec / 1e9
         return {"bound": bound, "achieved": round(gbs, 1 if bound == "hbm" else 2), "peak": round(peak, 2),
                 "unit": "GB/s", "frac": round(gbs / peak, 4), "us_per_launch": round(sec * 1e6 / n, 2),
                 "bytes_per_launch": int(byts / n)}
-    return {"ss_block_select": ent("hbm", sel_b, tot["select"], hbm_peak),
-            "sparse_decode_attn": ent("hbm", attn_b, tot["attn"], hbm_peak),
-            "flash_h2d_gather": ent("host-link", miss_b, tot["gather"], h2d_peak),
-            "kv_cache_lookup_insert": {"bound": "latency", "us_per_launch": round(tot["cache"] * 1e6 / n, 2)},
-            "launches_per_kernel": n,
-            "note": f"one request group ({eng.groups[0].nb} requests) per launch, {layers} layers, each launch "
-                    "alone (synchronize before and after), events on the launching stream"}
+
+    def table(tt):
+        return {"ss_block_select": ent("hbm", sel_b, tt["select"], hbm_peak),
+                "sparse_decode_attn": ent("hbm", attn_b, tt["attn"], hbm_peak),
+                "flash_h2d_gather": ent("host-link", miss_b, tt["gather"], h2d_peak),
+                "kv_cache_lookup_insert": {"bound": "latency", "us_per_launch": round(tt["cache"] * 1e6 / n, 2)}}
+    out = table(t_b2b)
+    out["launches_per_kernel"] = n
+    out["note"] = (f"one request group (~{c.batch // len(eng.groups)} requests) per launch, {layers} layers x "
+                   f"{len(eng.groups)} groups; each kernel's {n} launches back to back on one stream, nothing "
+                   "else running (one event pair per kernel)")
+    out["sync"] = table(t_sync)
+    out["sync"]["note"] = "each launch bracketed by synchronize (idle-GPU launch latency included)"
+    return out
 
 
 def measure_flash_h2d_alone(eng, n_miss=8192, reps=3):

@@ -26,6 +26,7 @@ namespace ss {
 // in flight (2.4 MB) is still far above the PCIe bandwidth-delay product.
 constexpr int kH2DThreadsMax = 512;
 constexpr int kH2DCtas = 16;
+constexpr int kServerSmemKB = 0;  // shared memory reserved per server CTA (dedicated SMs; 0: none)
 
 template <int kH2DUnroll>
 __global__ void __launch_bounds__(kH2DThreadsMax)
@@ -348,7 +349,15 @@ ss_status launch_flash_h2d_serve(const void* host_kv, int64_t host_blocks, const
     const int ctas = knob("SS_H2D_CTAS", kH2DCtas);
     auto kern = knob("SS_H2D_UNROLL", 16) >= 16 ? flash_h2d_server_kernel<16> : flash_h2d_server_kernel<8>;
     set_carveout(kern);
-    kern<<<ctas, threads, 0, stream>>>(
+    // Dedicated SMs: a server CTA that reserves (without using) most of an SM's
+    // shared memory keeps the HBM-bound select / attention / cache CTAs off its
+    // SM.  Measured (tools/kbench.py overlap): CTAs that share an SM with the
+    // server's zero-copy loads run several times slower (their loads queue
+    // behind the PCIe-latency ones), and the kernel waits for them.
+    const int smem = knob("SS_H2D_SMEM_KB", kServerSmemKB) * 1024;
+    if (smem > 0 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return SS_ERR_CUDA;
+    kern<<<ctas, threads, smem, stream>>>(
         (const uint4*)host_kv, host_blocks, jobs, njobs, block_bytes / 16, flags, 0u,
         timeout_ns_of(timeout_us), stats);
     SS_LAUNCH_CHECK();
