@@ -320,6 +320,204 @@ flash_h2d_server_kernel(const uint4* __restrict__ host, int64_t host_blocks,
     }
 }
 
+// Pipelined server (default): each warp keeps TWO units in flight.  It claims
+// and issues the loads of its next unit BEFORE it stores, fences and counts
+// the current one, so the PCIe link always has this warp's next 8 KiB of
+// reads outstanding while the current unit's HBM stores drain and its
+// completion atomics round-trip (inside a decode step those take microseconds:
+// HBM is saturated by the other request groups' select / attention).  Same job
+// protocol, statistics and abort as flash_h2d_server_kernel.
+struct SrvUnit {
+    int pj, pu, pnu;  // job, unit, units of the job (pj < 0: none)
+};
+
+template <int kU>
+__global__ void __launch_bounds__(256)
+flash_h2d_server_pipe_kernel(const uint4* __restrict__ host, int64_t host_blocks,
+                             const ss_h2d_job* __restrict__ jobs, int njobs, int64_t vpb,
+                             int32_t* flags, uint32_t zero, uint64_t timeout_ns,
+                             unsigned long long* stats) {
+    int32_t* ready = flags;
+    int32_t* done = flags + njobs;
+    int32_t* cursor = flags + 2 * njobs;
+    int32_t* fin = flags + 3 * njobs;
+    int32_t* abort_flag = flags + 4 * njobs;
+    int32_t* busy = stats ? (int32_t*)(stats + 6) : nullptr;
+    uint64_t* idle_t0 = stats ? (uint64_t*)(stats + 7) : nullptr;
+    ServeStats st{stats};
+    const int lane = lane_id();
+    constexpr int64_t kBatch = 32 * kU;
+    const int upb = (int)((vpb + kBatch - 1) / kBatch);
+    int lo = 0;
+    bool aborted = false;
+    uint64_t t_idle = gtimer_ns(), idle_sum = 0;
+    bool polling = false;
+
+    // one scan for a unit of the lowest ready job with units left (lane 0 scans,
+    // the result is broadcast); pj < 0 if none right now
+    auto try_claim = [&]() -> SrvUnit {
+        int pj = -1, pu = 0, pnu = 0;
+        if (lane == 0) {
+            for (int jj = lo; jj < njobs; ++jj) {
+                if (ld_acquire_gpu(ready + jj) == 0) continue;
+                const int32_t* cnt = jobs[jj].counts;
+                const int err = __ldcg(cnt + 3);
+                const int n = err ? 0 : min(__ldcg(cnt + 1), jobs[jj].max_misses);
+                const int nu = n * upb;
+                const int peek = *(volatile int32_t*)(cursor + jj);
+                if (nu == 0) {
+                    if (peek == 0 && atomicAdd(cursor + jj, 1) == 0) st_release_gpu(done + jj, kDoneServed);
+                    if (jj == lo) ++lo;
+                    continue;
+                }
+                if (peek >= nu) {
+                    if (jj == lo) ++lo;
+                    continue;
+                }
+                const int u = atomicAdd(cursor + jj, 1);
+                if (u >= nu) {
+                    if (jj == lo) ++lo;
+                    continue;
+                }
+                pj = jj;
+                pu = u;
+                pnu = nu;
+                break;
+            }
+        }
+        SrvUnit r;
+        r.pj = __shfl_sync(0xffffffffu, pj, 0);
+        r.pu = __shfl_sync(0xffffffffu, pu, 0);
+        r.pnu = __shfl_sync(0xffffffffu, pnu, 0);
+        lo = __shfl_sync(0xffffffffu, lo, 0);
+        return r;
+    };
+    // source / destination of a unit (lane's first vector)
+    auto addr = [&](const SrvUnit& x, const uint4*& src, uint4*& dst, int64_t& v0) {
+        const ss_h2d_job& jb = jobs[x.pj];
+        const int i = x.pu / upb, part = x.pu - i * upb;
+        src = host + (__ldcg(jb.miss_keys + i) % host_blocks) * vpb;
+        dst = (uint4*)jb.pool_kv + (int64_t)__ldcg(jb.miss_slots + i) * vpb;
+        v0 = (int64_t)part * kBatch + lane;
+    };
+    auto full_unit = [&](int64_t v0) { return v0 - lane + kBatch <= vpb; };
+    // issue a unit's loads into r (full units only)
+    auto issue = [&](const SrvUnit& x, uint4 (&r)[kU], const uint4*& src, uint4*& dst, int64_t& v0) {
+        addr(x, src, dst, v0);
+        if (full_unit(v0)) {
+#pragma unroll
+            for (int k = 0; k < kU; ++k) r[k] = ldg_stream(src + v0 + 32 * k);
+        }
+        if (lane == 0) st.busy_begin(busy, idle_t0);
+    };
+    // store a unit (every store depends on all loads through an opaque zero, so
+    // ptxas keeps the loads together), fence, count; the last unit of a job
+    // publishes done
+    auto retire = [&](const SrvUnit& x, uint4 (&r)[kU], const uint4* src, uint4* dst, int64_t v0) {
+        if (full_unit(v0)) {
+            uint32_t fold = 0;
+#pragma unroll
+            for (int k = 0; k < kU; ++k) fold ^= r[k].w;
+            const uint32_t dep = fold & zero;
+#pragma unroll
+            for (int k = 0; k < kU; ++k) {
+                uint4 y = r[k];
+                y.x ^= dep;
+                stg_v4(dst + v0 + 32 * k, y);
+            }
+        } else {
+            const int part = x.pu % upb;
+            for (int64_t v = v0; v < min(vpb, (int64_t)(part + 1) * kBatch); v += 32) stg_v4(dst + v, ldg_stream(src + v));
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+            st.busy_end(busy, idle_t0);
+            const int f = atomicAdd(fin + x.pj, 1);
+            if (f == x.pnu - 1) {
+                __threadfence();
+                st_release_gpu(done + x.pj, kDoneServed);
+            }
+        }
+    };
+    // blocking claim: polls until a unit is ready, every job is handed out
+    // (pj < 0, done), or the timeout aborts (pj < 0, aborted)
+    auto claim_wait = [&]() -> SrvUnit {
+        while (true) {
+            SrvUnit x = try_claim();
+            if (x.pj >= 0) {
+                if (lane == 0 && polling) idle_sum += gtimer_ns() - t_idle;
+                polling = false;
+                return x;
+            }
+            if (lo >= njobs) return x;
+            int stop = 0;
+            if (lane == 0) {
+                if (!polling) {
+                    polling = true;
+                    t_idle = gtimer_ns();
+                }
+                if (*(volatile int32_t*)abort_flag) {
+                    stop = 1;
+                } else if (gtimer_ns() - t_idle > timeout_ns) {
+                    if (atomicExch(abort_flag, 1) == 0 && stats) {
+                        int first = lo;
+                        while (first < njobs && ld_acquire_gpu(ready + first) != 0) ++first;
+                        stats[5] = (unsigned long long)(first + 1);
+                    }
+                    stop = 1;
+                } else {
+                    __nanosleep(64);
+                }
+            }
+            if (__shfl_sync(0xffffffffu, stop, 0)) {
+                aborted = true;
+                return x;
+            }
+        }
+    };
+
+    uint4 rA[kU], rB[kU];
+    const uint4 *sA = nullptr, *sB = nullptr;
+    uint4 *dA = nullptr, *dB = nullptr;
+    int64_t vA = 0, vB = 0;
+    SrvUnit cur = claim_wait();
+    if (cur.pj >= 0) issue(cur, rA, sA, dA, vA);
+    // two steps per iteration so the register buffers alternate statically
+    while (cur.pj >= 0) {
+        SrvUnit nxt = try_claim();
+        if (nxt.pj >= 0) issue(nxt, rB, sB, dB, vB);
+        retire(cur, rA, sA, dA, vA);
+        if (nxt.pj < 0) {
+            nxt = claim_wait();
+            if (nxt.pj < 0) break;
+            issue(nxt, rB, sB, dB, vB);
+        }
+        cur = try_claim();
+        if (cur.pj >= 0) issue(cur, rA, sA, dA, vA);
+        retire(nxt, rB, sB, dB, vB);
+        if (cur.pj < 0) {
+            cur = claim_wait();
+            if (cur.pj < 0) break;
+            issue(cur, rA, sA, dA, vA);
+        }
+    }
+    if (lane == 0 && stats) {
+        if (polling) idle_sum += gtimer_ns() - t_idle;
+        atomicAdd(stats + 0, idle_sum);
+        atomicAdd(stats + 1, 1ull);
+    }
+    if (aborted && lane == 0) {
+        for (int jj = 0; jj < njobs; ++jj) {
+            if (ld_acquire_gpu(done + jj) == 0) {
+                atomicExch(jobs[jj].counts + 3, (int)SS_ERR_CUDA);
+                __threadfence();
+                st_release_gpu(done + jj, kDoneAborted);
+            }
+        }
+    }
+}
+
 // Stream-ordered wait for a done flag.  flag == 2 (the server aborted this
 // job) or a wait that times out marks the job failed in its counts word (this
 // kernel runs after the job's producer, so the mark cannot be overwritten by
@@ -347,7 +545,10 @@ ss_status launch_flash_h2d_serve(const void* host_kv, int64_t host_blocks, const
     if (njobs <= 0) return SS_OK;
     const int threads = knob("SS_H2D_THREADS", 128);
     const int ctas = knob("SS_H2D_CTAS", kH2DCtas);
-    auto kern = knob("SS_H2D_UNROLL", 16) >= 16 ? flash_h2d_server_kernel<16> : flash_h2d_server_kernel<8>;
+    const bool pipe = knob("SS_H2D_PIPE", 1) != 0;
+    const bool u16 = knob("SS_H2D_UNROLL", 16) >= 16;
+    auto kern = pipe ? (u16 ? flash_h2d_server_pipe_kernel<16> : flash_h2d_server_pipe_kernel<8>)
+                     : (u16 ? flash_h2d_server_kernel<16> : flash_h2d_server_kernel<8>);
     set_carveout(kern);
     // Dedicated SMs: a server CTA that reserves (without using) most of an SM's
     // shared memory keeps the HBM-bound select / attention / cache CTAs off its
@@ -373,7 +574,8 @@ ss_status launch_flag_wait(const int32_t* flag, int32_t* counts, int64_t timeout
 
 bool preload_h2d() {
     return preload_fn(flash_h2d_kernel<16>) && preload_fn(flash_h2d_kernel<8>) &&
-           preload_fn(flash_h2d_server_kernel<16>) && preload_fn(flash_h2d_server_kernel<8>) && preload_fn(flag_wait_kernel);
+           preload_fn(flash_h2d_server_kernel<16>) && preload_fn(flash_h2d_server_kernel<8>) &&
+           preload_fn(flash_h2d_server_pipe_kernel<16>) && preload_fn(flash_h2d_server_pipe_kernel<8>) && preload_fn(flag_wait_kernel);
 }
 
 }  // namespace ss
