@@ -155,7 +155,8 @@ def main():
         print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}))
 
 
-if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] in ("overlap", "meta", "d2h", "prefill", "h2dsweep")):
+if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] in ("overlap", "meta", "d2h", "prefill", "h2dsweep",
+                                                                          "h2dload")):
     main()
 
 
@@ -339,3 +340,52 @@ def bench_h2d_sweep(total_mib=256, iters=3):
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "h2dsweep":
     for r in bench_h2d_sweep():
         print(json.dumps(r))
+
+
+def bench_h2d_under_load(nmiss=8192, iters=3):
+    """FlashH2D (the per-launch gather, 16 CTAs) alone vs while a device-to-device
+    copy keeps HBM busy on another stream (~read + write at full bandwidth): how
+    much PCIe goodput the zero-copy loads keep when HBM is saturated, as it is
+    inside the decode step."""
+    hb = (4 << 30) // 16384
+    host = torch.empty(hb * 8192, dtype=torch.bfloat16, pin_memory=True)
+    ptr = ops.host_device_pointer(host)
+    pool = torch.empty(nmiss * 8192, dtype=torch.bfloat16, device="cuda")
+    keys = torch.randint(0, hb, (nmiss,), device="cuda", dtype=torch.int64)
+    slots = torch.arange(nmiss, dtype=torch.int32, device="cuda")
+    counts = torch.tensor([0, nmiss, 0, 0], dtype=torch.int32, device="cuda")
+    a = torch.empty(4 << 30, dtype=torch.uint8, device="cuda")
+    b = torch.empty_like(a)
+    side = torch.cuda.Stream()
+    res = {}
+    for mode in ("alone", "hbm_copy_concurrent"):
+        ts = []
+        for _ in range(iters + 1):
+            torch.cuda.synchronize()
+            if mode != "alone":
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    for _ in range(4):
+                        b.copy_(a)
+            s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+            torch.cuda._sleep(100000)
+            s.record()
+            ops.flash_h2d_gather(ptr, hb, keys, slots, counts, nmiss, pool, 16384)
+            e.record()
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e))
+        ms = sorted(ts[1:])[len(ts[1:]) // 2]
+        res[mode + "_GBps"] = round(nmiss * 16384 / ms / 1e6, 2)
+    t0 = torch.cuda.Event(True)
+    t1 = torch.cuda.Event(True)
+    t0.record()
+    for _ in range(4):
+        b.copy_(a)
+    t1.record()
+    torch.cuda.synchronize()
+    res["hbm_copy_alone_GBps"] = round(4 * 2 * a.numel() / t0.elapsed_time(t1) / 1e6, 1)
+    return res
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "h2dload":
+    print(json.dumps(bench_h2d_under_load()))
