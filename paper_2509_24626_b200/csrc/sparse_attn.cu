@@ -561,11 +561,40 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
 // FMA path does; P is split p = hi + lo (both bf16, |p - hi - lo| <= 2^-17 p),
 // so P V carries ~2^-17 relative error instead of bf16's 2^-9.
 // ============================================================================
-constexpr int kMmaNW = 6;  // warps per CTA: 6 x 32 KiB of stages
+// Stages per warp (NS) and warps per CTA (NW) trade pipeline depth against the
+// number of warps a pair is split across: NS x NW x 16 KiB stays ~192 KiB per
+// CTA (one CTA per SM).  NS = 2, NW = 6 (round 1) splits a C3 pair over ~16
+// warps; NS = 4, NW = 3 keeps the same bytes in flight per SM with half the
+// warps, so half the partials to merge per pair.
+constexpr int kMmaNW = 6;  // warps per CTA at NS = 2 (workspace sizing bound)
+template <int NS>
+struct MmaCfg {
+    static constexpr int NW = NS == 2 ? 6 : (NS == 3 ? 4 : 3);
+};
 
+template <int NS>
 struct MmaWarpSmem {
-    alignas(1024) unsigned char buf[2][16384];  // [stage] K-lo | K-hi | V-lo | V-hi
-    uint64_t bar[2][2];                          // [stage][K half / V half]
+    alignas(1024) unsigned char buf[NS][16384];  // [stage] K-lo | K-hi | V-lo | V-hi
+    uint64_t bar[NS][2];                          // [stage][K half / V half]
+};
+
+// Per-stage unit descriptors kept in registers: a runtime stage index selects
+// among statically indexed scalars (no local-memory array).
+template <int NS>
+struct StageRegs {
+    int kind[NS], row[NS], pair[NS];
+    __device__ __forceinline__ int get(const int (&a)[NS], int s) const {
+        int v = a[0];
+#pragma unroll
+        for (int i = 1; i < NS; ++i)
+            if (s == i) v = a[i];
+        return v;
+    }
+    __device__ __forceinline__ void set(int (&a)[NS], int s, int v) {
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+            if (s == i) a[i] = v;
+    }
 };
 
 __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* tm, int x, int y,
@@ -605,15 +634,15 @@ __device__ __forceinline__ uint32_t bf16x2_bits(__nv_bfloat162 v) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int G>
-__global__ void __launch_bounds__(kMmaNW * 32, 1)
+template <int G, int NS>
+__global__ void __launch_bounds__(MmaCfg<NS>::NW * 32, 1)
 sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_pool,
                        const __grid_constant__ CUtensorMap tm_tail) {
     if (a.counts != nullptr && a.counts[3] != 0) return;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* base = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    MmaWarpSmem& sm = reinterpret_cast<MmaWarpSmem*>(base)[warp_id()];
+    MmaWarpSmem<NS>& sm = reinterpret_cast<MmaWarpSmem<NS>*>(base)[warp_id()];
     const int lane = lane_id();
     const int w = warp_id() * gridDim.x + blockIdx.x;
     if (w >= a.W) return;
@@ -630,10 +659,11 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
     trace(0);
 
     if (lane == 0) {
-        mbar_init(&sm.bar[0][0], 1);
-        mbar_init(&sm.bar[0][1], 1);
-        mbar_init(&sm.bar[1][0], 1);
-        mbar_init(&sm.bar[1][1], 1);
+#pragma unroll
+        for (int st = 0; st < NS; ++st) {
+            mbar_init(&sm.bar[st][0], 1);
+            mbar_init(&sm.bar[st][1], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_pool)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_tail)) : "memory");
@@ -665,15 +695,16 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
         }
     };
     refill();
-    int next_l = 0;                       // next lane of the window to consider
-    int kind0 = 0, kind1 = 0;             // unit held by stage 0 / 1: kind (0 = none)
-    int row0 = 0, row1 = 0;               // its K row in the tensor map
-    int pair0 = -1, pair1 = -1;           // its pair (-1 = none)
+    int next_l = 0;   // next lane of the window to consider
+    // unit held by each stage: kind (0 = none), K row in the tensor map, pair (-1 = none)
+    StageRegs<NS> sr;
+#pragma unroll
+    for (int st = 0; st < NS; ++st) sr.kind[st] = 0, sr.row[st] = 0, sr.pair[st] = -1;
     auto issue_half = [&](int stage, int half) {
-        const int kind = stage ? kind1 : kind0;
+        const int kind = sr.get(sr.kind, stage);
         if (lane == 0 && kind != 0) {
             const CUtensorMap* tm = kind == 1 ? &tm_pool : &tm_tail;
-            const int row = (stage ? row1 : row0) + 32 * half;
+            const int row = sr.get(sr.row, stage) + 32 * half;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&sm.bar[stage][half], 8192);
             const uint32_t dst = smem_u32(sm.buf[stage]) + half * 8192;
@@ -687,16 +718,16 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
             if (m) {
                 const int l = __ffs(m) - 1;
                 next_l = l + 1;
-                (stage ? kind1 : kind0) = __shfl_sync(0xffffffffu, wkind, l);
-                (stage ? row1 : row0) = __shfl_sync(0xffffffffu, wrow, l);
-                (stage ? pair1 : pair0) = __shfl_sync(0xffffffffu, wpair, l);
+                sr.set(sr.kind, stage, __shfl_sync(0xffffffffu, wkind, l));
+                sr.set(sr.row, stage, __shfl_sync(0xffffffffu, wrow, l));
+                sr.set(sr.pair, stage, __shfl_sync(0xffffffffu, wpair, l));
                 issue_half(stage, 0);
                 return;
             }
             if (wbase + 32 >= u1) {
                 next_l = 32;
-                (stage ? kind1 : kind0) = 0;
-                (stage ? pair1 : pair0) = -1;
+                sr.set(sr.kind, stage, 0);
+                sr.set(sr.pair, stage, -1);
                 return;
             }
             wbase += 32;
@@ -704,10 +735,11 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
             refill();
         }
     };
-    issue_k(0);
-    issue_half(0, 1);
-    issue_k(1);
-    issue_half(1, 1);
+#pragma unroll
+    for (int st = 0; st < NS; ++st) {
+        issue_k(st);
+        issue_half(st, 1);
+    }
     uint32_t phases = 0u;
     int stage = 0;
 
@@ -745,8 +777,8 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
         for (int md = 0; md < 8; ++md) o[md][0] = o[md][1] = o[md][2] = o[md][3] = 0.f;
         const int tl = __ldg(a.tail_len + b);
 
-        while ((stage ? pair1 : pair0) == (int)p) {
-            const bool is_tail = (stage ? kind1 : kind0) == 2;
+        while (sr.get(sr.pair, stage) == (int)p) {
+            const bool is_tail = sr.get(sr.kind, stage) == 2;
             mbar_wait(&sm.bar[stage][0], (phases >> (2 * stage)) & 1u);
             phases ^= 1u << (2 * stage);
             const uint32_t kb = smem_u32(sm.buf[stage]);
@@ -860,7 +892,7 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
             }
             __syncwarp();
             issue_half(stage, 1);  // V half of this stage's next unit
-            stage ^= 1;
+            stage = stage + 1 == NS ? 0 : stage + 1;
         }
 
         // ---- flush pair p: lane holds heads 2c + e, dims 16md + r (+8) ----
@@ -959,9 +991,19 @@ static bool encode_kv_map(CUtensorMap* m, const void* base, uint64_t rows) {
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-constexpr size_t kMmaSmem = sizeof(MmaWarpSmem) * kMmaNW + 1024;  // + base alignment slack
+template <int NS>
+constexpr size_t mma_smem() {  // + base alignment slack
+    return sizeof(MmaWarpSmem<NS>) * MmaCfg<NS>::NW + 1024;
+}
+constexpr int kAttnStages = 2;  // default stages per warp (NS); SS_ATTN_STAGES=3|4 (debug A/B)
 
-template <int G>
+static int mma_stages() {
+    const int ns = knob("SS_ATTN_STAGES", kAttnStages);
+    return (ns == 3 || ns == 4) ? ns : 2;
+}
+static int mma_nw(int ns) { return ns == 2 ? MmaCfg<2>::NW : ns == 3 ? MmaCfg<3>::NW : MmaCfg<4>::NW; }
+
+template <int G, int NS>
 static ss_status launch_attn_mma_t(const AttnArgs& a, const void* pool, const void* tail,
                                    cudaStream_t stream) {
     CUtensorMap tm_pool, tm_tail;
@@ -970,21 +1012,22 @@ static ss_status launch_attn_mma_t(const AttnArgs& a, const void* pool, const vo
     if (!encode_kv_map(&tm_pool, pool, (uint64_t)INT32_MAX) ||
         !encode_kv_map(&tm_tail, tail, (uint64_t)a.B * a.Hkv * 2 * kBlockTokens))
         return SS_ERR_CUDA;
-    auto kern = sparse_attn_mma_kernel<G>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem) !=
+    auto kern = sparse_attn_mma_kernel<G, NS>;
+    constexpr int NW = MmaCfg<NS>::NW;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mma_smem<NS>()) !=
         cudaSuccess)
         return SS_ERR_CUDA;
-    // persistent 6-warp CTAs, one per SM (default).  SS_ATTN_CTA_WARPS=1
-    // launches one-warp CTAs instead (each warp's 33 KiB of stages its own CTA,
+    // persistent NW-warp CTAs, one per SM (default).  SS_ATTN_CTA_WARPS=1
+    // launches one-warp CTAs instead (each warp's stages its own CTA,
     // dispatched into whatever SM space co-running kernels leave); warps never
     // synchronise, so the kernel is the same (warp w = warp_id * gridDim + CTA).
-    // Measured: 0.89 vs 0.85 of HBM peak alone at C2, no in-step difference.
+    // Measured (NS = 2): 0.89 vs 0.85 of HBM peak alone at C2, no in-step difference.
     set_carveout(kern);
-    const int cta_warps = knob("SS_ATTN_CTA_WARPS", kMmaNW);
-    if (cta_warps == kMmaNW)
-        kern<<<num_sms(), kMmaNW * 32, kMmaSmem, stream>>>(a, tm_pool, tm_tail);
+    const int cta_warps = knob("SS_ATTN_CTA_WARPS", NW);
+    if (cta_warps == NW)
+        kern<<<num_sms(), NW * 32, mma_smem<NS>(), stream>>>(a, tm_pool, tm_tail);
     else
-        kern<<<a.W, 32, sizeof(MmaWarpSmem) + 1024, stream>>>(a, tm_pool, tm_tail);
+        kern<<<a.W, 32, sizeof(MmaWarpSmem<NS>) + 1024, stream>>>(a, tm_pool, tm_tail);
     SS_LAUNCH_CHECK();
     return SS_OK;
 }
@@ -1067,16 +1110,21 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
     // ranges when the problem is small (C3: ~16 partials per pair to merge instead
     // of ~28); W <= U keeps every range non-empty
     const int min_units = knob("SS_ATTN_MIN_UNITS", kMinUnitsPerWarp);
-    a.W = (int)std::max<int64_t>(1, std::min<int64_t>(attn_total_warps(dt), a.U / std::max(1, min_units)));
+    // bf16 tensor-core path (SS_ATTN_MMA=0 selects the CUDA-core FMA path)
+    const int use_mma = knob("SS_ATTN_MMA", 1);
+    const int ns = mma_stages();
+    const int total_warps = (dt == SS_BF16 && use_mma) ? num_sms() * mma_nw(ns) : attn_total_warps(dt);
+    a.W = (int)std::max<int64_t>(1, std::min<int64_t>(total_warps, a.U / std::max(1, min_units)));
     size_t part = (size_t)a.W * 2 * G * kAttnPartStride * 4;
     a.part = (float*)ws;
     a.tickets = (int32_t*)((char*)ws + part);
     a.trace = attn_trace_on() ? (unsigned long long*)((char*)ws + attn_ws_bytes_core(d, dt)) : nullptr;
-    // bf16: tensor-core path (SS_ATTN_MMA=0 selects the CUDA-core FMA path)
-    const int use_mma = knob("SS_ATTN_MMA", 1);
 #define SS_ATTN_CASE(GG)                                                                    \
     case GG:                                                                                \
-        if (dt == SS_BF16 && use_mma) return launch_attn_mma_t<GG>(a, pool_kv, tail_kv, stream); \
+        if (dt == SS_BF16 && use_mma)                                                      \
+            return ns == 4 ? launch_attn_mma_t<GG, 4>(a, pool_kv, tail_kv, stream)        \
+                 : ns == 3 ? launch_attn_mma_t<GG, 3>(a, pool_kv, tail_kv, stream)        \
+                           : launch_attn_mma_t<GG, 2>(a, pool_kv, tail_kv, stream);       \
         return dt == SS_BF16 ? launch_attn_t<true, GG>(a, stream) : launch_attn_t<false, GG>(a, stream);
     switch (G) {
         SS_ATTN_CASE(1)
@@ -1092,7 +1140,9 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
 bool preload_attn() {
     bool ok = preload_fn(attn_merge_kernel);
 #define SS_PL(GG)                                              \
-    ok &= preload_fn(sparse_attn_mma_kernel<GG>);             \
+    ok &= preload_fn(sparse_attn_mma_kernel<GG, 2>);          \
+    ok &= preload_fn(sparse_attn_mma_kernel<GG, 3>);          \
+    ok &= preload_fn(sparse_attn_mma_kernel<GG, 4>);          \
     ok &= preload_fn(sparse_attn_kernel<true, GG>);           \
     ok &= preload_fn(sparse_attn_kernel<false, GG>);
     SS_PL(1) SS_PL(2) SS_PL(4) SS_PL(8)
