@@ -669,7 +669,8 @@ def bench_ours(args):
 
     # ---- e2e through the public API with host buffers (right after the timed
     # region, so both see a comparable, warmed cache): every step copies its q
-    # in from pinned host memory and its outputs out ----
+    # in from pinned host memory and its outputs out, inside the timed region;
+    # with the graph it is one ss_decode_step_host C-ABI call per step ----
     q_host = qs[t_e2e:t_e2e + e2e_steps].cpu().pin_memory()
     outs = gatherer.outputs() if gatherer is not None else eng.outputs()
     out_host = [torch.empty(o.shape, dtype=torch.float32, pin_memory=True) for o in outs]
@@ -678,10 +679,16 @@ def bench_ours(args):
     e2e_cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
     torch.cuda._sleep(HOST_AHEAD_CYCLES)
     e_s.record()
+    from paper_2509_24626_b200 import ops as _ops
     for i in range(e2e_steps):
-        do_step(q_host[i], t_e2e + i)
-        for oh, o in zip(out_host, outs):
-            oh.copy_(o, non_blocking=True)
+        if graph is not None:
+            # one C-ABI call per step: q host -> device, the step graph, outputs
+            # device -> host (ss_decode_step_host)
+            _ops.decode_step_host(graph, q_host[i], q_static, outs, out_host)
+        else:
+            do_step(q_host[i], t_e2e + i)
+            for oh, o in zip(out_host, outs):
+                oh.copy_(o, non_blocking=True)
         counts_sum(e2e_cnt)
     e_e.record()
     barrier()
@@ -691,6 +698,9 @@ def bench_ours(args):
            "h2d_bytes_per_step": int(q_host[0].numel() * q_host.element_size()),
            "d2h_bytes_per_step": int(sum(o.numel() * o.element_size() for o in out_host)),
            "steps": e2e_steps,
+           "via": ("ss_decode_step_host (C ABI) per step: pinned q host->device, the step graph, every "
+                   "layer's outputs device->host" if graph is not None else
+                   "eager engine step + torch copies from / to pinned host memory"),
            "hit_rate": round(float(e2e_cnt[0]) / max(1.0, float(e2e_cnt[0] + e2e_cnt[1])), 4),
            "misses_per_step": float(e2e_cnt[1]) / e2e_steps}
 

@@ -460,6 +460,19 @@ ss_status ss_host_free(void* host, size_t bytes);
 const char* ss_status_string(ss_status s);
 const char* ss_version(void);
 
+/* One decode step from HOST buffers (the e2e path of the benchmark): copies
+ * this step's queries host -> device, launches the step's instantiated CUDA
+ * graph (every layer's S1..S5 (+S6) calls of this library, captured by the
+ * caller), and copies the step's outputs device -> host, all enqueued on
+ * `stream` in that order; nothing synchronises.
+ *   graph_exec  cudaGraphExec_t of the captured step.
+ *   q_host      pinned host [q_bytes] -> q_dev (the graph's query buffer).
+ *   out_dev[i]  device outputs -> out_host[i] (pinned) [out_bytes[i]], i < n_out.
+ * Errors: SS_ERR_INVALID_ARG (null pointers), SS_ERR_CUDA (enqueue failed). */
+ss_status ss_decode_step_host(void* graph_exec, const void* q_host, void* q_dev, size_t q_bytes,
+                              int32_t n_out, const void* const* out_dev, void* const* out_host,
+                              const size_t* out_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

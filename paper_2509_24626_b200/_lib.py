@@ -28,7 +28,7 @@ EXPORTS = ("block_meta_update", "ss_block_select", "kv_cache_lookup_insert", "fl
            "block_meta_update_mean", "ss_block_select_mean", "flash_h2d_serve", "ss_flag_signal",
            "ss_flag_wait", "ss_preload_kernels",
            "sparse_decode_attn_part", "sparse_attn_merge", "ss_device_numa_node", "ss_host_alloc",
-           "ss_host_free")
+           "ss_host_free", "ss_decode_step_host")
 
 
 class SSDims(ctypes.Structure):
@@ -91,6 +91,8 @@ def load() -> ctypes.CDLL:
     L.ss_host_alloc.restype = I32
     L.ss_host_free.argtypes = [P, SZ]
     L.ss_host_free.restype = I32
+    L.ss_decode_step_host.argtypes = [P, P, P, SZ, I32, P, P, P, P]
+    L.ss_decode_step_host.restype = I32
     L.ss_status_string.argtypes = [I32]
     L.ss_status_string.restype = ctypes.c_char_p
     L.ss_version.restype = ctypes.c_char_p

@@ -339,6 +339,23 @@ size_t ss_workspace_size(int32_t which, ss_dims dims, int32_t max_blk, int32_t k
     }
 }
 
+ss_status ss_decode_step_host(void* graph_exec, const void* q_host, void* q_dev, size_t q_bytes,
+                              int32_t n_out, const void* const* out_dev, void* const* out_host,
+                              const size_t* out_bytes, void* stream) {
+    if (!graph_exec || n_out < 0 || (q_bytes && (!q_host || !q_dev))) return SS_ERR_INVALID_ARG;
+    if (n_out > 0 && (!out_dev || !out_host || !out_bytes)) return SS_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (q_bytes && cudaMemcpyAsync(q_dev, q_host, q_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return SS_ERR_CUDA;
+    if (cudaGraphLaunch((cudaGraphExec_t)graph_exec, s) != cudaSuccess) return SS_ERR_CUDA;
+    for (int i = 0; i < n_out; ++i) {
+        if (!out_dev[i] || !out_host[i]) return SS_ERR_INVALID_ARG;
+        if (cudaMemcpyAsync(out_host[i], out_dev[i], out_bytes[i], cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            return SS_ERR_CUDA;
+    }
+    return SS_OK;
+}
+
 ss_status ss_host_device_pointer(void* host, void** dev) {
     if (!host || !dev) return SS_ERR_INVALID_ARG;
     return cudaHostGetDevicePointer(dev, host, 0) == cudaSuccess ? SS_OK : SS_ERR_CUDA;

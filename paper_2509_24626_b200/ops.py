@@ -188,6 +188,24 @@ class HostPool:
             pass
 
 
+def decode_step_host(graph: "torch.cuda.CUDAGraph", q_host: torch.Tensor, q_dev: torch.Tensor,
+                     outs_dev, outs_host, stream=None) -> None:
+    """One captured decode step from host buffers (ss_decode_step_host): q_host
+    (pinned) -> q_dev, graph launch, outs_dev[i] -> outs_host[i] (pinned)."""
+    import ctypes
+    n = len(outs_dev)
+    assert q_host.is_pinned() and all(o.is_pinned() for o in outs_host) and n == len(outs_host)
+    assert q_host.numel() * q_host.element_size() == q_dev.numel() * q_dev.element_size()
+    dev = (ctypes.c_void_p * max(1, n))(*[_ptr(o) for o in outs_dev])
+    host = (ctypes.c_void_p * max(1, n))(*[o.data_ptr() for o in outs_host])
+    nbytes = (ctypes.c_size_t * max(1, n))(*[o.numel() * o.element_size() for o in outs_dev])
+    for od, oh in zip(outs_dev, outs_host):
+        assert od.numel() * od.element_size() == oh.numel() * oh.element_size()
+    check(_lib.load().ss_decode_step_host(graph.raw_cuda_graph_exec(), q_host.data_ptr(), _ptr(q_dev),
+                                          q_host.numel() * q_host.element_size(), n, dev, host, nbytes,
+                                          _stream(stream)), "ss_decode_step_host")
+
+
 def flash_h2d_gather(host_kv_dev_ptr: int, host_blocks: int, miss_keys: torch.Tensor,
                      miss_slots: torch.Tensor, counts: torch.Tensor, max_misses: int,
                      pool_kv: torch.Tensor, block_bytes: int, stream=None) -> None:
