@@ -103,6 +103,14 @@ def run(B, args):
            "working_set_GiB": round(ws_blocks * 16384 / 2**30, 2),
            "working_set_over_cache": round(ws_blocks * 16384 / (args.cache_gib << 30), 3),
            "capacity_errors": errs, "last_status": status}
+    if errs:
+        # per-step demand exceeds the cache: every such layer call fails with
+        # SS_ERR_CAPACITY and attends nothing, so there is no throughput to report
+        for kk in ("ms_per_step_4_layers", "tokens_per_s_4_layers", "tokens_per_s_32_layer_equiv", "hit_rate",
+                   "misses_per_step", "h2d_MB_per_step", "h2d_KB_per_token"):
+            res[kk] = None
+        res["infeasible"] = (f"{B * H * k} selected blocks per layer-step exceed the {slots} slots of a "
+                             "layer's cache: SS_ERR_CAPACITY, nothing attended")
     del eng
     hp.close()
     torch.cuda.empty_cache()
