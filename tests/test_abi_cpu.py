@@ -125,3 +125,13 @@ def test_python_modules_import_on_cpu():
         importlib.import_module(m)
     import ast
     ast.parse(open(os.path.join(ROOT, "bench.py")).read())
+
+
+def test_bench_gpus_relaunch_refuses_without_gpus():
+    """CPU box: `bench.py --gpus 2` finds fewer visible GPUs than asked and exits 2."""
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"], capture_output=True,
+                       text=True, timeout=300, cwd=ROOT,
+                       env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert r.returncode == 2, (r.returncode, r.stderr[-2000:])
+    assert "visible" in r.stderr

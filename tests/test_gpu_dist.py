@@ -140,3 +140,17 @@ def test_bench_torchrun_world1_runs_the_multi_gpu_path():
     assert line["errors_in_timed_region"] == 0 and line.get("valid", True)
     assert line["kernels"]["nccl_all_gather"]["launches_per_step"] == 32 * line["config"]["request_groups"]
     assert line["value"] > 0
+
+
+def test_bench_gpus_beyond_visible_fails_loudly():
+    """`bench.py --gpus N` re-launches itself with N ranks; asking for more GPUs
+    than are visible must fail with a message, not silently run on one."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    n = torch.cuda.device_count() + 1
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--steps", "3",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=300, cwd=ROOT,
+                       env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert r.returncode == 2, (r.returncode, r.stdout[-2000:], r.stderr[-2000:])
+    assert "visible" in r.stderr
+    assert not [x for x in r.stdout.splitlines() if x.startswith("{")]
