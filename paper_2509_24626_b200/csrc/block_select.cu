@@ -560,8 +560,39 @@ constexpr int kSelChunkMin = 512;  // workspace sizing bound (SS_SEL_CHUNK may g
 
 // The chunk a call uses; doubled (up to kSelChunkMax) while the candidate merge
 // of the pair's chunks would exceed kSelMaxMerge keys (its shared-memory bound).
-static int sel_chunk(int G, int max_blk, int k) {
-    int ch = sel_chunk_env() ? sel_chunk_env() : (G > 1 ? kSelChunkGqa : kSelChunkDefault);
+// MHA (G = 1) chunk chooser: c chunks per pair of CH = ceil(max_blk / c)
+// blocks (multiple of 32, >= kSelChunkMin); a CTA's time is ~proportional to
+// its chunk, so a launch costs ~ceil(pairs * c / resident CTAs) waves x CH.
+// Minimise that, ties -> fewer waves.  Full C2 batch (512 pairs): c = 4 (the
+// round-1 1024); one request group (96 / 128 pairs): c = 3 / 2 -- one wave
+// instead of 1.3 / 1.7 (measured alone, tools/kbench.py --batch 3 / 4: 0.73 /
+// 0.78 of HBM vs 0.58 / 0.73 at 1024; profiles/r02_group_shape_sweep.txt).
+// GQA (G > 1) keeps 2048: there the CTAs are issue-bound and more of them in
+// flight beat whole waves (C3: 1.73 waves at 2048 157 us vs one wave at 4096
+// 165 us, 1.19 waves at 3072 191 us).
+static int sel_chunk_mha(int max_blk, int pairs) {
+    const int resident = 2 * num_sms();  // __launch_bounds__(kSelThreads, 2)
+    int best_ch = kSelChunkDefault;
+    int64_t best_cost = INT64_MAX, best_waves = INT64_MAX;
+    for (int c = 1; c <= 16; ++c) {
+        const int ch = ((max_blk + c - 1) / c + 31) / 32 * 32;
+        if (ch > kSelChunkMax) continue;
+        if (ch < kSelChunkMin) break;
+        const int chunks = (max_blk + ch - 1) / ch;
+        const int64_t waves = ((int64_t)pairs * chunks + resident - 1) / resident;
+        const int64_t cost = waves * ch;
+        if (cost < best_cost || (cost == best_cost && waves < best_waves)) {
+            best_cost = cost;
+            best_waves = waves;
+            best_ch = ch;
+        }
+    }
+    return best_ch;
+}
+
+static int sel_chunk(int G, int max_blk, int k, int pairs) {
+    int ch = sel_chunk_env() ? sel_chunk_env()
+                             : (G > 1 ? kSelChunkGqa : sel_chunk_mha(max_blk, pairs));
     while ((size_t)((max_blk + ch - 1) / ch) * k > kSelMaxMerge && ch < kSelChunkMax) ch *= 2;
     return ch;
 }
@@ -585,7 +616,7 @@ static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_
                               int k, const ss_dims& d, int32_t* sel, double* scores, void* ws,
                               cudaStream_t stream) {
     size_t pairs = (size_t)d.batch * d.num_kv_heads;
-    const int CH = sel_chunk(G, max_blk, k);
+    const int CH = sel_chunk(G, max_blk, k, (int)pairs);
     int nchunks = (max_blk + CH - 1) / CH;
     size_t nc = pairs * nchunks * k;
     int32_t* tickets = (int32_t*)ws;
@@ -616,7 +647,7 @@ ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_
                               void* ws, cudaStream_t stream, bool mean) {
     int G = d.num_q_heads / d.num_kv_heads;
     {   // the largest chunk must keep the candidate merge within kSelMaxMerge keys
-        const int ch = sel_chunk(G, max_blk, k);  // the chunk the launch will use
+        const int ch = sel_chunk(G, max_blk, k, d.batch * d.num_kv_heads);  // the chunk the launch will use
         const int nchunks = (max_blk + ch - 1) / ch;
         if ((size_t)nchunks * k > kSelMaxMerge && nchunks > 1) return SS_ERR_UNSUPPORTED;
     }
