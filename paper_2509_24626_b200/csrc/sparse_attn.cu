@@ -138,13 +138,11 @@ __device__ __forceinline__ void load_q(const AttnArgs& a, int b, int h, int lane
 }
 
 // A warp whose range cut pair p has written its partial (m, l, o) of the G
-// heads: take a ticket; the last contributor merges all partials in warp
-// order (deterministic) and writes the output, then resets the ticket.
-template <int G>
-__device__ __forceinline__ void finish_partial(const AttnArgs& a, int64_t p, int w) {
+// heads: take a ticket; true for the last contributor, which then merges all
+// partials (merge_partials).
+__device__ __forceinline__ bool partial_is_last(const AttnArgs& a, int64_t p) {
     const int lane = lane_id();
     const int Ku = a.k + 1;
-    const int b = (int)(p / a.Hkv), h = (int)(p % a.Hkv);
     __threadfence();
     __syncwarp();
     int ticket = 0;
@@ -152,7 +150,18 @@ __device__ __forceinline__ void finish_partial(const AttnArgs& a, int64_t p, int
     ticket = __shfl_sync(0xffffffffu, ticket, 0);
     const int64_t wf = warp_of_unit(p * Ku, a.U, a.W);
     const int64_t wl = warp_of_unit((p + 1) * Ku - 1, a.U, a.W);
-    if (ticket != (int)(wl - wf)) return;
+    return ticket == (int)(wl - wf);
+}
+
+// The last contributor merges all partials of pair p in warp order
+// (deterministic) and writes the output, then resets the ticket.
+template <int G>
+__device__ void merge_partials(const AttnArgs& a, int64_t p, int w) {
+    const int lane = lane_id();
+    const int Ku = a.k + 1;
+    const int b = (int)(p / a.Hkv), h = (int)(p % a.Hkv);
+    const int64_t wf = warp_of_unit(p * Ku, a.U, a.W);
+    const int64_t wl = warp_of_unit((p + 1) * Ku - 1, a.U, a.W);
     __threadfence();
     auto trace = [&](int i) {
         if (a.trace != nullptr && lane == 0) {
@@ -357,6 +366,7 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
     int stage = 0;
 
     const int64_t p_first = u0 / Ku, p_last = (u1 - 1) / Ku;
+    int64_t defer0 = -1, defer1 = -1;  // pairs this warp merges after its range
     float4 qn[G];  // q of the next pair, prefetched in registers
     load_q<BF16, G>(a, (int)(p_first / a.Hkv), (int)(p_first % a.Hkv), lane, qn);
     for (int64_t p = p_first; p <= p_last; ++p) {
@@ -533,8 +543,10 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
             *reinterpret_cast<float4*>(pp + 4 + 4 * lane) =
                 make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
         }
-        finish_partial<G>(a, p, w);
+        if (partial_is_last(a, p)) (defer0 < 0 ? defer0 : defer1) = p;  // merged after the range
     }
+    if (defer0 >= 0) merge_partials<G>(a, defer0, w);
+    if (defer1 >= 0) merge_partials<G>(a, defer1, w);
 }
 
 // ============================================================================
@@ -755,6 +767,7 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
     const uint32_t v_hi = (uint32_t)(mi & 1);
 
     const int64_t p_first = u0 / Ku, p_last = (u1 - 1) / Ku;
+    int64_t defer0 = -1, defer1 = -1;  // pairs this warp merges after its range
     for (int64_t p = p_first; p <= p_last; ++p) {
         const int b = (int)(p / a.Hkv), h = (int)(p % a.Hkv);
         // Q^T fragment (B operand): k-step s holds head r's dims 16s+2c, +1 (b0)
@@ -931,8 +944,13 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
                 }
             }
         }
-        finish_partial<G>(a, p, w);
+        // the last contributor merges -- after its own range is streamed: a
+        // merge in the middle of a range would delay that warp's remaining
+        // units (the kernel's tail); a range cuts at most two pairs
+        if (partial_is_last(a, p)) (defer0 < 0 ? defer0 : defer1) = p;
     }
+    if (defer0 >= 0) merge_partials<G>(a, defer0, w);
+    if (defer1 >= 0) merge_partials<G>(a, defer1, w);
     trace(2);
 }
 
