@@ -234,7 +234,7 @@ __device__ void merge_partials(const AttnArgs& a, int64_t p, int w) {
                 }
             }
             const int n = min(32, nc - i0);
-            constexpr int UNR = GC >= 4 ? 4 : 8;  // loads in flight vs registers
+            constexpr int UNR = GC >= 4 ? 8 : 16;  // loads in flight vs registers (the stage registers are dead here)
 #pragma unroll UNR
             for (int j = 0; j < n; ++j) {
                 const int64_t bj = __shfl_sync(0xffffffffu, base_i, j);
