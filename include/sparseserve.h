@@ -14,13 +14,21 @@
  *   sparse_decode_attn     S5     attention over the selected blocks + tail
  *
  * and block_meta_update (S0) runs when a block fills.
+ * Around them: flash_h2d_serve (S4 for a whole step in one persistent launch,
+ * with ss_flag_signal / ss_flag_wait), ss_host_alloc (the NUMA-placed pinned
+ * host KV pool), ss_decode_step_host (one captured step from host buffers),
+ * and the NEXT-row calls (KV append / seal / FlashD2H save, working set,
+ * admission, prefill layer save, mean-of-keys metadata).
  *
  * Conventions (all calls):
  *  - Every pointer is caller-owned.  "device" = cudaMalloc'd (or torch) memory
  *    on the current device; "host-mapped" = pinned host memory whose DEVICE
  *    address is passed (cudaHostAlloc / cudaHostRegister(...Mapped...) +
  *    cudaHostGetDevicePointer; under UVA that equals the host address).  The
- *    library never allocates, frees or keeps global state; calls are reentrant.
+ *    library never allocates, frees or keeps global state (exceptions, both
+ *    explicit: the FlashD2H thread pool ss_d2h_create owns threads, and
+ *    ss_host_alloc allocates the host pool the caller frees); calls are
+ *    reentrant.
  *  - `stream` is a cudaStream_t passed as void*.  Every call is asynchronous on
  *    it and never synchronises with the host.
  *  - Host-side argument errors return SS_ERR_INVALID_ARG / SS_ERR_UNSUPPORTED
@@ -36,7 +44,7 @@
  *    SS_F32.  Scores are float64, attention accumulates and outputs float32.
  *
  * Semantics are defined by the CPU oracle (oracle/oracle.c) and DESIGN.md §3
- * readings R1..R16; the CUDA path must match it bit-exactly for indices,
+ * readings R1..R20; the CUDA path must match it bit-exactly for indices,
  * masks, cache state and gathered bytes, and within 2e-3 (bf16) / 1e-5 (f32)
  * max-abs for attention outputs.
  */
