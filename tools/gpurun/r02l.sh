@@ -17,3 +17,11 @@ SS_LIB_VARIANT=debug SS_ATTN_TRACE=1 python tools/kbench.py attn --cfg C2 --batc
 SS_LIB_VARIANT=debug SS_ATTN_TRACE=1 python tools/kbench.py attn --cfg C3
 } > gpurun_out/r02l/kbench_attn.txt 2>&1
 timeout 900 python bench.py --no-cpu-baseline > gpurun_out/r02l/bench_c2.json 2> gpurun_out/r02l/bench_c2.err
+# initcheck attribution: kernel-side reads vs host copies of partly written buffers
+SEL='test_select_c1_shape or test_select_gqa_ragged_multichunk or test_cache_multistep_bit_exact or test_flash_h2d_gather_byte_exact or test_attention_tolerance or test_block_meta_update_bit_exact'
+timeout 1200 compute-sanitizer --tool initcheck --target-processes all --print-limit 100000 \
+    python -m pytest -q -x -p no:cacheprovider tests/test_gpu_parity.py -k "$SEL" > gpurun_out/r02l/initcheck_full.log 2>&1
+grep -c "on access by cudaMemcpy" gpurun_out/r02l/initcheck_full.log > gpurun_out/r02l/initcheck_counts.txt
+grep -c "by thread" gpurun_out/r02l/initcheck_full.log >> gpurun_out/r02l/initcheck_counts.txt
+grep -A3 "by thread" gpurun_out/r02l/initcheck_full.log | grep -E "at .* in " | sed -E 's/.* in ([^ ]*).*/\1/' | sort | uniq -c >> gpurun_out/r02l/initcheck_counts.txt
+gzip -9 gpurun_out/r02l/initcheck_full.log
