@@ -88,3 +88,47 @@ def test_head_shard_ranges():
     assert head_shard(32, 32, 7, 8) == (28, 32, 28, 32)
     with pytest.raises(ValueError):
         head_shard(32, 8, 0, 3)
+
+
+def _og_worker(rank, world, port, ret):
+    """OutputGather (the bench's S6 hook) over gloo: per request group its own
+    communicator and a [L][Hq][nb][d] gathered buffer."""
+    import types
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2509_24626_b200.shard import OutputGather
+    L, hq_local, d = 3, 4, 8
+    nbs = [2, 3]
+    groups = []
+    for gi, nb in enumerate(nbs):
+        out = torch.arange(L * hq_local * nb * d, dtype=torch.float32).view(L, hq_local, nb, d)
+        groups.append(types.SimpleNamespace(nb=nb, out=out + 1000 * rank + 100 * gi))
+    eng = types.SimpleNamespace(cfg=types.SimpleNamespace(layers=L, num_q_heads=hq_local), groups=groups,
+                                device=torch.device("cpu"))
+    og = OutputGather(eng, world)
+    hook = og.hook()
+    for l in range(L):
+        for gi, g in enumerate(groups):
+            hook(gi, g, l)
+    if rank == 0:
+        ret.put([t.numpy() for t in og.outputs()])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_output_gather_hook_world2():
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_og_worker, args=(r, 2, port, ret)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = ret.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    L, hq_local, d = 3, 4, 8
+    for gi, nb in enumerate([2, 3]):
+        base = np.arange(L * hq_local * nb * d, dtype=np.float32).reshape(L, hq_local, nb, d)
+        exp = np.concatenate([base + 1000 * r + 100 * gi for r in range(2)], axis=1)   # rank-major heads
+        np.testing.assert_array_equal(got[gi], exp)
