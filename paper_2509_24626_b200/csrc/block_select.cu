@@ -33,6 +33,8 @@
 // bf16 (1 KiB f32); fp64 work = 2*G*128 DFMA per block.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace ss {
@@ -88,16 +90,16 @@ __device__ __forceinline__ double f32_scaled(uint32_t x) {
 // Writes the selected positions, ascending, to out_pos (smem or global via
 // functor).  k_sel = min(k, n) positions are produced.
 // ---------------------------------------------------------------------------
-template <typename Emit>
-__device__ void cta_topk(const uint64_t* keys, int n, int k_sel, int* hist, int* sw, Emit emit) {
+template <int NT, typename Emit>
+__device__ void cta_topk_t(const uint64_t* keys, int n, int k_sel, int* hist, int* sw, Emit emit) {
     const int tid = threadIdx.x;
     uint64_t prefix = 0, mask = 0;
     int rem = k_sel;
     if (k_sel < n) {
         for (int shift = 56; shift >= 0; shift -= 8) {
-            for (int i = tid; i < 256; i += kSelThreads) hist[i] = 0;
+            for (int i = tid; i < 256; i += NT) hist[i] = 0;
             __syncthreads();
-            for (int i = tid; i < n; i += kSelThreads) {
+            for (int i = tid; i < n; i += NT) {
                 uint64_t key = keys[i];
                 if ((key & mask) == prefix) atomicAdd(&hist[(int)((key >> shift) & 0xFF)], 1);
             }
@@ -139,12 +141,12 @@ __device__ void cta_topk(const uint64_t* keys, int n, int k_sel, int* hist, int*
         rem = n;  // all (every key matches the empty prefix)
     }
     // Compaction in position order.  Thread t owns positions [t*per, (t+1)*per).
-    const int per = (n + kSelThreads - 1) / kSelThreads;
+    const int per = (n + NT - 1) / NT;
     const int p0 = tid * per, p1 = min(n, p0 + per);
     int eq = 0;
     for (int p = p0; p < p1; ++p) eq += ((keys[p] & mask) == prefix);
     int tot;
-    int eq_base = block_excl_scan<kSelThreads>(eq, sw, tot);
+    int eq_base = block_excl_scan<NT>(eq, sw, tot);
     int nsel = 0;
     {
         int er = eq_base;
@@ -155,7 +157,7 @@ __device__ void cta_topk(const uint64_t* keys, int n, int k_sel, int* hist, int*
             nsel += s;
         }
     }
-    int out_base = block_excl_scan<kSelThreads>(nsel, sw, tot);
+    int out_base = block_excl_scan<NT>(nsel, sw, tot);
     {
         int er = eq_base, o = out_base;
         for (int p = p0; p < p1; ++p) {
@@ -169,6 +171,11 @@ __device__ void cta_topk(const uint64_t* keys, int n, int k_sel, int* hist, int*
 }
 
 // ---------------------------------------------------------------------------
+template <typename Emit>
+__device__ __forceinline__ void cta_topk(const uint64_t* keys, int n, int k_sel, int* hist, int* sw, Emit emit) {
+    cta_topk_t<kSelThreads>(keys, n, k_sel, hist, sw, emit);
+}
+
 template <bool BF16, int G, bool ICV, bool MEAN, int TT>
 __global__ void __launch_bounds__(kSelThreads, (G > 1 && !MEAN && TT == 1) ? 3 : 2)
 block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
@@ -545,6 +552,313 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     }  // work items
 }
 
+// ---------------------------------------------------------------------------
+// GQA select on the tensor cores, exact by filtering (bf16, G = 2, 4, 8).
+//
+// The score is a dense contraction: S_g(j) = sum_c max(q_gc M_jc, q_gc m_jc)
+// = sum over the 256 "channels" [m_j0..m_j127, M_j0..M_j127] of
+// [q-_g ; q+_g] (q+ = max(q, 0), q- = min(q, 0); one of the two products is an
+// exact 0).  So a warp computes approximate scores of 16 blocks x 8 heads per
+// mma.sync m16n8k16 (bf16 x bf16 products are exact in the f32 accumulator;
+// the A operand is the metadata tile exactly as stored, ldmatrix'd from
+// shared memory; the B operand is q), and a second mma over |A| x |B| gives
+// sum_c |q_gc X_jc|, which bounds the f32 accumulation error:
+//     |s~_j - S_j| <= eps_j = 2^-10 * max_g sum|t| + 2^-100
+// (f32 accumulation of 256 exact products, even with truncating adds, errs
+// by < 2^-13.9 sum|t|; the margin is 16x; the fp64 oracle's own rounding is
+// < 2^-45 sum|t|).  With L_j = s~_j - eps_j, U_j = s~_j + eps_j and tau the
+// k-th largest L_j of the chunk, every block of the exact top-k has U_j >= tau
+// (k blocks have S >= L >= tau; a block with U < tau has S < tau).  Those
+// candidates -- k plus the few within 2 eps of the threshold -- are rescored
+// EXACTLY (the oracle's fp64 sequential sum, as block_select_kernel does) and
+// the exact top-k with the same tie rule is taken among them: the selection is
+// bit-identical to the oracle's.  Non-finite approximations make a block a
+// candidate (L = -inf, U = +inf).  The fp64 work drops from every block to
+// ~k per chunk, the integer operand building disappears, and the kernel is
+// left with the metadata stream: 16 KiB tiles by 1-D TMA bulk copies, one
+// stage per warp, 4 warps per CTA, 2 CTAs per SM.
+// ---------------------------------------------------------------------------
+constexpr int kTcWarps = 4;
+constexpr int kTcThreads = kTcWarps * 32;
+constexpr int kTileBytes = 64 * kHeadDim * 2;  // 32 blocks x [min|max] x 128 ch, bf16
+
+__device__ __forceinline__ uint32_t ord32(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+
+// k-th largest (1-based) 32-bit key of keys[0..n): CTA radix select, 8-bit
+// digits MSB first.  Contains __syncthreads().
+__device__ uint32_t cta_kth_u32(const uint32_t* keys, int n, int kk, int* hist, int* sw) {
+    const int tid = threadIdx.x;
+    uint32_t prefix = 0, mask = 0;
+    int rem = kk;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = tid; i < 256; i += kTcThreads) hist[i] = 0;
+        __syncthreads();
+        for (int i = tid; i < n; i += kTcThreads) {
+            const uint32_t key = keys[i];
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xFF], 1);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            int cnt[8], s = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                cnt[i] = hist[255 - (tid * 8 + i)];
+                s += cnt[i];
+            }
+            const int incl = warp_incl_scan(s);
+            int above = incl - s;
+            if (above < rem && rem <= incl) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (above < rem && rem <= above + cnt[i]) {
+                        sw[40] = 255 - (tid * 8 + i);
+                        sw[41] = rem - above;
+                    }
+                    above += cnt[i];
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t digit = (uint32_t)sw[40];
+        rem = sw[41];
+        __syncthreads();
+        prefix |= digit << shift;
+        mask |= 0xFFu << shift;
+    }
+    return prefix;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kTcThreads, 2)
+block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta,
+                       const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
+                       int nchunks, int CH, int region_bytes, int32_t* __restrict__ sel,
+                       uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_j,
+                       int32_t* __restrict__ tickets) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // [region: tile stages (tile phase) | keys u64 + jpos i32 (select phase)]
+    // [lo f32 [CH]][hi f32 [CH]][qs f64 [128 G]][qf i32 [128 G]][hist 256][sw 64][bar]
+    unsigned char* stage_base = smem_raw;
+    uint64_t* keys = (uint64_t*)smem_raw;
+    float* lo = (float*)(smem_raw + region_bytes);
+    float* hi = lo + CH;
+    double* qs = (double*)(hi + CH);
+    int32_t* qf = (int32_t*)(qs + kHeadDim * G);
+    int* hist = (int*)(qf + kHeadDim * G);
+    int* sw = hist + 256;
+    uint64_t* bars = (uint64_t*)(sw + 64);
+    const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+    const int pair = blockIdx.x / nchunks, ci = blockIdx.x % nchunks;
+    const int b = pair / Hkv, h = pair % Hkv;
+    const int nb = n_blk_arr[b];
+    const int nch_b = max(1, (nb + CH - 1) / CH);
+    if (ci >= nch_b) return;
+    const int j0 = ci * CH;
+    const int nb_chunk = min(CH, nb - j0);
+    const int ntiles = (nb_chunk + 31) / 32;
+    const char* meta_pair = (const char*)meta + ((size_t)pair * (max_blk / 32)) * kTileBytes;
+    const uint16_t* qb16 = (const uint16_t*)q + ((size_t)b * Hq + (size_t)h * G) * kHeadDim;
+
+    // ---- exact-path q (x 2^896, signed) and max-row masks; mma B fragments ----
+    for (int i = tid; i < kHeadDim * G; i += kTcThreads) {
+        const int g = i % G, c = i / G;
+        const double qd = (double)__uint_as_float(((uint32_t)qb16[(size_t)g * kHeadDim + c]) << 16) * kQScale;
+        qs[i] = qd;
+        qf[i] = qd >= 0.0 ? -1 : 0;
+    }
+    if (lane == 0) {
+        mbar_init(&bars[warp], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // B fragment of chunk s (k rows 0-7: the min channels 8s..8s+7 -> q-, rows
+    // 8-15: the max channels -> q+; column n = head): lane holds rows 2c, 2c+1
+    // (b0) and 2c+8, 2c+9 (b1) of column r
+    const int r = lane >> 2, c = lane & 3;
+    uint32_t qb[16][2], qa[16][2];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        uint32_t w = 0;
+        if (r < G) w = __ldg(reinterpret_cast<const uint32_t*>(qb16 + (size_t)r * kHeadDim + 8 * s + 2 * c));
+        const uint32_t neg = ((w & 0x8000u) ? 0x0000FFFFu : 0u) | ((w & 0x80000000u) ? 0xFFFF0000u : 0u);
+        qb[s][0] = w & neg;   // q- (q < 0, incl. -0: an exact zero product either way)
+        qb[s][1] = w & ~neg;  // q+
+        qa[s][0] = qb[s][0] & 0x7FFF7FFFu;
+        qa[s][1] = qb[s][1] & 0x7FFF7FFFu;
+    }
+    __syncthreads();
+
+    // ---- tile phase: approximate scores + error bounds -> lo / hi ----
+    unsigned char* stage = stage_base + warp * kTileBytes;
+    uint32_t phase = 0;
+    auto issue = [&](int t) {
+        if (lane == 0 && t < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bars[warp], kTileBytes);
+            bulk_g2s(stage, meta_pair + (size_t)(j0 / 32 + t) * kTileBytes, kTileBytes, &bars[warp]);
+        }
+    };
+    const int mi = lane >> 3, rr = lane & 7;
+    // ldmatrix row address of A (16 blocks x 16 k) for chunk s, m-tile mt:
+    // matrices {min, blocks 0-7}, {min, 8-15}, {max, 0-7}, {max, 8-15}
+    const uint32_t a_off = (uint32_t)((mi >> 1) * 512 + (8 * (mi & 1) + rr) * 16);
+    issue(warp);
+    for (int t = warp; t < ntiles; t += kTcWarps) {
+        mbar_wait(&bars[warp], phase);
+        phase ^= 1u;
+        const uint32_t sb = smem_u32(stage);
+        float ds[2][4], da[2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) ds[mt][e] = da[mt][e] = 0.f;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                uint32_t af[4];
+                ldsm_x4(sb + s * 1024 + mt * 256 + a_off, af);
+                hmma(ds[mt], af, qb[s][0], qb[s][1]);
+                af[0] &= 0x7FFF7FFFu;
+                af[1] &= 0x7FFF7FFFu;
+                af[2] &= 0x7FFF7FFFu;
+                af[3] &= 0x7FFF7FFFu;
+                hmma(da[mt], af, qa[s][0], qa[s][1]);
+            }
+        }
+        __syncwarp();
+        issue(t + kTcWarps);  // the stage is consumed: next tile in flight
+        // lane: rows r, r + 8 of each m-tile, heads 2c, 2c + 1
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                float sv = -INFINITY, av = 0.f;
+                int bad = 0;  // a non-finite approximation makes the block a candidate
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    if (2 * c + e < G) {
+                        const float dv = ds[mt][2 * half + e], dav = da[mt][2 * half + e];
+                        bad |= !(fabsf(dv) <= 3.0e38f) || !(dav <= 3.0e38f);
+                        sv = fmaxf(sv, dv);
+                        av = fmaxf(av, dav);
+                    }
+                }
+                // max over the quad's heads (the 4 lanes share rows r, r + 8)
+                sv = fmaxf(sv, __shfl_xor_sync(0xffffffffu, sv, 1));
+                sv = fmaxf(sv, __shfl_xor_sync(0xffffffffu, sv, 2));
+                av = fmaxf(av, __shfl_xor_sync(0xffffffffu, av, 1));
+                av = fmaxf(av, __shfl_xor_sync(0xffffffffu, av, 2));
+                bad |= __shfl_xor_sync(0xffffffffu, bad, 1);
+                bad |= __shfl_xor_sync(0xffffffffu, bad, 2);
+                const bool anybad = bad != 0;
+                const int jj = t * 32 + 16 * mt + 8 * half + r;
+                if (c == 0 && jj < nb_chunk) {
+                    const float eps = __fmaf_ru(av, 0x1p-10f, 0x1p-100f);
+                    if (anybad || !(eps <= 3.0e38f)) {
+                        lo[jj] = -INFINITY;
+                        hi[jj] = INFINITY;
+                    } else {
+                        lo[jj] = __fsub_rd(sv, eps);
+                        hi[jj] = __fadd_ru(sv, eps);
+                    }
+                }
+            }
+    }
+    __syncthreads();
+
+    // ---- threshold and candidates ----
+    const int kk = min(k, nb_chunk);
+    uint32_t* lkey = (uint32_t*)lo;   // in place: lo[] -> ord32(lo[])
+    for (int i = tid; i < nb_chunk; i += kTcThreads) lkey[i] = ord32(lo[i]);
+    __syncthreads();
+    const uint32_t tau = kk < nb_chunk ? cta_kth_u32(lkey, nb_chunk, kk, hist, sw) : 0u;
+    int32_t* jpos = (int32_t*)(smem_raw + (size_t)max(CH, min(nchunks * k, kSelMaxMerge)) * 8);
+    int n_cand;
+    {
+        const int per = (nb_chunk + kTcThreads - 1) / kTcThreads;
+        const int p0 = tid * per, p1 = min(nb_chunk, p0 + per);
+        int cnt = 0;
+        for (int p = p0; p < p1; ++p) cnt += ord32(hi[p]) >= tau;
+        int tot;
+        int o = block_excl_scan<kTcThreads>(cnt, sw, tot);
+        for (int p = p0; p < p1; ++p)
+            if (ord32(hi[p]) >= tau) jpos[o++] = p;
+        n_cand = tot;
+    }
+    __syncthreads();
+
+    // ---- exact fp64 rescoring of the candidates (the oracle's arithmetic) ----
+    for (int i = tid; i < n_cand; i += kTcThreads) {
+        const int p = jpos[i];
+        const char* tb = meta_pair + (size_t)(j0 / 32 + p / 32) * kTileBytes + (p % 32) * 16;
+        double acc[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[g] = 0.0;
+#pragma unroll 2
+        for (int s = 0; s < 16; ++s) {
+            const uint4 wn4 = ldg_stream(tb + (size_t)((s * 2 + 0) * 32) * 16);
+            const uint4 wx4 = ldg_stream(tb + (size_t)((s * 2 + 1) * 32) * 16);
+            const uint32_t wn[4] = {wn4.x, wn4.y, wn4.z, wn4.w};
+            const uint32_t wx[4] = {wx4.x, wx4.y, wx4.z, wx4.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int w = e >> 1, ch = 8 * s + e;
+                const int32_t hN = (e & 1) ? bf16_hi_hiword(wn[w]) : bf16_lo_hiword(wn[w]);
+                const int32_t hM = (e & 1) ? bf16_hi_hiword(wx[w]) : bf16_lo_hiword(wx[w]);
+                const int32_t dd = hM ^ hN;
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    acc[g] = __fma_rn(qs[ch * G + g], __hiloint2double(hN ^ (qf[ch * G + g] & dd), 0), acc[g]);
+            }
+        }
+        double sc = acc[0];
+#pragma unroll
+        for (int g = 1; g < G; ++g) sc = acc[g] > sc ? acc[g] : sc;
+        keys[i] = ord_key(sc + 0.0);
+    }
+    __syncthreads();
+
+    // ---- exact top-k among the candidates (positions ascending = j ascending) ----
+    int32_t* sel_pair = sel + (size_t)pair * k;
+    if (nch_b == 1) {
+        cta_topk_t<kTcThreads>(keys, n_cand, kk, hist, sw, [&](int o, int pp) { sel_pair[o] = j0 + jpos[pp]; });
+        for (int rr2 = kk + tid; rr2 < k; rr2 += kTcThreads) sel_pair[rr2] = -1;
+        return;
+    }
+    uint64_t* ck = cand_key + ((size_t)pair * nchunks + ci) * k;
+    int32_t* cj = cand_j + ((size_t)pair * nchunks + ci) * k;
+    cta_topk_t<kTcThreads>(keys, n_cand, kk, hist, sw, [&](int o, int pp) {
+        ck[o] = keys[pp];
+        cj[o] = j0 + jpos[pp];
+    });
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sw[48] = atomicAdd(&tickets[pair], 1);
+    __syncthreads();
+    if (sw[48] != nch_b - 1) return;
+    __threadfence();
+    int n = 0;
+    for (int cc = 0; cc < nch_b; ++cc) {
+        const int sz = min(CH, nb - cc * CH);
+        const int kcc = min(k, sz);
+        const uint64_t* sk = cand_key + ((size_t)pair * nchunks + cc) * k;
+        const int32_t* sj = cand_j + ((size_t)pair * nchunks + cc) * k;
+        for (int i = tid; i < kcc; i += kTcThreads) {
+            keys[n + i] = __ldcg(sk + i);
+            jpos[n + i] = __ldcg(sj + i);
+        }
+        n += kcc;
+    }
+    __syncthreads();
+    const int kf = min(k, nb);
+    cta_topk_t<kTcThreads>(keys, n, kf, hist, sw, [&](int o, int pp) { sel_pair[o] = jpos[pp]; });
+    for (int rr2 = kf + tid; rr2 < k; rr2 += kTcThreads) sel_pair[rr2] = -1;
+    if (tid == 0) tickets[pair] = 0;
+}
+
 // Blocks scored per CTA (the chunk): 1024 for MHA (G = 1), 2048 for GQA
 // (G > 1: 4-8x the fp64 work per block, so longer CTAs amortise the q setup and
 // the top-k).  Measured (tools/kbench.py, C2 / C3 full batch and one request
@@ -642,6 +956,30 @@ static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_
     return SS_OK;
 }
 
+template <int G>
+static ss_status launch_sel_tc(const void* q, const void* meta, const int32_t* n_blk, int max_blk, int k,
+                               const ss_dims& d, int32_t* sel, void* ws, cudaStream_t stream) {
+    const size_t pairs = (size_t)d.batch * d.num_kv_heads;
+    const int CH = sel_chunk(G, max_blk, k, (int)pairs);
+    const int nchunks = (max_blk + CH - 1) / CH;
+    const size_t nc = pairs * nchunks * k;
+    int32_t* tickets = (int32_t*)ws;
+    uint64_t* cand_key = (uint64_t*)((char*)ws + ((pairs * 4 + 255) & ~(size_t)255));
+    int32_t* cand_j = (int32_t*)((char*)cand_key + nc * 8);
+    const int cap = std::max(CH, std::min(nchunks * k, kSelMaxMerge));
+    const int region = std::max(kTcWarps * kTileBytes, ((cap * 12) + 127) / 128 * 128);
+    const size_t smem = (size_t)region + (size_t)CH * 8 + (size_t)kHeadDim * G * 12 + 256 * 4 + 64 * 4 + 64;
+    auto kern = block_select_tc_kernel<G>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return SS_ERR_CUDA;
+    set_carveout(kern);
+    kern<<<nchunks * (int)pairs, kTcThreads, smem, stream>>>(q, meta, n_blk, max_blk, k, d.num_q_heads,
+                                                              d.num_kv_heads, nchunks, CH, region, sel,
+                                                              cand_key, cand_j, tickets);
+    SS_LAUNCH_CHECK();
+    return SS_OK;
+}
+
 ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_blk, int max_blk,
                               int k, const ss_dims& d, ss_dtype dt, int32_t* sel, double* scores,
                               void* ws, cudaStream_t stream, bool mean) {
@@ -663,8 +1001,13 @@ ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_
 #define SS_SEL_NOICV(BF, GG) (void)0;
 #endif
 #define SS_SEL_ARGS q, meta, n_blk, max_blk, k, d, sel, scores, ws, stream
+    // GQA bf16 selections without a scores output: tensor-core scoring + exact
+    // fp64 rescoring of the candidates (block_select_tc_kernel; SS_SEL_TC=0: the
+    // all-fp64 kernel, which also serves calls that ask for every score)
+    const bool tc = knob("SS_SEL_TC", 1) != 0 && !mean && dt == SS_BF16 && G > 1 && scores == nullptr;
 #define SS_SEL_CASE(GG)                                                                       \
     case GG:                                                                                  \
+        if (GG > 1 && tc) return launch_sel_tc<(GG > 1 ? GG : 2)>(q, meta, n_blk, max_blk, k, d, sel, ws, stream); \
         if (mean)                                                                             \
             return dt == SS_BF16 ? launch_sel_t<true, GG, true, true>(SS_SEL_ARGS)            \
                                  : launch_sel_t<false, GG, true, true>(SS_SEL_ARGS);          \
@@ -701,6 +1044,9 @@ bool preload_select() {
     ok &= preload_fn(block_select_kernel<false, GG, true, false, 1>);
     SS_PL(1) SS_PL(2) SS_PL(4) SS_PL(8)
 #undef SS_PL
+    ok &= preload_fn(block_select_tc_kernel<2>);
+    ok &= preload_fn(block_select_tc_kernel<4>);
+    ok &= preload_fn(block_select_tc_kernel<8>);
     return ok;
 }
 

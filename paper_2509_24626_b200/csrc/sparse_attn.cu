@@ -44,37 +44,6 @@ constexpr int kAttnPartStride = 132;
 // floats per (warp, seg, g) partial: m, l, pad, pad, o[128]
 constexpr int kMinUnitsPerWarp = 8;  // measured: C3 26.6 us at 8 vs 30.7 at 4 / 16, C2 unchanged
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(phase)
-            : "memory");
-    }
-}
-
 struct AttnArgs {
     const void* q;
     const void* pool;
@@ -234,7 +203,7 @@ __device__ void merge_partials(const AttnArgs& a, int64_t p, int w) {
                 }
             }
             const int n = min(32, nc - i0);
-            constexpr int UNR = GC >= 4 ? 8 : 16;  // loads in flight vs registers (the stage registers are dead here)
+            constexpr int UNR = 8;  // loads in flight vs registers (GC = 4: 8 measured better than 4 at C3)
 #pragma unroll UNR
             for (int j = 0; j < n; ++j) {
                 const int64_t bj = __shfl_sync(0xffffffffu, base_i, j);
@@ -366,7 +335,6 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
     int stage = 0;
 
     const int64_t p_first = u0 / Ku, p_last = (u1 - 1) / Ku;
-    int64_t defer0 = -1, defer1 = -1;  // pairs this warp merges after its range
     float4 qn[G];  // q of the next pair, prefetched in registers
     load_q<BF16, G>(a, (int)(p_first / a.Hkv), (int)(p_first % a.Hkv), lane, qn);
     for (int64_t p = p_first; p <= p_last; ++p) {
@@ -543,10 +511,8 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
             *reinterpret_cast<float4*>(pp + 4 + 4 * lane) =
                 make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
         }
-        if (partial_is_last(a, p)) (defer0 < 0 ? defer0 : defer1) = p;  // merged after the range
+        if (partial_is_last(a, p)) merge_partials<G>(a, p, w);
     }
-    if (defer0 >= 0) merge_partials<G>(a, defer0, w);
-    if (defer1 >= 0) merge_partials<G>(a, defer1, w);
 }
 
 // ============================================================================
@@ -617,30 +583,11 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* tm, int 
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(addr)
-                 : "memory");
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(addr)
-                 : "memory");
-}
 // 8x8 b16 transpose across the warp (fragment layout in and out)
 __device__ __forceinline__ uint32_t movm_t(uint32_t x) {
     uint32_t y;
     asm("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
     return y;
-}
-// D[16x8] += A[16x16] B[16x8], bf16 in, f32 accumulate
-__device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-        "{%8,%9}, {%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 __device__ __forceinline__ uint32_t bf16x2_bits(__nv_bfloat162 v) {
     return *reinterpret_cast<uint32_t*>(&v);
@@ -767,7 +714,6 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
     const uint32_t v_hi = (uint32_t)(mi & 1);
 
     const int64_t p_first = u0 / Ku, p_last = (u1 - 1) / Ku;
-    int64_t defer0 = -1, defer1 = -1;  // pairs this warp merges after its range
     for (int64_t p = p_first; p <= p_last; ++p) {
         const int b = (int)(p / a.Hkv), h = (int)(p % a.Hkv);
         // Q^T fragment (B operand): k-step s holds head r's dims 16s+2c, +1 (b0)
@@ -944,13 +890,10 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
                 }
             }
         }
-        // the last contributor merges -- after its own range is streamed: a
-        // merge in the middle of a range would delay that warp's remaining
-        // units (the kernel's tail); a range cuts at most two pairs
-        if (partial_is_last(a, p)) (defer0 < 0 ? defer0 : defer1) = p;
+        // the last contributor merges at once (measured: deferring the merge to
+        // the end of the warp's range did not shorten the kernel, r02l)
+        if (partial_is_last(a, p)) merge_partials<G>(a, p, w);
     }
-    if (defer0 >= 0) merge_partials<G>(a, defer0, w);
-    if (defer1 >= 0) merge_partials<G>(a, defer1, w);
     trace(2);
 }
 

@@ -125,6 +125,66 @@ def test_select_large_k_many_chunks_merge_bound(ops, G):
     _select_case(ops, synth.DT_BF16, 1, G, 1, [32768], 300, seed=40 + G)
 
 
+@pytest.mark.parametrize("G,k", [(2, 1), (4, 64), (8, 300), (4, 128)])
+def test_select_gqa_ties_tensor_core_path(ops, G, k):
+    """GQA bf16 without a scores output runs the tensor-core filter + exact
+    rescoring (block_select_tc_kernel): duplicated blocks give exact score ties
+    that straddle the k-th place; the selection must equal the oracle's."""
+    _select_case(ops, synth.DT_BF16, 2, 2 * G, 2, [3000, 700], k, seed=60 + G + k, ties=True)
+
+
+def _select_sel_only(ops, q_f, blocks_f, B, Hq, Hkv, n_blk, k):
+    """bf16 selection only (the tensor-core path for GQA) vs the oracle."""
+    max_blk = ((max(n_blk) + 31) // 32) * 32
+    store = synth.encode(blocks_f, synth.DT_BF16)
+    qs = synth.encode(q_f, synth.DT_BF16)
+    meta_log = oracle.block_meta(store, key_stride=2 * 32 * D).reshape(B, Hkv, max_blk, 2, D)
+    nbk = np.array(n_blk, np.int32)
+    exp_sel = oracle.topk(oracle.block_score(qs, meta_log, nbk), nbk, k)
+    d = ops.dims(B, Hq, Hkv)
+    ws = ops.alloc_workspace(0, d, max_blk, k)
+    sel = torch.empty(B, Hkv, k, dtype=torch.int32, device="cuda")
+    ops.ss_block_select(to_torch(qs), to_torch(logical_to_tiled(meta_log)), torch.from_numpy(nbk).cuda(),
+                        max_blk, k, d, sel, ws)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(sel.cpu().numpy(), exp_sel)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_select_gqa_near_ties_below_f32_resolution(ops, G):
+    """Blocks whose exact scores differ by far less than the f32 approximation
+    can resolve (one key nudged by one bf16 ulp in a copy of another block):
+    the exact fp64 rescoring of the candidates must order them as the oracle."""
+    rng = synth.rng_for(1000, 7, G)
+    B, Hkv, n = 2, 2, 1500
+    max_blk = ((n + 31) // 32) * 32
+    blocks = synth.kv_blocks(rng, B * Hkv * max_blk, D, synth.channel_scales(rng))
+    blocks = synth.bf16_bits_to_f32(synth.f32_to_bf16_bits(blocks)).reshape(blocks.shape)
+    src = rng.integers(0, B * Hkv * max_blk, size=400)
+    for i, j in enumerate(rng.integers(0, B * Hkv * max_blk, size=400)):
+        blocks[j] = blocks[src[i]]
+        if i % 2:   # nudge one key element of the copy by one bf16 ulp (exact in bf16)
+            t, c = int(rng.integers(0, 32)), int(rng.integers(0, D))
+            bits = synth.f32_to_bf16_bits(blocks[j, 0, t, c:c + 1])
+            blocks[j, 0, t, c] = synth.bf16_bits_to_f32(bits + np.uint16(1))[0]
+    q = rng.standard_normal((B, Hkv * G, D)).astype(np.float32)
+    for k in (16, 64):
+        _select_sel_only(ops, q, blocks, B, Hkv * G, Hkv, [n, n - 333], k)
+
+
+@pytest.mark.parametrize("scale_q,scale_k", [(1e10, 1e30), (1e-20, 1e-25), (1.0, 1e-38)])
+def test_select_gqa_extreme_magnitudes(ops, scale_q, scale_k):
+    """f32 overflow (inf / NaN approximations make every such block a candidate)
+    and underflow (covered by the absolute error term) in the tensor-core
+    filter: selections still equal the oracle's fp64 ones."""
+    rng = synth.rng_for(1000, 8, int(np.log10(scale_k) + 50))
+    B, G, Hkv, n = 1, 4, 2, 900
+    max_blk = ((n + 31) // 32) * 32
+    blocks = synth.kv_blocks(rng, B * Hkv * max_blk, D) * np.float32(scale_k)
+    q = (rng.standard_normal((B, Hkv * G, D)) * scale_q).astype(np.float32)
+    _select_sel_only(ops, q, blocks, B, Hkv * G, Hkv, [n], 32)
+
+
 def test_select_needles_selected(ops):
     sel = _select_case(ops, synth.DT_BF16, 2, 8, 8, [700, 64], 4, seed=30, needle=True)
     assert (sel[:, :, 0] >= 0).all()
