@@ -581,6 +581,8 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
 constexpr int kTcWarps = 4;
 constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTileBytes = 64 * kHeadDim * 2;  // 32 blocks x [min|max] x 128 ch, bf16
+constexpr int kSelTcStages = 1;  // tile stages per warp (SS_SEL_TC_STAGES, debug A/B)
+constexpr int kSelTcRot = 0;     // start-tile rotation multiplier per CTA (SS_SEL_ROT, debug A/B)
 
 __device__ __forceinline__ uint32_t ord32(float f) {
     const uint32_t b = __float_as_uint(f);
@@ -631,11 +633,11 @@ __device__ uint32_t cta_kth_u32(const uint32_t* keys, int n, int kk, int* hist, 
     return prefix;
 }
 
-template <int G>
-__global__ void __launch_bounds__(kTcThreads, 2)
+template <int G, int NS>
+__global__ void __launch_bounds__(kTcThreads, NS == 1 ? 2 : 1)
 block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                        const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
-                       int nchunks, int CH, int region_bytes, int32_t* __restrict__ sel,
+                       int nchunks, int CH, int region_bytes, int rot_mul, int32_t* __restrict__ sel,
                        uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_j,
                        int32_t* __restrict__ tickets) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -670,7 +672,8 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
         qf[i] = qd >= 0.0 ? -1 : 0;
     }
     if (lane == 0) {
-        mbar_init(&bars[warp], 1);
+#pragma unroll
+        for (int st = 0; st < NS; ++st) mbar_init(&bars[warp * NS + st], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // B fragment of chunk s (k rows 0-7: the min channels 8s..8s+7 -> q-, rows
@@ -691,23 +694,33 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
     __syncthreads();
 
     // ---- tile phase: approximate scores + error bounds -> lo / hi ----
-    unsigned char* stage = stage_base + warp * kTileBytes;
-    uint32_t phase = 0;
-    auto issue = [&](int t) {
-        if (lane == 0 && t < ntiles) {
+    // NS stages per warp; the warp's i-th tile is logical tile warp + i * kTcWarps,
+    // read from physical tile (logical + rot) % ntiles: CTAs start at different
+    // offsets of their chunks instead of all streaming the same address phase
+    const int rot = ntiles > 0 ? (int)(((int64_t)blockIdx.x * rot_mul) % ntiles) : 0;
+    const int my_tiles = ntiles > warp ? (ntiles - warp + kTcWarps - 1) / kTcWarps : 0;
+    auto phys = [&](int i) { int t = warp + i * kTcWarps + rot; return t >= ntiles ? t - ntiles : t; };
+    auto issue = [&](int i) {
+        if (lane == 0 && i < my_tiles) {
+            const int st = i % NS;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(&bars[warp], kTileBytes);
-            bulk_g2s(stage, meta_pair + (size_t)(j0 / 32 + t) * kTileBytes, kTileBytes, &bars[warp]);
+            mbar_expect_tx(&bars[warp * NS + st], kTileBytes);
+            bulk_g2s(stage_base + (size_t)(warp * NS + st) * kTileBytes,
+                     meta_pair + (size_t)(j0 / 32 + phys(i)) * kTileBytes, kTileBytes, &bars[warp * NS + st]);
         }
     };
+    uint32_t phases = 0;
     const int mi = lane >> 3, rr = lane & 7;
     // ldmatrix row address of A (16 blocks x 16 k) for chunk s, m-tile mt:
     // matrices {min, blocks 0-7}, {min, 8-15}, {max, 0-7}, {max, 8-15}
     const uint32_t a_off = (uint32_t)((mi >> 1) * 512 + (8 * (mi & 1) + rr) * 16);
-    issue(warp);
-    for (int t = warp; t < ntiles; t += kTcWarps) {
-        mbar_wait(&bars[warp], phase);
-        phase ^= 1u;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) issue(i);
+    for (int i = 0; i < my_tiles; ++i) {
+        const int st = i % NS, t = phys(i);
+        mbar_wait(&bars[warp * NS + st], (phases >> st) & 1u);
+        phases ^= 1u << st;
+        unsigned char* stage = stage_base + (size_t)(warp * NS + st) * kTileBytes;
         const uint32_t sb = smem_u32(stage);
         float ds[2][4], da[2][4];
 #pragma unroll
@@ -729,7 +742,7 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
             }
         }
         __syncwarp();
-        issue(t + kTcWarps);  // the stage is consumed: next tile in flight
+        issue(i + NS);  // the stage is consumed: the warp's tile i + NS into it
         // lane: rows r, r + 8 of each m-tile, heads 2c, 2c + 1
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
@@ -967,14 +980,16 @@ static ss_status launch_sel_tc(const void* q, const void* meta, const int32_t* n
     uint64_t* cand_key = (uint64_t*)((char*)ws + ((pairs * 4 + 255) & ~(size_t)255));
     int32_t* cand_j = (int32_t*)((char*)cand_key + nc * 8);
     const int cap = std::max(CH, std::min(nchunks * k, kSelMaxMerge));
-    const int region = std::max(kTcWarps * kTileBytes, ((cap * 12) + 127) / 128 * 128);
+    const int ns = knob("SS_SEL_TC_STAGES", kSelTcStages) >= 2 ? 2 : 1;
+    const int region = std::max(kTcWarps * ns * kTileBytes, ((cap * 12) + 127) / 128 * 128);
     const size_t smem = (size_t)region + (size_t)CH * 8 + (size_t)kHeadDim * G * 12 + 256 * 4 + 64 * 4 + 64;
-    auto kern = block_select_tc_kernel<G>;
+    const int rot_mul = knob("SS_SEL_ROT", kSelTcRot);
+    auto kern = ns == 2 ? block_select_tc_kernel<G, 2> : block_select_tc_kernel<G, 1>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return SS_ERR_CUDA;
     set_carveout(kern);
     kern<<<nchunks * (int)pairs, kTcThreads, smem, stream>>>(q, meta, n_blk, max_blk, k, d.num_q_heads,
-                                                              d.num_kv_heads, nchunks, CH, region, sel,
+                                                              d.num_kv_heads, nchunks, CH, region, rot_mul, sel,
                                                               cand_key, cand_j, tickets);
     SS_LAUNCH_CHECK();
     return SS_OK;
@@ -1044,9 +1059,9 @@ bool preload_select() {
     ok &= preload_fn(block_select_kernel<false, GG, true, false, 1>);
     SS_PL(1) SS_PL(2) SS_PL(4) SS_PL(8)
 #undef SS_PL
-    ok &= preload_fn(block_select_tc_kernel<2>);
-    ok &= preload_fn(block_select_tc_kernel<4>);
-    ok &= preload_fn(block_select_tc_kernel<8>);
+    ok &= preload_fn(block_select_tc_kernel<2, 1>) && preload_fn(block_select_tc_kernel<2, 2>);
+    ok &= preload_fn(block_select_tc_kernel<4, 1>) && preload_fn(block_select_tc_kernel<4, 2>);
+    ok &= preload_fn(block_select_tc_kernel<8, 1>) && preload_fn(block_select_tc_kernel<8, 2>);
     return ok;
 }
 
