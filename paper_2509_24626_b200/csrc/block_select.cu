@@ -90,7 +90,7 @@ __device__ __forceinline__ double f32_scaled(uint32_t x) {
 // Writes the selected positions, ascending, to out_pos (smem or global via
 // functor).  k_sel = min(k, n) positions are produced.
 // ---------------------------------------------------------------------------
-template <int NT, typename Emit>
+template <int NT, bool AGG = true, typename Emit>
 __device__ void cta_topk_t(const uint64_t* keys, int n, int k_sel, int* hist, int* sw, Emit emit) {
     const int tid = threadIdx.x;
     uint64_t prefix = 0, mask = 0;
@@ -99,9 +99,25 @@ __device__ void cta_topk_t(const uint64_t* keys, int n, int k_sel, int* hist, in
         for (int shift = 56; shift >= 0; shift -= 8) {
             for (int i = tid; i < 256; i += NT) hist[i] = 0;
             __syncthreads();
-            for (int i = tid; i < n; i += NT) {
-                uint64_t key = keys[i];
-                if ((key & mask) == prefix) atomicAdd(&hist[(int)((key >> shift) & 0xFF)], 1);
+            // warp-aggregated: the keys of a chunk share their leading digits
+            // (sign / exponent), so plain per-key shared atomics serialise on
+            // one or two bins; one atomic per distinct digit per warp instead
+            if constexpr (AGG) {
+                for (int i0 = tid - lane_id(); i0 < n; i0 += NT) {
+                    const int i = i0 + lane_id();
+                    int digit = 256;  // sentinel: no vote
+                    if (i < n) {
+                        const uint64_t key = keys[i];
+                        if ((key & mask) == prefix) digit = (int)((key >> shift) & 0xFF);
+                    }
+                    const unsigned grp = __match_any_sync(0xffffffffu, digit);
+                    if (digit < 256 && lane_id() == __ffs(grp) - 1) atomicAdd(&hist[digit], __popc(grp));
+                }
+            } else {  // (register-tight callers: the GQA fp64 kernel)
+                for (int i = tid; i < n; i += NT) {
+                    const uint64_t key = keys[i];
+                    if ((key & mask) == prefix) atomicAdd(&hist[(int)((key >> shift) & 0xFF)], 1);
+                }
             }
             __syncthreads();
             if (tid < 32) {
@@ -171,13 +187,17 @@ __device__ void cta_topk_t(const uint64_t* keys, int n, int k_sel, int* hist, in
 }
 
 // ---------------------------------------------------------------------------
-template <typename Emit>
+template <bool AGG, typename Emit>
 __device__ __forceinline__ void cta_topk(const uint64_t* keys, int n, int k_sel, int* hist, int* sw, Emit emit) {
-    cta_topk_t<kSelThreads>(keys, n, k_sel, hist, sw, emit);
+    cta_topk_t<kSelThreads, AGG>(keys, n, k_sel, hist, sw, emit);
 }
 
+// G > 1 (min/max): the all-fp64 GQA kernel now serves calls that ask for every
+// score (debug / tests) and f32 inputs; bf16 selections run on the tensor
+// cores (block_select_tc_kernel).  One CTA per SM gives it the registers to
+// keep its load ring and G x TT accumulators without spilling.
 template <bool BF16, int G, bool ICV, bool MEAN, int TT>
-__global__ void __launch_bounds__(kSelThreads, (G > 1 && !MEAN && TT == 1) ? 3 : 2)
+__global__ void __launch_bounds__(kSelThreads, (G > 1 && !MEAN) ? 1 : 2)
 block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                     const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
                     int nchunks, int CH, int npairs, int l2pf, int32_t* __restrict__ sel, double* __restrict__ scores,
@@ -513,14 +533,14 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     const int kc = min(k, nb_chunk);
     int32_t* sel_pair = sel + (size_t)pair * k;
     if (nch_b == 1) {
-        cta_topk(keys, nb_chunk, kc, hist, sw, [&](int o, int p) { sel_pair[o] = j0 + p; });
+        cta_topk<G == 1>(keys, nb_chunk, kc, hist, sw, [&](int o, int p) { sel_pair[o] = j0 + p; });
         for (int r = kc + tid; r < k; r += kSelThreads) sel_pair[r] = -1;
         continue;
     }
     // Multi-chunk: emit candidates, then the last CTA of the pair merges.
     uint64_t* ck = cand_key + ((size_t)pair * nchunks + ci) * k;
     int32_t* cj = cand_j + ((size_t)pair * nchunks + ci) * k;
-    cta_topk(keys, nb_chunk, kc, hist, sw, [&](int o, int p) {
+    cta_topk<G == 1>(keys, nb_chunk, kc, hist, sw, [&](int o, int p) {
         ck[o] = keys[p];
         cj[o] = j0 + p;
     });
@@ -546,7 +566,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     }
     __syncthreads();
     const int kf = min(k, nb);
-    cta_topk(keys, n, kf, hist, sw, [&](int o, int p) { sel_pair[o] = jpos[p]; });
+    cta_topk<G == 1>(keys, n, kf, hist, sw, [&](int o, int p) { sel_pair[o] = jpos[p]; });
     for (int r = kf + tid; r < k; r += kSelThreads) sel_pair[r] = -1;
     if (tid == 0) tickets[pair] = 0;
     }  // work items
@@ -598,9 +618,15 @@ __device__ uint32_t cta_kth_u32(const uint32_t* keys, int n, int kk, int* hist, 
     for (int shift = 24; shift >= 0; shift -= 8) {
         for (int i = tid; i < 256; i += kTcThreads) hist[i] = 0;
         __syncthreads();
-        for (int i = tid; i < n; i += kTcThreads) {
-            const uint32_t key = keys[i];
-            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xFF], 1);
+        for (int i0 = tid - lane_id(); i0 < n; i0 += kTcThreads) {  // warp-aggregated (see cta_topk_t)
+            const int i = i0 + lane_id();
+            int digit = 256;
+            if (i < n) {
+                const uint32_t key = keys[i];
+                if ((key & mask) == prefix) digit = (int)((key >> shift) & 0xFF);
+            }
+            const unsigned grp = __match_any_sync(0xffffffffu, digit);
+            if (digit < 256 && lane_id() == __ffs(grp) - 1) atomicAdd(&hist[digit], __popc(grp));
         }
         __syncthreads();
         if (tid < 32) {
