@@ -99,21 +99,7 @@ __device__ void cta_topk_t(const uint64_t* keys, int n, int k_sel, int* hist, in
         for (int shift = 56; shift >= 0; shift -= 8) {
             for (int i = tid; i < 256; i += NT) hist[i] = 0;
             __syncthreads();
-            // warp-aggregated: the keys of a chunk share their leading digits
-            // (sign / exponent), so plain per-key shared atomics serialise on
-            // one or two bins; one atomic per distinct digit per warp instead
-            if constexpr (AGG) {
-                for (int i0 = tid - lane_id(); i0 < n; i0 += NT) {
-                    const int i = i0 + lane_id();
-                    int digit = 256;  // sentinel: no vote
-                    if (i < n) {
-                        const uint64_t key = keys[i];
-                        if ((key & mask) == prefix) digit = (int)((key >> shift) & 0xFF);
-                    }
-                    const unsigned grp = __match_any_sync(0xffffffffu, digit);
-                    if (digit < 256 && lane_id() == __ffs(grp) - 1) atomicAdd(&hist[digit], __popc(grp));
-                }
-            } else {  // (register-tight callers: the GQA fp64 kernel)
+            {  // (measured: warp-aggregated match_any voting was slower, r02o)
                 for (int i = tid; i < n; i += NT) {
                     const uint64_t key = keys[i];
                     if ((key & mask) == prefix) atomicAdd(&hist[(int)((key >> shift) & 0xFF)], 1);
@@ -618,15 +604,9 @@ __device__ uint32_t cta_kth_u32(const uint32_t* keys, int n, int kk, int* hist, 
     for (int shift = 24; shift >= 0; shift -= 8) {
         for (int i = tid; i < 256; i += kTcThreads) hist[i] = 0;
         __syncthreads();
-        for (int i0 = tid - lane_id(); i0 < n; i0 += kTcThreads) {  // warp-aggregated (see cta_topk_t)
-            const int i = i0 + lane_id();
-            int digit = 256;
-            if (i < n) {
-                const uint32_t key = keys[i];
-                if ((key & mask) == prefix) digit = (int)((key >> shift) & 0xFF);
-            }
-            const unsigned grp = __match_any_sync(0xffffffffu, digit);
-            if (digit < 256 && lane_id() == __ffs(grp) - 1) atomicAdd(&hist[digit], __popc(grp));
+        for (int i = tid; i < n; i += kTcThreads) {
+            const uint32_t key = keys[i];
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xFF], 1);
         }
         __syncthreads();
         if (tid < 32) {
@@ -830,35 +810,56 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
     __syncthreads();
 
     // ---- exact fp64 rescoring of the candidates (the oracle's arithmetic) ----
-    for (int i = tid; i < n_cand; i += kTcThreads) {
-        const int p = jpos[i];
-        const char* tb = meta_pair + (size_t)(j0 / 32 + p / 32) * kTileBytes + (p % 32) * 16;
-        double acc[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) acc[g] = 0.0;
-#pragma unroll 2
-        for (int s = 0; s < 16; ++s) {
-            const uint4 wn4 = ldg_stream(tb + (size_t)((s * 2 + 0) * 32) * 16);
-            const uint4 wx4 = ldg_stream(tb + (size_t)((s * 2 + 1) * 32) * 16);
-            const uint32_t wn[4] = {wn4.x, wn4.y, wn4.z, wn4.w};
-            const uint32_t wx[4] = {wx4.x, wx4.y, wx4.z, wx4.w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int w = e >> 1, ch = 8 * s + e;
-                const int32_t hN = (e & 1) ? bf16_hi_hiword(wn[w]) : bf16_lo_hiword(wn[w]);
-                const int32_t hM = (e & 1) ? bf16_hi_hiword(wx[w]) : bf16_lo_hiword(wx[w]);
-                const int32_t dd = hM ^ hN;
-#pragma unroll
-                for (int g = 0; g < G; ++g)
-                    acc[g] = __fma_rn(qs[ch * G + g], __hiloint2double(hN ^ (qf[ch * G + g] & dd), 0), acc[g]);
+    // A candidate's 512 B of metadata are 32 scattered 16-byte pieces of its
+    // tile; a batch of candidates is first staged into shared memory by the
+    // whole CTA with cp.async (all pieces in flight at once), then each thread
+    // rescores one candidate from shared memory.  (Loading them per thread
+    // serialised ~8 global round trips per candidate.)
+    {
+        const int cap_keys = max(CH, min(nchunks * k, kSelMaxMerge));
+        unsigned char* cstage = smem_raw + (((size_t)cap_keys * 12 + 127) & ~(size_t)127);
+        const int batch = min(kTcThreads, (region_bytes - (int)(cstage - smem_raw)) / 512);
+        for (int base = 0; base < n_cand; base += batch) {
+            const int nbt = min(batch, n_cand - base);
+            for (int i = tid; i < nbt * 32; i += kTcThreads) {
+                const int ci2 = i >> 5, pc = i & 31;       // candidate, piece (chunk s = pc / 2, min|max = pc % 2)
+                const int p = jpos[base + ci2];
+                const char* src = meta_pair + (size_t)(j0 / 32 + p / 32) * kTileBytes + (size_t)pc * 512 + (p % 32) * 16;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(cstage + ci2 * 512 + pc * 16)),
+                             "l"(src)
+                             : "memory");
             }
-        }
-        double sc = acc[0];
+            asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+            __syncthreads();
+            if (tid < nbt) {
+                const uint4* cp = reinterpret_cast<const uint4*>(cstage + tid * 512);
+                double acc[G];
 #pragma unroll
-        for (int g = 1; g < G; ++g) sc = acc[g] > sc ? acc[g] : sc;
-        keys[i] = ord_key(sc + 0.0);
+                for (int g = 0; g < G; ++g) acc[g] = 0.0;
+#pragma unroll 4
+                for (int s = 0; s < 16; ++s) {
+                    const uint4 wn4 = cp[2 * s], wx4 = cp[2 * s + 1];
+                    const uint32_t wn[4] = {wn4.x, wn4.y, wn4.z, wn4.w};
+                    const uint32_t wx[4] = {wx4.x, wx4.y, wx4.z, wx4.w};
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int w = e >> 1, ch = 8 * s + e;
+                        const int32_t hN = (e & 1) ? bf16_hi_hiword(wn[w]) : bf16_lo_hiword(wn[w]);
+                        const int32_t hM = (e & 1) ? bf16_hi_hiword(wx[w]) : bf16_lo_hiword(wx[w]);
+                        const int32_t dd = hM ^ hN;
+#pragma unroll
+                        for (int g = 0; g < G; ++g)
+                            acc[g] = __fma_rn(qs[ch * G + g], __hiloint2double(hN ^ (qf[ch * G + g] & dd), 0), acc[g]);
+                    }
+                }
+                double sc = acc[0];
+#pragma unroll
+                for (int g = 1; g < G; ++g) sc = acc[g] > sc ? acc[g] : sc;
+                keys[base + tid] = ord_key(sc + 0.0);
+            }
+            __syncthreads();
+        }
     }
-    __syncthreads();
 
     // ---- exact top-k among the candidates (positions ascending = j ascending) ----
     int32_t* sel_pair = sel + (size_t)pair * k;
@@ -1007,7 +1008,8 @@ static ss_status launch_sel_tc(const void* q, const void* meta, const int32_t* n
     int32_t* cand_j = (int32_t*)((char*)cand_key + nc * 8);
     const int cap = std::max(CH, std::min(nchunks * k, kSelMaxMerge));
     const int ns = knob("SS_SEL_TC_STAGES", kSelTcStages) >= 2 ? 2 : 1;
-    const int region = std::max(kTcWarps * ns * kTileBytes, ((cap * 12) + 127) / 128 * 128);
+    // region: the tile stages, later keys + positions + a candidate stage (>= 32 x 512 B)
+    const int region = std::max(kTcWarps * ns * kTileBytes, ((cap * 12) + 127) / 128 * 128 + 32 * 512);
     const size_t smem = (size_t)region + (size_t)CH * 8 + (size_t)kHeadDim * G * 12 + 256 * 4 + 64 * 4 + 64;
     const int rot_mul = knob("SS_SEL_ROT", kSelTcRot);
     auto kern = ns == 2 ? block_select_tc_kernel<G, 2> : block_select_tc_kernel<G, 1>;
