@@ -589,6 +589,7 @@ constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTileBytes = 64 * kHeadDim * 2;  // 32 blocks x [min|max] x 128 ch, bf16
 constexpr int kSelTcStages = 1;  // tile stages per warp (SS_SEL_TC_STAGES, debug A/B)
 constexpr int kSelTcRot = 0;     // start-tile rotation multiplier per CTA (SS_SEL_ROT, debug A/B)
+constexpr int kSelTcPf = 0;      // L2 prefetch distance in tiles (SS_SEL_TC_PF, debug A/B)
 
 __device__ __forceinline__ uint32_t ord32(float f) {
     const uint32_t b = __float_as_uint(f);
@@ -643,7 +644,8 @@ template <int G, int NS>
 __global__ void __launch_bounds__(kTcThreads, NS == 1 ? 2 : 1)
 block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                        const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
-                       int nchunks, int CH, int region_bytes, int rot_mul, int32_t* __restrict__ sel,
+                       int nchunks, int CH, int region_bytes, int rot_mul, int pf_dist,
+                       int32_t* __restrict__ sel,
                        uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_j,
                        int32_t* __restrict__ tickets) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -722,8 +724,15 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
     const uint32_t a_off = (uint32_t)((mi >> 1) * 512 + (8 * (mi & 1) + rr) * 16);
 #pragma unroll
     for (int i = 0; i < NS; ++i) issue(i);
+    // L2 prefetch of the warp's tiles pf_dist ahead (no shared memory: more
+    // bytes in flight from DRAM than the stages alone hold)
+    if (lane == 0)
+        for (int i = NS; i < NS + pf_dist && i < my_tiles; ++i)
+            prefetch_l2_bulk(meta_pair + (size_t)(j0 / 32 + phys(i)) * kTileBytes, kTileBytes);
     for (int i = 0; i < my_tiles; ++i) {
         const int st = i % NS, t = phys(i);
+        if (lane == 0 && pf_dist > 0 && i + NS + pf_dist < my_tiles)
+            prefetch_l2_bulk(meta_pair + (size_t)(j0 / 32 + phys(i + NS + pf_dist)) * kTileBytes, kTileBytes);
         mbar_wait(&bars[warp * NS + st], (phases >> st) & 1u);
         phases ^= 1u << st;
         unsigned char* stage = stage_base + (size_t)(warp * NS + st) * kTileBytes;
@@ -1020,7 +1029,8 @@ static ss_status launch_sel_tc(const void* q, const void* meta, const int32_t* n
         return SS_ERR_CUDA;
     set_carveout(kern);
     kern<<<nchunks * (int)pairs, kTcThreads, smem, stream>>>(q, meta, n_blk, max_blk, k, d.num_q_heads,
-                                                              d.num_kv_heads, nchunks, CH, region, rot_mul, sel,
+                                                              d.num_kv_heads, nchunks, CH, region, rot_mul,
+                                                              knob("SS_SEL_TC_PF", kSelTcPf), sel,
                                                               cand_key, cand_j, tickets);
     SS_LAUNCH_CHECK();
     return SS_OK;
