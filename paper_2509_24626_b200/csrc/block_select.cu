@@ -1009,9 +1009,14 @@ template <int G>
 static ss_status launch_sel_tc(const void* q, const void* meta, const int32_t* n_blk, int max_blk, int k,
                                const ss_dims& d, int32_t* sel, void* ws, cudaStream_t stream) {
     const size_t pairs = (size_t)d.batch * d.num_kv_heads;
-    // 4096-block chunks (fewer per-CTA threshold / rescoring / top-k epilogues;
-    // measured at C3: 138 us vs 155 at 2048, 247 at 1024), the debug knob aside
-    int CH = sel_chunk_env() ? sel_chunk_env() : kSelChunkMax;
+    // the largest chunk (<= 4096 blocks: fewer per-CTA threshold / rescoring /
+    // top-k epilogues; C3 full batch: 138 us at 4096 vs 155 at 2048) that still
+    // gives ~a wave of resident CTAs (2 per SM): one C3 request (8 pairs) gets
+    // 1024-block chunks instead of 64 CTAs on 148 SMs
+    int CH = kSelChunkMax;
+    const int64_t target = (int64_t)2 * num_sms() * 4 / 5;
+    while (CH > kSelChunkMin && (int64_t)pairs * ((max_blk + CH - 1) / CH) < target) CH /= 2;
+    if (sel_chunk_env()) CH = sel_chunk_env();
     while ((size_t)((max_blk + CH - 1) / CH) * k > kSelMaxMerge && CH < kSelChunkMax) CH *= 2;
     const int nchunks = (max_blk + CH - 1) / CH;
     const size_t nc = pairs * nchunks * k;
