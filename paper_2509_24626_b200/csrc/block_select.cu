@@ -482,8 +482,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                         if constexpr (TT == 2)
                             accB[g] = __fma_rn(qv[g], __hiloint2double(hNB ^ (fv[g] & dB), 0), accB[g]);
                     }
-                    continue;
-                }
+                } else {
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const double2 qq = qpn[c * G + g];
@@ -495,6 +494,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                             accB[g] = __fma_rn(qq.y, dminB, accB[g]);
                         }
                     }
+                }
                 }
             }
         }
@@ -648,7 +648,8 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
                        int32_t* __restrict__ sel,
                        uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_j,
                        int32_t* __restrict__ tickets) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char tc_smem[];
+    unsigned char* smem_raw = tc_smem;
     // [region: tile stages (tile phase) | keys u64 + jpos i32 (select phase)]
     // [lo f32 [CH]][hi f32 [CH]][qs f64 [128 G]][qf i32 [128 G]][hist 256][sw 64][bar]
     unsigned char* stage_base = smem_raw;

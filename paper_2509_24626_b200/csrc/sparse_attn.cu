@@ -544,7 +544,6 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
 // CTA (one CTA per SM).  NS = 2, NW = 6 (round 1) splits a C3 pair over ~16
 // warps; NS = 4, NW = 3 keeps the same bytes in flight per SM with half the
 // warps, so half the partials to merge per pair.
-constexpr int kMmaNW = 6;  // warps per CTA at NS = 2 (workspace sizing bound)
 template <int NS>
 struct MmaCfg {
     static constexpr int NW = NS == 2 ? 6 : (NS == 3 ? 4 : 3);
