@@ -124,7 +124,7 @@ __device__ __forceinline__ bool partial_is_last(const AttnArgs& a, int64_t p) {
 
 // The last contributor merges all partials of pair p in warp order
 // (deterministic) and writes the output, then resets the ticket.
-template <int G>
+template <int G, int UNR>
 __device__ void merge_partials(const AttnArgs& a, int64_t p, int w) {
     const int lane = lane_id();
     const int Ku = a.k + 1;
@@ -203,7 +203,6 @@ __device__ void merge_partials(const AttnArgs& a, int64_t p, int w) {
                 }
             }
             const int n = min(32, nc - i0);
-            constexpr int UNR = 8;  // loads in flight vs registers (GC = 4: 8 measured better than 4 at C3)
 #pragma unroll UNR
             for (int j = 0; j < n; ++j) {
                 const int64_t bj = __shfl_sync(0xffffffffu, base_i, j);
@@ -511,7 +510,7 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
             *reinterpret_cast<float4*>(pp + 4 + 4 * lane) =
                 make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
         }
-        if (partial_is_last(a, p)) merge_partials<G>(a, p, w);
+        if (partial_is_last(a, p)) merge_partials<G, 4>(a, p, w);
     }
 }
 
@@ -891,7 +890,7 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
         }
         // the last contributor merges at once (measured: deferring the merge to
         // the end of the warp's range did not shorten the kernel, r02l)
-        if (partial_is_last(a, p)) merge_partials<G>(a, p, w);
+        if (partial_is_last(a, p)) merge_partials<G, (G >= 8 ? 4 : 8)>(a, p, w);  // contributors' loads per batch (C3, G = 4: 8 measured better than 4)
     }
     trace(2);
 }
