@@ -351,22 +351,26 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     for (int tl = warp; tl < ntiles; tl += kSelWarps) {
         const int tile = j0 / 32 + tl;
         const char* tb = meta_pair + (size_t)tile * TILE_ELEMS * ES + lane * 16;
-        if (l2pf && lane == 0 && tl + kSelWarps < ntiles)  // next tile of this warp -> L2
+        if ((l2pf & 1) && lane == 0 && tl + kSelWarps < ntiles)  // next tile of this warp -> L2
             prefetch_l2_bulk(meta_pair + (size_t)(tile + kSelWarps) * TILE_ELEMS * ES, TILE_ELEMS * ES);
         // fully unrolled over the NCH chunks, loads kept D chunks ahead
         constexpr int D = 6, R = D + 1;
         uint4 mn[R], mx[R];
+        // (debug experiment SS_SEL_L2PF=2: read the min rows only -- wrong scores,
+        // half the metadata bytes: the step-time effect of a half-size read)
+        const bool half_exp = (l2pf & 2) != 0;
 #pragma unroll
         for (int s = 0; s < D; ++s) {
             mn[s] = ldg_stream(tb + (size_t)((s * 2 + 0) * 32) * 16);
-            mx[s] = ldg_stream(tb + (size_t)((s * 2 + 1) * 32) * 16);
+            mx[s] = half_exp ? mn[s] : ldg_stream(tb + (size_t)((s * 2 + 1) * 32) * 16);
         }
         double acc = 0.0;
 #pragma unroll
         for (int s = 0; s < NCH; ++s) {
             if (s + D < NCH) {
                 mn[(s + D) % R] = ldg_stream(tb + (size_t)(((s + D) * 2 + 0) * 32) * 16);
-                mx[(s + D) % R] = ldg_stream(tb + (size_t)(((s + D) * 2 + 1) * 32) * 16);
+                mx[(s + D) % R] = half_exp ? mn[(s + D) % R]
+                                           : ldg_stream(tb + (size_t)(((s + D) * 2 + 1) * 32) * 16);
             }
             const uint4 wn = mn[s % R], wx = mx[s % R];
             const uint4 mk = *reinterpret_cast<const uint4*>(qmask1 + s * (BF16 ? 4 : 4));
