@@ -43,6 +43,7 @@ namespace ss {
 constexpr int kAttnPartStride = 132;
 // floats per (warp, seg, g) partial: m, l, pad, pad, o[128]
 constexpr int kMinUnitsPerWarp = 8;  // measured: C3 26.6 us at 8 vs 30.7 at 4 / 16, C2 unchanged
+constexpr int kTraceSlots = 12;       // debug timeline words per warp (AttnArgs::trace)
 
 struct AttnArgs {
     const void* q;
@@ -63,9 +64,12 @@ struct AttnArgs {
     int mode;
     float* lse;
     int64_t U;  // pairs * (k + 1)
+    int merge_bulk;  // 1: end-of-range merges through bulk loads (default); 0: registers (debug A/B)
     int W;      // total warps
-    unsigned long long* trace;  // debug (SS_ATTN_TRACE=1): per warp globaltimer at entry / last unit / exit / merge start / merge end
+    unsigned long long* trace;  // debug (SS_ATTN_TRACE=1): per warp globaltimer at entry / last unit / exit / merge start / merge end / partial flush / ticket / (m, l) loaded
 };
+
+__device__ __forceinline__ bool knob_attn_merge_bulk(const AttnArgs& a) { return a.merge_bulk != 0; }
 
 template <bool BF16>
 struct AttnTraits {
@@ -109,13 +113,22 @@ __device__ __forceinline__ void load_q(const AttnArgs& a, int b, int h, int lane
 // A warp whose range cut pair p has written its partial (m, l, o) of the G
 // heads: take a ticket; true for the last contributor, which then merges all
 // partials (merge_partials).
+// The ticket is one acq_rel atomic: its release half (after the warp barrier,
+// cumulative over every lane's partial stores) publishes this warp's partial,
+// its acquire half makes the other contributors' partials visible to the last
+// one -- no separate sequentially consistent fences (measured: each
+// fence.sc.gpu cost ~0.8 us at the end of a launch, r02v).
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int32_t* p, int v) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
 __device__ __forceinline__ bool partial_is_last(const AttnArgs& a, int64_t p) {
     const int lane = lane_id();
     const int Ku = a.k + 1;
-    __threadfence();
     __syncwarp();
     int ticket = 0;
-    if (lane == 0) ticket = atomicAdd(&a.tickets[p], 1);
+    if (lane == 0) ticket = atom_add_acq_rel_gpu(&a.tickets[p], 1);
     ticket = __shfl_sync(0xffffffffu, ticket, 0);
     const int64_t wf = warp_of_unit(p * Ku, a.U, a.W);
     const int64_t wl = warp_of_unit((p + 1) * Ku - 1, a.U, a.W);
@@ -131,12 +144,11 @@ __device__ void merge_partials(const AttnArgs& a, int64_t p, int w) {
     const int b = (int)(p / a.Hkv), h = (int)(p % a.Hkv);
     const int64_t wf = warp_of_unit(p * Ku, a.U, a.W);
     const int64_t wl = warp_of_unit((p + 1) * Ku - 1, a.U, a.W);
-    __threadfence();
     auto trace = [&](int i) {
         if (a.trace != nullptr && lane == 0) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            a.trace[(int64_t)w * 5 + i] = t;
+            a.trace[(int64_t)w * kTraceSlots + i] = t;
         }
     };
     trace(3);
@@ -182,6 +194,7 @@ __device__ void merge_partials(const AttnArgs& a, int64_t p, int w) {
         }
 #pragma unroll
         for (int g = 0; g < GC; ++g) mt[g] = warp_max(mt[g]);
+        if (g0 == 0) trace(7);
         for (int i0 = 0; i0 < nc; i0 += 32) {
             // lane-parallel: contributor i0 + lane's partial offset and scale per head
             const int i = i0 + lane;
@@ -221,7 +234,7 @@ __device__ void merge_partials(const AttnArgs& a, int64_t p, int w) {
 #pragma unroll
         for (int g = 0; g < GC; ++g) {
             const float lsum = warp_sum(lt[g]);
-            const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+            const float inv = lsum > 0.f ? __frcp_rn(lsum) : 0.f;
             const int hq = h * G + g0 + g;
             if (a.lse != nullptr && lane == 0)
                 a.lse[(int64_t)hq * a.B + b] = lsum > 0.f ? mt[g] + log2f(lsum) : -INFINITY;
@@ -490,7 +503,7 @@ __global__ void __launch_bounds__(AttnTraits<BF16>::NW * 32, 1) sparse_attn_kern
         if (full) {
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                const float inv = l[g] > 0.f ? 1.f / l[g] : 0.f;
+                const float inv = l[g] > 0.f ? __frcp_rn(l[g]) : 0.f;
                 const int hq = h * G + g;
                 *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) =
                     make_float4(o[g][0] * inv, o[g][1] * inv, o[g][2] * inv, o[g][3] * inv);
@@ -551,8 +564,136 @@ struct MmaCfg {
 template <int NS>
 struct MmaWarpSmem {
     alignas(1024) unsigned char buf[NS][16384];  // [stage] K-lo | K-hi | V-lo | V-hi
+    unsigned char merge_extra[4096];              // with buf: the merge's landing zone (C3, G = 4: 17 partials)
     uint64_t bar[NS][2];                          // [stage][K half / V half]
+    uint64_t mbar;                                // end-of-range partial merge (bulk loads)
 };
+
+// End-of-range merge (the common case: the last contributor of a cut pair is
+// usually the warp whose range ENDS in the pair, so it merges after its last
+// unit, with its stage buffers idle).  The contributors' partials -- G heads x
+// kAttnPartStride floats each, contiguous -- are pulled into those buffers by
+// one bulk copy per contributor (lane i issues contributor i's), all on one
+// mbarrier: one round trip per buffer-full of partials (C2: every partial at
+// once; C3, G = 4: 15 of ~17), instead of one for (m, l) and one per 8
+// contributors' o through registers (merge_partials; ~0.9 us per round trip at
+// the end of a launch, r02v).  Rounds combine by the usual rescaling, in warp
+// order (deterministic).
+template <int G, int NS>
+__device__ void merge_partials_bulk(const AttnArgs& a, int64_t p, int w, MmaWarpSmem<NS>& sm, uint32_t& phase) {
+    constexpr int kBytes = G * kAttnPartStride * 4;
+    constexpr int kCapBuf = (NS * 16384 + 4096) / kBytes;  // buf + merge_extra (contiguous)
+    constexpr int kCap = kCapBuf < 32 ? kCapBuf : 32;  // contributors per round (lane-parallel)
+    static_assert(kCap >= 1, "a partial must fit the stage buffers");
+    const int lane = lane_id();
+    const int Ku = a.k + 1;
+    const int64_t wf = warp_of_unit(p * Ku, a.U, a.W);
+    const int64_t wl = warp_of_unit((p + 1) * Ku - 1, a.U, a.W);
+    const int nc = (int)(wl - wf + 1);
+    auto trace = [&](int i) {
+        if (a.trace != nullptr && lane == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.trace[(int64_t)w * kTraceSlots + i] = t;
+        }
+    };
+    trace(3);
+    const int64_t pkw = p * Ku * (int64_t)a.W;
+    unsigned char* dst = &sm.buf[0][0];
+    float* P = reinterpret_cast<float*>(dst);
+    float M[G], L[G], O[G][4];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        M[g] = -INFINITY;
+        L[g] = 0.f;
+        O[g][0] = O[g][1] = O[g][2] = O[g][3] = 0.f;
+    }
+    for (int r0 = 0; r0 < nc; r0 += kCap) {
+        const int n = min(kCap, nc - r0);
+        if (lane == 0) {
+            // the previous round's shared-memory reads (generic proxy) before
+            // this round's async-proxy writes
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&sm.mbar, (uint32_t)(n * kBytes));
+        }
+        __syncwarp();
+        if (lane < n) {
+            const int64_t w2 = wf + r0 + lane;
+            const int64_t off = ((w2 * 2 + (a.U * w2 >= pkw ? 0 : 1)) * G) * kAttnPartStride;
+            // the partials were written through the generic proxy (acquired by
+            // the ticket); order them before this async-proxy read
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            bulk_g2s(dst + lane * kBytes, a.part + off, kBytes, &sm.mbar);
+        }
+        mbar_wait(&sm.mbar, phase);
+        phase ^= 1u;
+        trace(r0 == 0 ? 7 : 9);
+        // (1) lane-parallel over the round's n*G (contributor, head) items --
+        // item i = j*G + g sits at P + i*kAttnPartStride, and lane t owns items
+        // t, t+32, ..., all of head g = t % G: the head max, the scale factors
+        // sc_i = 2^(m_i - M) (kept in the partial's pad word for step 2) and the
+        // l sums reduce over the lanes of one head (xor strides >= G).
+        // (2) every lane accumulates its 4 dims of o over the items (broadcast
+        // loads of sc).  (Measured: one lane walking every item with dependent
+        // loads / exp2 spent ~220 cycles per contributor at G = 4, r02ab +
+        // tools/merge_probe.cu.)
+        const int gl = lane % G;
+        float mloc = -INFINITY;
+        for (int i = lane; i < n * G; i += 32) mloc = fmaxf(mloc, P[i * kAttnPartStride]);
+#pragma unroll
+        for (int o = 16; o >= G; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+        float Mg = M[0];
+#pragma unroll
+        for (int g = 1; g < G; ++g)
+            if (gl == g) Mg = M[g];
+        const float mnew = fmaxf(Mg, mloc);
+        const float corr_l = Mg == -INFINITY ? 0.f : exp2f(Mg - mnew);
+        float lloc = 0.f;
+        for (int i = lane; i < n * G; i += 32) {
+            float* pi = P + i * kAttnPartStride;
+            const float sc = mnew == -INFINITY ? 0.f : exp2f(pi[0] - mnew);
+            lloc = fmaf(pi[1], sc, lloc);
+            pi[2] = sc;
+        }
+#pragma unroll
+        for (int o = 16; o >= G; o >>= 1) lloc += __shfl_xor_sync(0xffffffffu, lloc, o);
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const float cg = __shfl_sync(0xffffffffu, corr_l, g);
+            L[g] = fmaf(L[g], cg, __shfl_sync(0xffffffffu, lloc, g));
+            M[g] = __shfl_sync(0xffffffffu, mnew, g);
+            O[g][0] *= cg, O[g][1] *= cg, O[g][2] *= cg, O[g][3] *= cg;
+        }
+#pragma unroll 4
+        for (int j = 0; j < n; ++j) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float* pj = P + (j * G + g) * kAttnPartStride;
+                const float sc = pj[2];
+                const float4 ov = *reinterpret_cast<const float4*>(pj + 4 + 4 * lane);
+                O[g][0] = fmaf(ov.x, sc, O[g][0]);
+                O[g][1] = fmaf(ov.y, sc, O[g][1]);
+                O[g][2] = fmaf(ov.z, sc, O[g][2]);
+                O[g][3] = fmaf(ov.w, sc, O[g][3]);
+            }
+        }
+        __syncwarp();
+        trace(r0 == 0 ? 8 : 10);
+    }
+    const int b = (int)(p / a.Hkv), h = (int)(p % a.Hkv);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const float inv = L[g] > 0.f ? __frcp_rn(L[g]) : 0.f;  // == 1.f / L (IEEE), no division subroutine
+        const int hq = h * G + g;
+        if (a.lse != nullptr && lane == 0)
+            a.lse[(int64_t)hq * a.B + b] = L[g] > 0.f ? M[g] + log2f(L[g]) : -INFINITY;
+        *reinterpret_cast<float4*>(a.out + ((int64_t)hq * a.B + b) * kHeadDim + 4 * lane) =
+            make_float4(O[g][0] * inv, O[g][1] * inv, O[g][2] * inv, O[g][3] * inv);
+    }
+    trace(4);
+    if (lane == 0) a.tickets[p] = 0;
+}
 
 // Per-stage unit descriptors kept in registers: a runtime stage index selects
 // among statically indexed scalars (no local-memory array).
@@ -610,7 +751,7 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
         if (a.trace != nullptr && lane == 0) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            a.trace[(int64_t)w * 5 + i] = t;
+            a.trace[(int64_t)w * kTraceSlots + i] = t;
         }
     };
     trace(0);
@@ -621,6 +762,7 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
             mbar_init(&sm.bar[st][0], 1);
             mbar_init(&sm.bar[st][1], 1);
         }
+        mbar_init(&sm.mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_pool)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_tail)) : "memory");
@@ -653,6 +795,7 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
     };
     refill();
     int next_l = 0;   // next lane of the window to consider
+    int q_pref_pair = -1;  // pair whose q was last prefetched
     // unit held by each stage: kind (0 = none), K row in the tensor map, pair (-1 = none)
     StageRegs<NS> sr;
 #pragma unroll
@@ -677,8 +820,17 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
                 next_l = l + 1;
                 sr.set(sr.kind, stage, __shfl_sync(0xffffffffu, wkind, l));
                 sr.set(sr.row, stage, __shfl_sync(0xffffffffu, wrow, l));
-                sr.set(sr.pair, stage, __shfl_sync(0xffffffffu, wpair, l));
+                const int np = __shfl_sync(0xffffffffu, wpair, l);
+                sr.set(sr.pair, stage, np);
                 issue_half(stage, 0);
+                if (np != q_pref_pair) {
+                    // a new pair: its q (G x 256 B) into L1 now, so the q loads at
+                    // its start hit instead of stalling the warp ~1 us
+                    q_pref_pair = np;
+                    if (lane < 2 * G)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)a.q +
+                            ((int64_t)(np / a.Hkv) * a.Hq + (int64_t)(np % a.Hkv) * G) * kHeadDim * 2 + lane * 128));
+                }
                 return;
             }
             if (wbase + 32 >= u1) {
@@ -859,7 +1011,7 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 if (2 * c + e < G) {
-                    const float inv = l[e] > 0.f ? 1.f / l[e] : 0.f;
+                    const float inv = l[e] > 0.f ? __frcp_rn(l[e]) : 0.f;
                     float* op = a.out + ((int64_t)(h * G + 2 * c + e) * a.B + b) * kHeadDim + r;
                     if (a.lse != nullptr && r == 0)
                         a.lse[(int64_t)(h * G + 2 * c + e) * a.B + b] = l[e] > 0.f ? m[e] + log2f(l[e]) : -INFINITY;
@@ -873,6 +1025,8 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
             continue;
         }
         const int seg = (p == p_first) ? 0 : 1;
+        unsigned long long t_flush = 0;
+        if (a.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_flush));
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             if (2 * c + e < G) {
@@ -888,9 +1042,20 @@ sparse_attn_mma_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tm_
                 }
             }
         }
-        // the last contributor merges at once (measured: deferring the merge to
-        // the end of the warp's range did not shorten the kernel, r02l)
-        if (partial_is_last(a, p)) merge_partials<G, (G >= 8 ? 4 : 8)>(a, p, w);  // contributors' loads per batch (C3, G = 4: 8 measured better than 4)
+        // the last contributor merges: mid-range through registers (units still
+        // in flight in the stages), at the range end through bulk loads into the
+        // idle stage buffers.  (Measured: deferring a mid-range cut pair's ticket
+        // to the range end shortened the stragglers' streaming but made some
+        // warps last for two pairs -- two serial merges in the tail, r02z.)
+        if (partial_is_last(a, p)) {
+            if (a.trace != nullptr && lane == 0) a.trace[(int64_t)w * kTraceSlots + 5] = t_flush;
+            trace(6);
+            uint32_t mphase = 0;
+            if (p == p_last && knob_attn_merge_bulk(a))
+                merge_partials_bulk<G, NS>(a, p, w, sm, mphase);
+            else
+                merge_partials<G, (G >= 8 ? 4 : 8)>(a, p, w);  // contributors' loads per batch (C3, G = 4: 8 measured better than 4)
+        }
     }
     trace(2);
 }
@@ -917,8 +1082,8 @@ static size_t attn_ws_bytes_core(const ss_dims& d, ss_dtype dt) {
 }
 
 size_t attn_ws_bytes(const ss_dims& d, int k, ss_dtype dt) {
-    // + debug timeline (5 x u64 per warp) after the core workspace when traced
-    return attn_ws_bytes_core(d, dt) + (attn_trace_on() ? (size_t)attn_total_warps(dt) * 5 * 8 : 0);
+    // + debug timeline (kTraceSlots x u64 per warp) after the core workspace when traced
+    return attn_ws_bytes_core(d, dt) + (attn_trace_on() ? (size_t)attn_total_warps(dt) * kTraceSlots * 8 : 0);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -954,6 +1119,9 @@ template <int NS>
 constexpr size_t mma_smem() {  // + base alignment slack
     return sizeof(MmaWarpSmem<NS>) * MmaCfg<NS>::NW + 1024;
 }
+// (+ 1 KiB static shared memory) within the 227 KiB a CTA may use on sm_100
+static_assert(mma_smem<2>() + 1024 <= 232448 && mma_smem<3>() + 1024 <= 232448 && mma_smem<4>() + 1024 <= 232448,
+              "attention CTA exceeds the shared-memory limit");
 constexpr int kAttnStages = 2;  // default stages per warp (NS); SS_ATTN_STAGES=3|4 (debug A/B)
 
 static int mma_stages() {
@@ -1065,6 +1233,7 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
     a.scale_log2 = scale * 1.4426950408889634f;
     const int G = d.num_q_heads / d.num_kv_heads;
     a.U = (int64_t)d.batch * d.num_kv_heads * (k + 1);
+    a.merge_bulk = knob("SS_ATTN_MERGE_BULK", 1);
     // at least kMinUnitsPerWarp units (128 KiB in bf16) per warp: fewer, longer
     // ranges when the problem is small (C3: ~16 partials per pair to merge instead
     // of ~28); W <= U keeps every range non-empty

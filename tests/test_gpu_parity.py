@@ -425,6 +425,15 @@ def test_attention_many_pairs_stream_k(ops):
     _attn_case(ops, synth.DT_BF16, 16, 32, 32, 64, 4096, [3] * 16, seed=60)
 
 
+@pytest.mark.parametrize("G,k", [(1, 255), (2, 247), (4, 127), (8, 64)])
+def test_attention_one_pair_many_contributors(ops, G, k):
+    # one (b, h) pair cut over every warp of the launch (W = U / 8): its last
+    # contributor merges up to 32 partials -- G = 1, 2 through the end-of-range
+    # bulk-load merge (31 x 2 heads x 528 B: the 32 KiB edge), G = 4, 8 past it
+    # (the register merge)
+    _attn_case(ops, synth.DT_BF16, 1, G, 1, k, 600, [9], seed=90 + G)
+
+
 def test_attention_skipped_on_error_status(ops):
     d = ops.dims(1, 1, 1)
     ws = ops.alloc_workspace(2, d, 32, 1)

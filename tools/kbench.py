@@ -58,8 +58,11 @@ def bench_select(c, iters):
 def bench_attn(c, iters):
     B, Hq, Hkv, k, S = c["B"], c["Hq"], c["Hkv"], c["k"], c["S"]
     pool = torch.randn(S * 2 * 32 * 128, device="cuda").to(torch.bfloat16)
-    slot = torch.stack([torch.randperm(S, device="cuda")[:k] for _ in range(B * Hkv)]).view(B, Hkv, k)
-    slot = slot.sort(-1).values.to(torch.int32).contiguous()
+    def rand_slots():
+        sl = torch.stack([torch.randperm(S, device="cuda")[:k] for _ in range(B * Hkv)]).view(B, Hkv, k)
+        return sl.sort(-1).values.to(torch.int32).contiguous()
+    slot = rand_slots()
+    slot_sets = [slot] + [rand_slots() for _ in range(3)]   # back-to-back timing: no L2 reuse
     q = torch.randn(B, Hq, 128, device="cuda").to(torch.bfloat16)
     tail = torch.zeros(B * Hkv * 2 * 32 * 128, dtype=torch.bfloat16, device="cuda")
     tl = torch.zeros(B, dtype=torch.int32, device="cuda")
@@ -89,11 +92,22 @@ def bench_attn(c, iters):
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
     ms = sorted(ts)[len(ts) // 2]
+    # back to back (the bench's kernels_solo method): 40 launches over 4 slot sets
+    # after a device spin, one event pair -- the average launch duration
+    nb2b = 40
+    torch.sum(flush, dim=0, out=sink)
+    torch.cuda._sleep(3000000)
+    s.record()
+    for i in range(nb2b):
+        ops.sparse_decode_attn(q, pool, slot_sets[i % 4], k, tail, tl, d, 1 / math.sqrt(128), out, ws)
+    e.record()
+    torch.cuda.synchronize()
+    ms_b2b = s.elapsed_time(e) / nb2b
     byts = B * Hkv * k * 16384
     if os.environ.get("SS_ATTN_TRACE"):
         # per-warp globaltimer (ns) at entry / last unit done / exit (debug timeline)
         nw = 148 * 6
-        tr = ws.view(torch.uint8)[-nw * 40:].view(torch.int64).view(nw, 5).cpu()
+        tr = ws.view(torch.uint8)[-nw * 96:].view(torch.int64).view(nw, 12).cpu()
         ok = tr[:, 0] > 0
         widx = torch.arange(nw)[ok]
         tr = tr[ok]
@@ -107,13 +121,31 @@ def bench_attn(c, iters):
                           "last_unit_us": q(rel[:, 1]), "exit_us": q(rel[:, 2]),
                           "merges": len(mg), "merge_us": q(mdur) if len(mg) else None,
                           "merge_start_us": q(mstart) if len(mg) else None}))
+        if len(mg):
+            d = lambda i, j: (mg[:, j] - mg[:, i]).double() / 1e3
+            print(json.dumps({"merging_warps_us": {"flush_to_ticket": q(d(5, 6)), "ticket_to_merge_start": q(d(6, 3)),
+                                                   "merge_m_l_loads": q(d(3, 7)), "merge_o_loads_and_store": q(d(7, 4)),
+                                                   "merge_end_to_exit": q(d(4, 2))}}))
+            m2 = mg[mg[:, 8] > 0]
+            if len(m2):
+                d2 = lambda i, j: (m2[:, j] - m2[:, i]).double() / 1e3
+                r2 = m2[m2[:, 9] > 0]
+                out = {"bulk_merges": len(m2), "round0_load": q(d2(3, 7)), "round0_compute": q(d2(7, 8))}
+                if len(r2):
+                    d3 = lambda i, j: (r2[:, j] - r2[:, i]).double() / 1e3
+                    out.update({"two_round_merges": len(r2), "round1_load": q(d3(8, 9)), "round1_compute": q(d3(9, 10)),
+                                "store": q(d3(10, 4))})
+                else:
+                    out["store"] = q(d2(8, 4))
+                print(json.dumps(out))
         # imbalance structure: mean last-unit time by warp slot in the CTA and by SM id
         lu = rel[:, 1]
         slot, sm = widx // 148, widx % 148
         print(json.dumps({"last_unit_by_warp_slot": [round(float(lu[slot == i].mean()), 2) for i in range(6) if (slot == i).any()],
                           "last_unit_by_sm_decile": [round(float(lu[(sm >= 15 * i) & (sm < 15 * i + 15)].mean()), 2) for i in range(10)],
                           "last_unit_even_odd_sm": [round(float(lu[sm % 2 == 0].mean()), 2), round(float(lu[sm % 2 == 1].mean()), 2)]}))
-    return {"kernel": "attn", "us": ms * 1e3, "GBps": byts / ms / 1e6, "frac": byts / ms / 1e6 / PEAK}
+    return {"kernel": "attn", "us": ms * 1e3, "GBps": byts / ms / 1e6, "frac": byts / ms / 1e6 / PEAK,
+            "us_b2b": ms_b2b * 1e3, "frac_b2b": byts / ms_b2b / 1e6 / PEAK}
 
 
 def bench_gather(c, iters, nmiss=2500):
