@@ -35,6 +35,8 @@
 
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace ss {
@@ -90,13 +92,64 @@ __device__ __forceinline__ double f32_scaled(uint32_t x) {
 // Writes the selected positions, ascending, to out_pos (smem or global via
 // functor).  k_sel = min(k, n) positions are produced.
 // ---------------------------------------------------------------------------
+// The bits above the highest bit in which the keys differ are common to all of
+// them: the radix passes start at the digit holding that bit (one reduction
+// instead of up to 7 passes whose histograms put every key into ONE bin -- the
+// scores share sign, exponent and leading mantissa bits -- and serialise on its
+// shared-memory atomic; measured, r02ac).  Returns the first shift and sets
+// prefix / mask to the common bits.  Uses hist as scratch; contains __syncthreads().
+template <int NT, typename K>
+__device__ int radix_common_prefix(const K* keys, int n, int* hist, K& prefix, K& mask) {
+    constexpr int NB = (int)sizeof(K) * 8;
+    const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    K kmin = ~(K)0, kmax = 0;
+    for (int i = tid; i < n; i += NT) {
+        const K key = keys[i];
+        kmin = key < kmin ? key : kmin;
+        kmax = key > kmax ? key : kmax;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const K a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
+        kmin = a < kmin ? a : kmin;
+        kmax = b > kmax ? b : kmax;
+    }
+    K* red = reinterpret_cast<K*>(hist);  // [NT/32] min, [NT/32] max
+    __syncthreads();  // hist may still be read by a previous select
+    if (lane == 0) {
+        red[w] = kmin;
+        red[NT / 32 + w] = kmax;
+    }
+    __syncthreads();
+    kmin = red[0];
+    kmax = red[NT / 32];
+#pragma unroll
+    for (int i = 1; i < NT / 32; ++i) {
+        kmin = red[i] < kmin ? red[i] : kmin;
+        kmax = red[NT / 32 + i] > kmax ? red[NT / 32 + i] : kmax;
+    }
+    __syncthreads();
+    const K diff = kmin ^ kmax;
+    if (diff == 0) {  // every key equal: all bits common
+        prefix = kmin;
+        mask = ~(K)0;
+        return -8;
+    }
+    const int hb = NB - 1 - (sizeof(K) == 8 ? __clzll((long long)diff) : __clz((int)diff));
+    const int shift = hb / 8 * 8;
+    mask = shift + 8 >= NB ? (K)0 : (~(K)0) << (shift + 8);
+    prefix = kmin & mask;
+    return shift;
+}
+
 template <int NT, bool AGG = true, typename Emit>
 __device__ void cta_topk_t(const uint64_t* keys, int n, int k_sel, int* hist, int* sw, Emit emit) {
     const int tid = threadIdx.x;
     uint64_t prefix = 0, mask = 0;
     int rem = k_sel;
     if (k_sel < n) {
-        for (int shift = 56; shift >= 0; shift -= 8) {
+        const int shift0 = radix_common_prefix<NT>(keys, n, hist, prefix, mask);
+        for (int shift = shift0; shift >= 0; shift -= 8) {
             for (int i = tid; i < 256; i += NT) hist[i] = 0;
             __syncthreads();
             {  // (measured: warp-aggregated match_any voting was slower, r02o)
@@ -606,7 +659,13 @@ __device__ uint32_t cta_kth_u32(const uint32_t* keys, int n, int kk, int* hist, 
     const int tid = threadIdx.x;
     uint32_t prefix = 0, mask = 0;
     int rem = kk;
-    for (int shift = 24; shift >= 0; shift -= 8) {
+    // the candidate filter only needs a LOWER bound of the k-th largest key (a
+    // smaller tau admits more candidates, all rescored exactly): start below the
+    // keys' common prefix and stop after two digits -- the lower edge of the
+    // bin holding the k-th key, 16 bits below the keys' spread
+    const int shift0 = radix_common_prefix<kTcThreads>(keys, n, hist, prefix, mask);
+    const int shift_end = shift0 - 8;
+    for (int shift = shift0; shift >= 0 && shift >= shift_end; shift -= 8) {
         for (int i = tid; i < 256; i += kTcThreads) hist[i] = 0;
         __syncthreads();
         for (int i = tid; i < n; i += kTcThreads) {
@@ -644,11 +703,28 @@ __device__ uint32_t cta_kth_u32(const uint32_t* keys, int n, int kk, int* hist, 
     return prefix;
 }
 
+#ifdef SS_DEBUG_KNOBS
+// debug timeline of the tensor-core select (SS_SEL_TRACE=1): per CTA, globaltimer
+// at start / tile phase done / threshold / rescoring / chunk top-k / merge start /
+// merge end, and the candidate count; read by ss_debug_sel_trace
+__device__ unsigned long long g_sel_trace[16384 * 8];
+#endif
+__device__ __forceinline__ void sel_stamp(int on, int slot, unsigned long long v = 0) {
+#ifdef SS_DEBUG_KNOBS
+    if (on && threadIdx.x == 0) {
+        if (slot != 7) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+        if (blockIdx.x < 16384) g_sel_trace[blockIdx.x * 8 + slot] = v;
+    }
+#else
+    (void)on, (void)slot, (void)v;
+#endif
+}
+
 template <int G, int NS>
 __global__ void __launch_bounds__(kTcThreads, NS == 1 ? 2 : 1)
 block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                        const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
-                       int nchunks, int CH, int region_bytes, int rot_mul, int pf_dist,
+                       int nchunks, int CH, int region_bytes, int rot_mul, int pf_dist, int tr,
                        int32_t* __restrict__ sel,
                        uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_j,
                        int32_t* __restrict__ tickets) {
@@ -666,6 +742,7 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
     int* sw = hist + 256;
     uint64_t* bars = (uint64_t*)(sw + 64);
     const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+    sel_stamp(tr, 0);
     const int pair = blockIdx.x / nchunks, ci = blockIdx.x % nchunks;
     const int b = pair / Hkv, h = pair % Hkv;
     const int nb = n_blk_arr[b];
@@ -801,6 +878,7 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
             }
     }
     __syncthreads();
+    sel_stamp(tr, 1);
 
     // ---- threshold and candidates ----
     const int kk = min(k, nb_chunk);
@@ -808,7 +886,11 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
     for (int i = tid; i < nb_chunk; i += kTcThreads) lkey[i] = ord32(lo[i]);
     __syncthreads();
     const uint32_t tau = kk < nb_chunk ? cta_kth_u32(lkey, nb_chunk, kk, hist, sw) : 0u;
-    int32_t* jpos = (int32_t*)(smem_raw + (size_t)max(CH, min(nchunks * k, kSelMaxMerge)) * 8);
+    // per-chunk layout after the tile phase: candidate positions at the region
+    // start, their exact keys after CH positions, the rescoring stage from there
+    // to the end of hi[] (the region and lo / hi are dead by then)
+    int32_t* jpos = (int32_t*)smem_raw;
+    uint64_t* ckeys = (uint64_t*)(smem_raw + (size_t)CH * 4);
     int n_cand;
     {
         const int per = (nb_chunk + kTcThreads - 1) / kTcThreads;
@@ -822,6 +904,8 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
         n_cand = tot;
     }
     __syncthreads();
+    sel_stamp(tr, 2);
+    sel_stamp(tr, 7, (unsigned long long)n_cand);
 
     // ---- exact fp64 rescoring of the candidates (the oracle's arithmetic) ----
     // A candidate's 512 B of metadata are 32 scattered 16-byte pieces of its
@@ -830,9 +914,12 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
     // rescores one candidate from shared memory.  (Loading them per thread
     // serialised ~8 global round trips per candidate.)
     {
-        const int cap_keys = max(CH, min(nchunks * k, kSelMaxMerge));
-        unsigned char* cstage = smem_raw + (((size_t)cap_keys * 12 + 127) & ~(size_t)127);
-        const int batch = min(kTcThreads, (region_bytes - (int)(cstage - smem_raw)) / 512);
+        // one batch of (up to) kTcThreads candidates per round trip: ~k + a few
+        // candidates fit at once (the former stage, behind the merge's key space,
+        // held 32: five DRAM round trips with one warp rescoring, r02ac)
+        unsigned char* cstage = smem_raw + (((size_t)CH * 4 + (size_t)n_cand * 8 + 127) & ~(size_t)127);
+        const int stage_end = region_bytes + 8 * CH;  // end of hi[]
+        const int batch = max(1, min(kTcThreads, (stage_end - (int)(cstage - smem_raw)) / 512));
         for (int base = 0; base < n_cand; base += batch) {
             const int nbt = min(batch, n_cand - base);
             for (int i = tid; i < nbt * 32; i += kTcThreads) {
@@ -869,31 +956,36 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
                 double sc = acc[0];
 #pragma unroll
                 for (int g = 1; g < G; ++g) sc = acc[g] > sc ? acc[g] : sc;
-                keys[base + tid] = ord_key(sc + 0.0);
+                ckeys[base + tid] = ord_key(sc + 0.0);
             }
             __syncthreads();
         }
     }
 
+    sel_stamp(tr, 3);
     // ---- exact top-k among the candidates (positions ascending = j ascending) ----
     int32_t* sel_pair = sel + (size_t)pair * k;
     if (nch_b == 1) {
-        cta_topk_t<kTcThreads>(keys, n_cand, kk, hist, sw, [&](int o, int pp) { sel_pair[o] = j0 + jpos[pp]; });
+        cta_topk_t<kTcThreads>(ckeys, n_cand, kk, hist, sw, [&](int o, int pp) { sel_pair[o] = j0 + jpos[pp]; });
         for (int rr2 = kk + tid; rr2 < k; rr2 += kTcThreads) sel_pair[rr2] = -1;
         return;
     }
     uint64_t* ck = cand_key + ((size_t)pair * nchunks + ci) * k;
     int32_t* cj = cand_j + ((size_t)pair * nchunks + ci) * k;
-    cta_topk_t<kTcThreads>(keys, n_cand, kk, hist, sw, [&](int o, int pp) {
-        ck[o] = keys[pp];
+    cta_topk_t<kTcThreads>(ckeys, n_cand, kk, hist, sw, [&](int o, int pp) {
+        ck[o] = ckeys[pp];
         cj[o] = j0 + jpos[pp];
     });
+    sel_stamp(tr, 4);
     __threadfence();
     __syncthreads();
     if (tid == 0) sw[48] = atomicAdd(&tickets[pair], 1);
     __syncthreads();
     if (sw[48] != nch_b - 1) return;
     __threadfence();
+    sel_stamp(tr, 5);
+    // merge layout: every chunk's candidates' keys, then their positions
+    int32_t* mjpos = (int32_t*)(smem_raw + (size_t)max(CH, min(nchunks * k, kSelMaxMerge)) * 8);
     int n = 0;
     for (int cc = 0; cc < nch_b; ++cc) {
         const int sz = min(CH, nb - cc * CH);
@@ -902,15 +994,384 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
         const int32_t* sj = cand_j + ((size_t)pair * nchunks + cc) * k;
         for (int i = tid; i < kcc; i += kTcThreads) {
             keys[n + i] = __ldcg(sk + i);
-            jpos[n + i] = __ldcg(sj + i);
+            mjpos[n + i] = __ldcg(sj + i);
         }
         n += kcc;
     }
     __syncthreads();
     const int kf = min(k, nb);
-    cta_topk_t<kTcThreads>(keys, n, kf, hist, sw, [&](int o, int pp) { sel_pair[o] = jpos[pp]; });
+    cta_topk_t<kTcThreads>(keys, n, kf, hist, sw, [&](int o, int pp) { sel_pair[o] = mjpos[pp]; });
     for (int rr2 = kf + tid; rr2 < k; rr2 += kTcThreads) sel_pair[rr2] = -1;
     if (tid == 0) tickets[pair] = 0;
+    sel_stamp(tr, 6);
+}
+
+// ---------------------------------------------------------------------------
+// Cluster form of the tensor-core GQA select (the default for bf16 GQA).  The
+// CS chunks of one (b, h) pair are the CS CTAs of one thread-block cluster, so
+// the candidate threshold is taken over the WHOLE pair instead of per chunk:
+//   1. tile phase as block_select_tc_kernel: approximate f32 scores with error
+//      bounds, L_j <= S_j <= U_j, for the CTA's chunk;
+//   2. tau' <= the k-th largest L_j of the pair, through distributed shared
+//      memory: cluster min / max of the finite L, a 256-bin histogram LINEAR in
+//      the value of L (monotone bins, few keys per bin -- the 8-bit radix digits
+//      of the ordered keys put most keys into one or two bins whose shared
+//      atomics serialise, r02ac), the bin b* holding the k-th largest, and tau'
+//      = the smallest L in bin b* (<= the k-th largest);
+//   3. candidates U_j >= tau' (and every block whose approximation is not
+//      finite) are rescored EXACTLY (the oracle's fp64 sum): ~k per PAIR
+//      instead of ~k per chunk, i.e. CS x fewer scattered 512-byte metadata
+//      re-reads from DRAM -- those re-reads, issued by every CTA at once, were
+//      the largest cost of the per-chunk form (r02ac/r02ad);
+//   4. each CTA keeps its exact top-k (only when it has more than k
+//      candidates) and writes (key, j) into the leader CTA's shared memory at
+//      its rank's offset -- ascending j across the cluster -- and the leader
+//      takes the exact top-k (ties -> lower j) and writes sel.
+// Exactness: k blocks have S >= L >= (k-th largest L) >= tau', so a block with
+// U < tau' has S < tau' and is beaten by k blocks; the union of the CTAs' exact
+// local top-k sets contains the pair's exact top-k.  No global workspace, no
+// tickets, no second launch-wide merge.
+// ---------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+constexpr int kTccMaxCluster = 16;
+
+template <int G, int NS>
+__global__ void __launch_bounds__(kTcThreads, NS == 1 ? 2 : 1)
+block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ meta,
+                        const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
+                        int CS, int CH, int region_bytes, int tr, int32_t* __restrict__ sel) {
+    extern __shared__ __align__(128) unsigned char tc_smem[];
+    unsigned char* smem_raw = tc_smem;
+    // [region: tile stages | candidate positions, keys, rescoring stage | leader
+    //  gather (key u64, j i32) at gather_off] [lo f32 [CH]][hi f32 [CH]]
+    // [qs f64 [128 G]][qf i32 [128 G]][hist 256][sw 64][xch 32 x u64][bars]
+    unsigned char* stage_base = smem_raw;
+    float* lo = (float*)(smem_raw + region_bytes);
+    float* hi = lo + CH;
+    double* qs = (double*)(hi + CH);
+    int32_t* qf = (int32_t*)(qs + kHeadDim * G);
+    int* hist = (int*)(qf + kHeadDim * G);
+    int* sw = hist + 256;
+    unsigned long long* xch = (unsigned long long*)(sw + 64);  // cluster exchange slots
+    uint64_t* bars = (uint64_t*)(xch + 32);
+    cg::cluster_group cluster = cg::this_cluster();
+    const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+    sel_stamp(tr, 0);
+    const int rank = (int)cluster.block_rank();
+    const int pair = blockIdx.x / CS, ci = rank;
+    const int b = pair / Hkv, h = pair % Hkv;
+    const int nb = n_blk_arr[b];
+    int32_t* sel_pair = sel + (size_t)pair * k;
+    if (k >= nb) {  // every block is selected (uniform over the cluster: no barrier)
+        if (rank == 0)
+            for (int i = tid; i < k; i += kTcThreads) sel_pair[i] = i < nb ? i : -1;
+        return;
+    }
+    const int j0 = ci * CH;
+    const int nb_chunk = max(0, min(CH, nb - j0));
+    const int ntiles = (nb_chunk + 31) / 32;
+    const char* meta_pair = (const char*)meta + ((size_t)pair * (max_blk / 32)) * kTileBytes;
+    const uint16_t* qb16 = (const uint16_t*)q + ((size_t)b * Hq + (size_t)h * G) * kHeadDim;
+
+    for (int i = tid; i < kHeadDim * G; i += kTcThreads) {
+        const int g = i % G, c = i / G;
+        const double qd = (double)__uint_as_float(((uint32_t)qb16[(size_t)g * kHeadDim + c]) << 16) * kQScale;
+        qs[i] = qd;
+        qf[i] = qd >= 0.0 ? -1 : 0;
+    }
+    for (int i = tid; i < 256; i += kTcThreads) hist[i] = 0;
+    if (lane == 0) {
+#pragma unroll
+        for (int st = 0; st < NS; ++st) mbar_init(&bars[warp * NS + st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    const int r = lane >> 2, c = lane & 3;
+    uint32_t qb[16][2], qa[16][2];
+#pragma unroll
+    for (int s2 = 0; s2 < 16; ++s2) {
+        uint32_t w = 0;
+        if (r < G) w = __ldg(reinterpret_cast<const uint32_t*>(qb16 + (size_t)r * kHeadDim + 8 * s2 + 2 * c));
+        const uint32_t neg = ((w & 0x8000u) ? 0x0000FFFFu : 0u) | ((w & 0x80000000u) ? 0xFFFF0000u : 0u);
+        qb[s2][0] = w & neg;
+        qb[s2][1] = w & ~neg;
+        qa[s2][0] = qb[s2][0] & 0x7FFF7FFFu;
+        qa[s2][1] = qb[s2][1] & 0x7FFF7FFFu;
+    }
+    __syncthreads();
+
+    // ---- 1. tile phase (as block_select_tc_kernel) ----
+    const int my_tiles = ntiles > warp ? (ntiles - warp + kTcWarps - 1) / kTcWarps : 0;
+    auto issue = [&](int i) {
+        if (lane == 0 && i < my_tiles) {
+            const int st = i % NS;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bars[warp * NS + st], kTileBytes);
+            bulk_g2s(stage_base + (size_t)(warp * NS + st) * kTileBytes,
+                     meta_pair + (size_t)(j0 / 32 + warp + i * kTcWarps) * kTileBytes, kTileBytes,
+                     &bars[warp * NS + st]);
+        }
+    };
+    uint32_t phases = 0;
+    const int mi = lane >> 3, rr = lane & 7;
+    const uint32_t a_off = (uint32_t)((mi >> 1) * 512 + (8 * (mi & 1) + rr) * 16);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) issue(i);
+    for (int i = 0; i < my_tiles; ++i) {
+        const int st = i % NS, t = warp + i * kTcWarps;
+        mbar_wait(&bars[warp * NS + st], (phases >> st) & 1u);
+        phases ^= 1u << st;
+        const uint32_t sb = smem_u32(stage_base + (size_t)(warp * NS + st) * kTileBytes);
+        float ds[2][4], da[2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) ds[mt][e] = da[mt][e] = 0.f;
+#pragma unroll
+        for (int s2 = 0; s2 < 16; ++s2) {
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                uint32_t af[4];
+                ldsm_x4(sb + s2 * 1024 + mt * 256 + a_off, af);
+                hmma(ds[mt], af, qb[s2][0], qb[s2][1]);
+                af[0] &= 0x7FFF7FFFu;
+                af[1] &= 0x7FFF7FFFu;
+                af[2] &= 0x7FFF7FFFu;
+                af[3] &= 0x7FFF7FFFu;
+                hmma(da[mt], af, qa[s2][0], qa[s2][1]);
+            }
+        }
+        __syncwarp();
+        issue(i + NS);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                float sv = -INFINITY, av = 0.f;
+                int bad = 0;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    if (2 * c + e < G) {
+                        const float dv = ds[mt][2 * half + e], dav = da[mt][2 * half + e];
+                        bad |= !(fabsf(dv) <= 3.0e38f) || !(dav <= 3.0e38f);
+                        sv = fmaxf(sv, dv);
+                        av = fmaxf(av, dav);
+                    }
+                }
+                sv = fmaxf(sv, __shfl_xor_sync(0xffffffffu, sv, 1));
+                sv = fmaxf(sv, __shfl_xor_sync(0xffffffffu, sv, 2));
+                av = fmaxf(av, __shfl_xor_sync(0xffffffffu, av, 1));
+                av = fmaxf(av, __shfl_xor_sync(0xffffffffu, av, 2));
+                bad |= __shfl_xor_sync(0xffffffffu, bad, 1);
+                bad |= __shfl_xor_sync(0xffffffffu, bad, 2);
+                const int jj = t * 32 + 16 * mt + 8 * half + r;
+                if (c == 0 && jj < nb_chunk) {
+                    const float eps = __fmaf_ru(av, 0x1p-10f, 0x1p-100f);
+                    if (bad != 0 || !(eps <= 3.0e38f)) {
+                        lo[jj] = -INFINITY;
+                        hi[jj] = INFINITY;
+                    } else {
+                        lo[jj] = __fsub_rd(sv, eps);
+                        hi[jj] = __fadd_ru(sv, eps);
+                    }
+                }
+            }
+    }
+    __syncthreads();
+    sel_stamp(tr, 1);
+
+    // ---- 2. tau' over the pair (distributed shared memory) ----
+    const int kk = k;  // < nb here
+    // (a) finite-L min / max / count of the CTA -> own xch[0..2]
+    {
+        float mn = INFINITY, mx = -INFINITY;
+        int cnt = 0;
+        for (int i = tid; i < nb_chunk; i += kTcThreads) {
+            const float v = lo[i];
+            if (v != -INFINITY) {
+                mn = fminf(mn, v);
+                mx = fmaxf(mx, v);
+                ++cnt;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        }
+        if (lane == 0) {
+            sw[warp] = __float_as_int(mn);
+            sw[8 + warp] = __float_as_int(mx);
+            sw[16 + warp] = cnt;
+        }
+        __syncthreads();
+        if (tid == 0) {  // (warp 0's values are this thread's)
+            for (int wi = 1; wi < kTcWarps; ++wi) {
+                mn = fminf(mn, __int_as_float(sw[wi]));
+                mx = fmaxf(mx, __int_as_float(sw[8 + wi]));
+                cnt += sw[16 + wi];
+            }
+            xch[0] = (unsigned long long)(uint32_t)__float_as_int(mn);
+            xch[1] = (unsigned long long)(uint32_t)__float_as_int(mx);
+            xch[2] = (unsigned long long)cnt;
+        }
+    }
+    cluster.sync();  // #1: every CTA's (min, max, count) and zeroed histogram visible
+    float Lmin = INFINITY, Lmax = -INFINITY;
+    int nfin = 0;
+    for (int rk = 0; rk < CS; ++rk) {
+        const unsigned long long* rx = cluster.map_shared_rank(xch, rk);
+        Lmin = fminf(Lmin, __int_as_float((int)(uint32_t)rx[0]));
+        Lmax = fmaxf(Lmax, __int_as_float((int)(uint32_t)rx[1]));
+        nfin += (int)rx[2];
+    }
+    float tau = -INFINITY;  // every block a candidate unless k finite L exist
+    if (nfin >= kk) {
+        // (b) linear histogram of the finite L over [Lmin, Lmax]
+        const float scale = Lmax > Lmin ? 256.f / (Lmax - Lmin) : 0.f;
+        auto bin_of = [&](float v) { return min(255, (int)((v - Lmin) * scale)); };
+        for (int i = tid; i < nb_chunk; i += kTcThreads) {
+            const float v = lo[i];
+            if (v != -INFINITY) atomicAdd(&hist[bin_of(v)], 1);
+        }
+        cluster.sync();  // #2
+        // every CTA sums the cluster's histograms (bins tid, tid + 128) and finds b*
+        int tot0 = 0, tot1 = 0;
+        for (int rk = 0; rk < CS; ++rk) {
+            const int* rh = cluster.map_shared_rank(hist, rk);
+            tot0 += rh[tid];
+            tot1 += rh[tid + 128];
+        }
+        cluster.sync();  // #3: remote reads of hist done before it is reused
+        hist[tid] = tot0;
+        hist[tid + 128] = tot1;
+        __syncthreads();
+        if (tid < 32) {
+            int cnt8[8], s8 = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                cnt8[i] = hist[255 - (tid * 8 + i)];
+                s8 += cnt8[i];
+            }
+            const int incl = warp_incl_scan(s8);
+            int above = incl - s8;
+            if (above < kk && kk <= incl) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (above < kk && kk <= above + cnt8[i]) sw[40] = 255 - (tid * 8 + i);
+                    above += cnt8[i];
+                }
+            }
+        }
+        __syncthreads();
+        const int bstar = sw[40];
+        // (c) tau' = a lower edge of bin b*, one bin wide of margin: a key v in
+        // bin b* has fl(fl(v - Lmin) * scale) >= b*, so v >= Lmin + (b* - 1) /
+        // scale whatever the two roundings did (each is relative 2^-24; the
+        // margin is a whole bin), and tau' <= the k-th largest L.  (Taking the
+        // smallest L of bin b* instead cost one more pass and cluster barrier.)
+        tau = bstar >= 1 ? __fsub_rd(Lmin, 0.f) + __fdiv_rd((float)(bstar - 1), scale) : -INFINITY;
+        if (!(tau <= Lmax)) tau = -INFINITY;  // (scale overflowed / NaN: every block a candidate)
+    }
+    sel_stamp(tr, 2);
+
+    // ---- 3. candidates of this chunk (U >= tau'), rescored exactly ----
+    int32_t* jpos = (int32_t*)smem_raw;                    // [<= CH]
+    uint64_t* ckeys = (uint64_t*)(smem_raw + (size_t)CH * 4);
+    int n_cand;
+    {
+        const int per = (nb_chunk + kTcThreads - 1) / kTcThreads;
+        const int p0 = tid * per, p1 = min(nb_chunk, p0 + per);
+        int cnt = 0;
+        for (int p2 = p0; p2 < p1; ++p2) cnt += hi[p2] >= tau;
+        int tot;
+        int o = block_excl_scan<kTcThreads>(cnt, sw, tot);
+        for (int p2 = p0; p2 < p1; ++p2)
+            if (hi[p2] >= tau) jpos[o++] = p2;
+        n_cand = tot;
+    }
+    sel_stamp(tr, 7, (unsigned long long)n_cand);
+    __syncthreads();
+    {
+        unsigned char* cstage = smem_raw + (((size_t)CH * 4 + (size_t)n_cand * 8 + 127) & ~(size_t)127);
+        const int stage_end = region_bytes + 8 * CH;
+        const int batch = max(1, min(kTcThreads, (stage_end - (int)(cstage - smem_raw)) / 512));
+        for (int base = 0; base < n_cand; base += batch) {
+            const int nbt = min(batch, n_cand - base);
+            for (int i = tid; i < nbt * 32; i += kTcThreads) {
+                const int ci2 = i >> 5, pc = i & 31;
+                const int p2 = jpos[base + ci2];
+                const char* src = meta_pair + (size_t)(j0 / 32 + p2 / 32) * kTileBytes + (size_t)pc * 512 + (p2 % 32) * 16;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(cstage + ci2 * 512 + pc * 16)),
+                             "l"(src)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+            __syncthreads();
+            if (tid < nbt) {
+                const uint4* cp = reinterpret_cast<const uint4*>(cstage + tid * 512);
+                double acc[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) acc[g] = 0.0;
+#pragma unroll 4
+                for (int s2 = 0; s2 < 16; ++s2) {
+                    const uint4 wn4 = cp[2 * s2], wx4 = cp[2 * s2 + 1];
+                    const uint32_t wn[4] = {wn4.x, wn4.y, wn4.z, wn4.w};
+                    const uint32_t wx[4] = {wx4.x, wx4.y, wx4.z, wx4.w};
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int w2 = e >> 1, ch = 8 * s2 + e;
+                        const int32_t hN = (e & 1) ? bf16_hi_hiword(wn[w2]) : bf16_lo_hiword(wn[w2]);
+                        const int32_t hM = (e & 1) ? bf16_hi_hiword(wx[w2]) : bf16_lo_hiword(wx[w2]);
+                        const int32_t dd = hM ^ hN;
+#pragma unroll
+                        for (int g = 0; g < G; ++g)
+                            acc[g] = __fma_rn(qs[ch * G + g], __hiloint2double(hN ^ (qf[ch * G + g] & dd), 0), acc[g]);
+                    }
+                }
+                double sc = acc[0];
+#pragma unroll
+                for (int g = 1; g < G; ++g) sc = acc[g] > sc ? acc[g] : sc;
+                ckeys[base + tid] = ord_key(sc + 0.0);
+            }
+            __syncthreads();
+        }
+    }
+    sel_stamp(tr, 3);
+
+    // ---- 4. (local exact top-k) -> the leader's gather area -> exact top-k ----
+    const int n_out = min(n_cand, kk);
+    if (tid == 0) xch[4] = (unsigned long long)n_out;
+    cluster.sync();  // #5: counts visible; every CTA done with its own stage
+    int off = 0, n_all = 0;  // this CTA's offset in the gathered list; its total (read before
+    for (int rk = 0; rk < CS; ++rk) {  // the last barrier: the other CTAs exit after it)
+        const int cr = (int)cluster.map_shared_rank(xch, rk)[4];
+        off += rk < rank ? cr : 0;
+        n_all += cr;
+    }
+    const int gather_off = CH * 12;  // leader region: [positions | keys] of its own candidates below
+    unsigned char* lead = cluster.map_shared_rank(smem_raw, 0);
+    uint64_t* gkey = reinterpret_cast<uint64_t*>(lead + gather_off);
+    int32_t* gj = reinterpret_cast<int32_t*>(lead + gather_off + (size_t)CS * kk * 8);
+    if (n_cand > kk) {
+        cta_topk_t<kTcThreads>(ckeys, n_cand, kk, hist, sw, [&](int o, int pp) {
+            gkey[off + o] = ckeys[pp];
+            gj[off + o] = j0 + jpos[pp];
+        });
+    } else {
+        for (int i = tid; i < n_cand; i += kTcThreads) {
+            gkey[off + i] = ckeys[i];
+            gj[off + i] = j0 + jpos[i];
+        }
+    }
+    sel_stamp(tr, 4);
+    cluster.sync();  // #6: the gathered list complete in the leader
+    if (rank != 0) return;
+    sel_stamp(tr, 5);
+    const uint64_t* lkeys = reinterpret_cast<const uint64_t*>(smem_raw + gather_off);
+    const int32_t* lj = reinterpret_cast<const int32_t*>(smem_raw + gather_off + (size_t)CS * kk * 8);
+    cta_topk_t<kTcThreads>(lkeys, n_all, kk, hist, sw, [&](int o, int pp) { sel_pair[o] = lj[pp]; });
+    sel_stamp(tr, 6);
 }
 
 // Blocks scored per CTA (the chunk): 1024 for MHA (G = 1), 2048 for GQA
@@ -1040,9 +1501,62 @@ static ss_status launch_sel_tc(const void* q, const void* meta, const int32_t* n
     set_carveout(kern);
     kern<<<nchunks * (int)pairs, kTcThreads, smem, stream>>>(q, meta, n_blk, max_blk, k, d.num_q_heads,
                                                               d.num_kv_heads, nchunks, CH, region, rot_mul,
-                                                              knob("SS_SEL_TC_PF", kSelTcPf), sel,
+                                                              knob("SS_SEL_TC_PF", kSelTcPf), knob("SS_SEL_TRACE", 0), sel,
                                                               cand_key, cand_j, tickets);
     SS_LAUNCH_CHECK();
+    return SS_OK;
+}
+
+// Cluster form (block_select_tcc_kernel): CS CTAs per pair (power of two <= 16,
+// chunks <= 4096 blocks), doubled while the launch has fewer than ~0.8 of a wave
+// of CTAs; two tile stages per warp and one CTA per SM when the launch has at
+// most one CTA per SM.  Returns SS_ERR_UNSUPPORTED when the shape does not fit
+// (the caller falls back to the per-chunk form).
+template <int G>
+static ss_status launch_sel_tcc(const void* q, const void* meta, const int32_t* n_blk, int max_blk, int k,
+                                const ss_dims& d, int32_t* sel, cudaStream_t stream) {
+    const int64_t pairs = (int64_t)d.batch * d.num_kv_heads;
+    int CS = 1;
+    while (CS < kTccMaxCluster && (max_blk + CS - 1) / CS > kSelChunkMax) CS *= 2;
+    if ((max_blk + CS - 1) / CS > kSelChunkMax) return SS_ERR_UNSUPPORTED;
+    const int64_t target = (int64_t)2 * num_sms() * 4 / 5;
+    while (CS < kTccMaxCluster && pairs * CS < target && (max_blk + 2 * CS - 1) / (2 * CS) >= 256) CS *= 2;
+    const int CH = ((max_blk + CS - 1) / CS + 31) / 32 * 32;
+    // two stages per warp (one CTA per SM) when the launch has at most one CTA
+    // per SM -- except for 16-CTA clusters, which need 16 SMs of one GPC at one
+    // CTA per SM and did not all fit at once (C3 one request: a second wave of
+    // clusters 32 us late, r02ad)
+    const int ns = (pairs * CS <= num_sms() && CS <= 8) ? 2 : 1;
+    // region: the tile stages; later the candidate positions / keys and the
+    // rescoring stage; in the leader the gathered (key, j) list at CH * 12 --
+    // which must end before hi[] does
+    const int gather_end = CH * 12 + CS * k * 12;
+    const int region = std::max(kTcWarps * ns * kTileBytes, ((gather_end - 8 * CH) + 127) / 128 * 128);
+    const size_t smem = (size_t)region + (size_t)CH * 8 + (size_t)kHeadDim * G * 12 + 256 * 4 + 64 * 4 + 32 * 8 +
+                        (size_t)kTcWarps * ns * 8;
+    if (smem > (size_t)(ns == 1 ? 113 * 1024 : 227 * 1024)) return SS_ERR_UNSUPPORTED;
+    auto kern = ns == 2 ? block_select_tcc_kernel<G, 2> : block_select_tcc_kernel<G, 1>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return SS_ERR_CUDA;
+    if (CS > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        return SS_ERR_CUDA;
+    set_carveout(kern);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(pairs * CS));
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int tr = knob("SS_SEL_TRACE", 0);
+    if (cudaLaunchKernelEx(&cfg, kern, q, meta, n_blk, max_blk, k, (int)d.num_q_heads, (int)d.num_kv_heads, CS, CH,
+                           region, tr, sel) != cudaSuccess)
+        return SS_ERR_CUDA;
     return SS_OK;
 }
 
@@ -1071,9 +1585,17 @@ ss_status launch_block_select(const void* q, const void* meta, const int32_t* n_
     // fp64 rescoring of the candidates (block_select_tc_kernel; SS_SEL_TC=0: the
     // all-fp64 kernel, which also serves calls that ask for every score)
     const bool tc = knob("SS_SEL_TC", 1) != 0 && !mean && dt == SS_BF16 && G > 1 && scores == nullptr;
+    // cluster form of it (block_select_tcc_kernel); SS_SEL_TCC=0: the per-chunk form (debug A/B)
+    const bool tcc = knob("SS_SEL_TCC", 1) != 0;
 #define SS_SEL_CASE(GG)                                                                       \
     case GG:                                                                                  \
-        if (GG > 1 && tc) return launch_sel_tc<(GG > 1 ? GG : 2)>(q, meta, n_blk, max_blk, k, d, sel, ws, stream); \
+        if (GG > 1 && tc) {                                                                   \
+            if (tcc) {                                                                        \
+                const ss_status st_ = launch_sel_tcc<(GG > 1 ? GG : 2)>(q, meta, n_blk, max_blk, k, d, sel, stream); \
+                if (st_ != SS_ERR_UNSUPPORTED) return st_;                                     \
+            }                                                                                 \
+            return launch_sel_tc<(GG > 1 ? GG : 2)>(q, meta, n_blk, max_blk, k, d, sel, ws, stream); \
+        }                                                                                     \
         if (mean)                                                                             \
             return dt == SS_BF16 ? launch_sel_t<true, GG, true, true>(SS_SEL_ARGS)            \
                                  : launch_sel_t<false, GG, true, true>(SS_SEL_ARGS);          \
@@ -1113,7 +1635,19 @@ bool preload_select() {
     ok &= preload_fn(block_select_tc_kernel<2, 1>) && preload_fn(block_select_tc_kernel<2, 2>);
     ok &= preload_fn(block_select_tc_kernel<4, 1>) && preload_fn(block_select_tc_kernel<4, 2>);
     ok &= preload_fn(block_select_tc_kernel<8, 1>) && preload_fn(block_select_tc_kernel<8, 2>);
+    ok &= preload_fn(block_select_tcc_kernel<2, 1>) && preload_fn(block_select_tcc_kernel<2, 2>);
+    ok &= preload_fn(block_select_tcc_kernel<4, 1>) && preload_fn(block_select_tcc_kernel<4, 2>);
+    ok &= preload_fn(block_select_tcc_kernel<8, 1>) && preload_fn(block_select_tcc_kernel<8, 2>);
     return ok;
 }
 
 }  // namespace ss
+
+#ifdef SS_DEBUG_KNOBS
+// debug build only: copy the tensor-core select timeline (8 u64 per CTA, CTAs
+// 0..n_ctas-1) to host memory
+extern "C" int ss_debug_sel_trace(void* host, int n_ctas) {
+    if (n_ctas > 16384) n_ctas = 16384;
+    return cudaMemcpyFromSymbol(host, ss::g_sel_trace, (size_t)n_ctas * 8 * 8) == cudaSuccess ? 0 : 1;
+}
+#endif

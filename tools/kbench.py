@@ -52,6 +52,28 @@ def bench_select(c, iters):
         i[0] += 1
     ms = timeit(f, iters)
     byts = B * Hkv * n * 512 + q.numel() * 2
+    if os.environ.get("SS_SEL_TRACE"):
+        # tensor-core select timeline (debug build): per CTA start / tiles done /
+        # threshold / rescoring / chunk top-k / merge start / merge end, n_cand
+        import ctypes
+        import numpy as np
+        from paper_2509_24626_b200 import _lib
+        lib = _lib.load()
+        torch.cuda.synchronize()
+        buf = np.zeros((16384, 8), dtype=np.uint64)
+        lib.ss_debug_sel_trace(ctypes.c_void_p(buf.ctypes.data), 16384)
+        tr = buf[buf[:, 0] > 0].astype(np.int64)
+        t0 = tr[:, 0].min()
+        qq = lambda x: [round(float(np.quantile(x, v)), 2) for v in (0.0, 0.5, 0.9, 1.0)] if len(x) else None
+        d = lambda i, j, m=None: (tr[m][:, j] - tr[m][:, i]) / 1e3 if m is not None else (tr[:, j] - tr[:, i]) / 1e3
+        mg = tr[:, 5] >= tr[:, 0]
+        mg &= tr[:, 6] >= tr[:, 5]
+        mg &= tr[:, 5] > t0
+        print(json.dumps({"ctas": len(tr), "start_us": qq((tr[:, 0] - t0) / 1e3), "tiles_us": qq(d(0, 1)),
+                          "threshold_us": qq(d(1, 2)), "rescore_us": qq(d(2, 3)), "chunk_topk_us": qq(d(3, 4)),
+                          "n_cand": qq(tr[:, 7]), "chunk_end_us": qq((tr[:, 4] - t0) / 1e3),
+                          "merges": int(mg.sum()), "merge_us": qq(d(5, 6, mg)) if mg.any() else None,
+                          "merge_end_us": qq((tr[mg][:, 6] - t0) / 1e3) if mg.any() else None}))
     return {"kernel": "select", "us": ms * 1e3, "GBps": byts / ms / 1e6, "frac": byts / ms / 1e6 / PEAK}
 
 
