@@ -142,13 +142,16 @@ __device__ int radix_common_prefix(const K* keys, int n, int* hist, K& prefix, K
     return shift;
 }
 
-template <int NT, bool AGG = true, typename Emit>
+// CP: start below the keys' common prefix (the tensor-core selects' merges of
+// fp64 scores that share sign, exponent and leading mantissa bits); the MHA
+// chunk top-k measured ~3 % slower with the extra reduction (r02ad), so off there.
+template <int NT, bool AGG = true, bool CP = false, typename Emit>
 __device__ void cta_topk_t(const uint64_t* keys, int n, int k_sel, int* hist, int* sw, Emit emit) {
     const int tid = threadIdx.x;
     uint64_t prefix = 0, mask = 0;
     int rem = k_sel;
     if (k_sel < n) {
-        const int shift0 = radix_common_prefix<NT>(keys, n, hist, prefix, mask);
+        const int shift0 = CP ? radix_common_prefix<NT>(keys, n, hist, prefix, mask) : 56;
         for (int shift = shift0; shift >= 0; shift -= 8) {
             for (int i = tid; i < 256; i += NT) hist[i] = 0;
             __syncthreads();
@@ -707,13 +710,13 @@ __device__ uint32_t cta_kth_u32(const uint32_t* keys, int n, int kk, int* hist, 
 // debug timeline of the tensor-core select (SS_SEL_TRACE=1): per CTA, globaltimer
 // at start / tile phase done / threshold / rescoring / chunk top-k / merge start /
 // merge end, and the candidate count; read by ss_debug_sel_trace
-__device__ unsigned long long g_sel_trace[16384 * 8];
+__device__ unsigned long long g_sel_trace[16384 * 12];
 #endif
 __device__ __forceinline__ void sel_stamp(int on, int slot, unsigned long long v = 0) {
 #ifdef SS_DEBUG_KNOBS
     if (on && threadIdx.x == 0) {
         if (slot != 7) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
-        if (blockIdx.x < 16384) g_sel_trace[blockIdx.x * 8 + slot] = v;
+        if (blockIdx.x < 16384) g_sel_trace[blockIdx.x * 12 + slot] = v;
     }
 #else
     (void)on, (void)slot, (void)v;
@@ -966,13 +969,13 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
     // ---- exact top-k among the candidates (positions ascending = j ascending) ----
     int32_t* sel_pair = sel + (size_t)pair * k;
     if (nch_b == 1) {
-        cta_topk_t<kTcThreads>(ckeys, n_cand, kk, hist, sw, [&](int o, int pp) { sel_pair[o] = j0 + jpos[pp]; });
+        cta_topk_t<kTcThreads, true, true>(ckeys, n_cand, kk, hist, sw, [&](int o, int pp) { sel_pair[o] = j0 + jpos[pp]; });
         for (int rr2 = kk + tid; rr2 < k; rr2 += kTcThreads) sel_pair[rr2] = -1;
         return;
     }
     uint64_t* ck = cand_key + ((size_t)pair * nchunks + ci) * k;
     int32_t* cj = cand_j + ((size_t)pair * nchunks + ci) * k;
-    cta_topk_t<kTcThreads>(ckeys, n_cand, kk, hist, sw, [&](int o, int pp) {
+    cta_topk_t<kTcThreads, true, true>(ckeys, n_cand, kk, hist, sw, [&](int o, int pp) {
         ck[o] = ckeys[pp];
         cj[o] = j0 + jpos[pp];
     });
@@ -1000,7 +1003,7 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
     }
     __syncthreads();
     const int kf = min(k, nb);
-    cta_topk_t<kTcThreads>(keys, n, kf, hist, sw, [&](int o, int pp) { sel_pair[o] = mjpos[pp]; });
+    cta_topk_t<kTcThreads, true, true>(keys, n, kf, hist, sw, [&](int o, int pp) { sel_pair[o] = mjpos[pp]; });
     for (int rr2 = kf + tid; rr2 < k; rr2 += kTcThreads) sel_pair[rr2] = -1;
     if (tid == 0) tickets[pair] = 0;
     sel_stamp(tr, 6);
@@ -1069,7 +1072,6 @@ block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ met
     }
     const int j0 = ci * CH;
     const int nb_chunk = max(0, min(CH, nb - j0));
-    const int ntiles = (nb_chunk + 31) / 32;
     const char* meta_pair = (const char*)meta + ((size_t)pair * (max_blk / 32)) * kTileBytes;
     const uint16_t* qb16 = (const uint16_t*)q + ((size_t)b * Hq + (size_t)h * G) * kHeadDim;
 
@@ -1099,25 +1101,49 @@ block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ met
     }
     __syncthreads();
 
-    // ---- 1. tile phase (as block_select_tc_kernel) ----
-    const int my_tiles = ntiles > warp ? (ntiles - warp + kTcWarps - 1) / kTcWarps : 0;
-    auto issue = [&](int i) {
-        if (lane == 0 && i < my_tiles) {
-            const int st = i % NS;
+    // ---- 1. tile phase, tiles of the PAIR handed out dynamically ----
+    // (a static split left the cluster's CTAs 7.6 us apart at the end of the
+    // phase -- CTAs sharing an SM stream slower -- and every cluster barrier
+    // waits for the slowest, r02ad).  A warp takes tile t of the pair from a
+    // counter in the leader's shared memory (DSMEM atomic, issued one tile
+    // ahead), and writes its blocks' (L, U) into the OWNER CTA's lo / hi
+    // (t*32 / CH), plus its own running min / max / count of the finite L.
+    int* ctr_local = reinterpret_cast<int*>(&xch[31]);
+    if (tid == 0) *ctr_local = 0;
+    cluster.sync();  // #0: the leader's counter is zero; every CTA resident
+    int* ctr = cluster.map_shared_rank(ctr_local, 0);
+    const int ntiles_pair = (nb + 31) / 32;
+    auto issue = [&](int st, int t) {
+        if (lane == 0 && t < ntiles_pair) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&bars[warp * NS + st], kTileBytes);
-            bulk_g2s(stage_base + (size_t)(warp * NS + st) * kTileBytes,
-                     meta_pair + (size_t)(j0 / 32 + warp + i * kTcWarps) * kTileBytes, kTileBytes,
-                     &bars[warp * NS + st]);
+            bulk_g2s(stage_base + (size_t)(warp * NS + st) * kTileBytes, meta_pair + (size_t)t * kTileBytes,
+                     kTileBytes, &bars[warp * NS + st]);
         }
     };
+    int t_st0 = 0, t_st1 = 0;  // tile held by stage 0 / 1
+    {
+        int t0 = 0;
+        if (lane == 0) t0 = atomicAdd(ctr, 1);
+        t_st0 = __shfl_sync(0xffffffffu, t0, 0);
+        issue(0, t_st0);
+        if (NS == 2) {
+            if (lane == 0) t0 = atomicAdd(ctr, 1);
+            t_st1 = __shfl_sync(0xffffffffu, t0, 0);
+            issue(1, t_st1);
+        }
+    }
+    int pre_raw = 0;  // lane 0: the next tile index, requested one tile ahead
+    if (lane == 0) pre_raw = atomicAdd(ctr, 1);
+    float lmn = INFINITY, lmx = -INFINITY;
+    int lcnt = 0;
     uint32_t phases = 0;
     const int mi = lane >> 3, rr = lane & 7;
     const uint32_t a_off = (uint32_t)((mi >> 1) * 512 + (8 * (mi & 1) + rr) * 16);
-#pragma unroll
-    for (int i = 0; i < NS; ++i) issue(i);
-    for (int i = 0; i < my_tiles; ++i) {
-        const int st = i % NS, t = warp + i * kTcWarps;
+    for (int i = 0;; ++i) {
+        const int st = NS == 2 ? (i & 1) : 0;
+        const int t = st ? t_st1 : t_st0;
+        if (t >= ntiles_pair) break;  // later grabs are larger: nothing left for this warp
         mbar_wait(&bars[warp * NS + st], (phases >> st) & 1u);
         phases ^= 1u << st;
         const uint32_t sb = smem_u32(stage_base + (size_t)(warp * NS + st) * kTileBytes);
@@ -1141,7 +1167,16 @@ block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ met
             }
         }
         __syncwarp();
-        issue(i + NS);
+        {   // the stage is consumed: the pre-requested tile into it, request the next
+            const int tn = __shfl_sync(0xffffffffu, pre_raw, 0);
+            if (st) t_st1 = tn; else t_st0 = tn;
+            issue(st, tn);
+            if (lane == 0 && tn < ntiles_pair) pre_raw = atomicAdd(ctr, 1);
+        }
+        const int owner = t * 32 / CH;
+        float* lo_o = cluster.map_shared_rank(lo, owner);
+        float* hi_o = cluster.map_shared_rank(hi, owner);
+        const int jbase = t * 32 - owner * CH;
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -1163,36 +1198,31 @@ block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ met
                 av = fmaxf(av, __shfl_xor_sync(0xffffffffu, av, 2));
                 bad |= __shfl_xor_sync(0xffffffffu, bad, 1);
                 bad |= __shfl_xor_sync(0xffffffffu, bad, 2);
-                const int jj = t * 32 + 16 * mt + 8 * half + r;
-                if (c == 0 && jj < nb_chunk) {
+                const int rel = 16 * mt + 8 * half + r;
+                if (c == 0 && t * 32 + rel < nb) {
                     const float eps = __fmaf_ru(av, 0x1p-10f, 0x1p-100f);
                     if (bad != 0 || !(eps <= 3.0e38f)) {
-                        lo[jj] = -INFINITY;
-                        hi[jj] = INFINITY;
+                        lo_o[jbase + rel] = -INFINITY;
+                        hi_o[jbase + rel] = INFINITY;
                     } else {
-                        lo[jj] = __fsub_rd(sv, eps);
-                        hi[jj] = __fadd_ru(sv, eps);
+                        const float lv = __fsub_rd(sv, eps);
+                        lo_o[jbase + rel] = lv;
+                        hi_o[jbase + rel] = __fadd_ru(sv, eps);
+                        lmn = fminf(lmn, lv);
+                        lmx = fmaxf(lmx, lv);
+                        ++lcnt;
                     }
                 }
             }
     }
-    __syncthreads();
     sel_stamp(tr, 1);
 
     // ---- 2. tau' over the pair (distributed shared memory) ----
     const int kk = k;  // < nb here
-    // (a) finite-L min / max / count of the CTA -> own xch[0..2]
+    // (a) finite-L min / max / count of the L this CTA computed -> own xch[0..2]
     {
-        float mn = INFINITY, mx = -INFINITY;
-        int cnt = 0;
-        for (int i = tid; i < nb_chunk; i += kTcThreads) {
-            const float v = lo[i];
-            if (v != -INFINITY) {
-                mn = fminf(mn, v);
-                mx = fmaxf(mx, v);
-                ++cnt;
-            }
-        }
+        float mn = lmn, mx = lmx;
+        int cnt = lcnt;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -1216,7 +1246,7 @@ block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ met
             xch[2] = (unsigned long long)cnt;
         }
     }
-    cluster.sync();  // #1: every CTA's (min, max, count) and zeroed histogram visible
+    cluster.sync();  // #1: every lo / hi complete; every CTA's (min, max, count) visible
     float Lmin = INFINITY, Lmax = -INFINITY;
     int nfin = 0;
     for (int rk = 0; rk < CS; ++rk) {
@@ -1308,6 +1338,7 @@ block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ met
             }
             asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
             __syncthreads();
+            if (base == 0) sel_stamp(tr, 8);
             if (tid < nbt) {
                 const uint4* cp = reinterpret_cast<const uint4*>(cstage + tid * 512);
                 double acc[G];
@@ -1354,7 +1385,7 @@ block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ met
     uint64_t* gkey = reinterpret_cast<uint64_t*>(lead + gather_off);
     int32_t* gj = reinterpret_cast<int32_t*>(lead + gather_off + (size_t)CS * kk * 8);
     if (n_cand > kk) {
-        cta_topk_t<kTcThreads>(ckeys, n_cand, kk, hist, sw, [&](int o, int pp) {
+        cta_topk_t<kTcThreads, true, true>(ckeys, n_cand, kk, hist, sw, [&](int o, int pp) {
             gkey[off + o] = ckeys[pp];
             gj[off + o] = j0 + jpos[pp];
         });
@@ -1370,7 +1401,7 @@ block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ met
     sel_stamp(tr, 5);
     const uint64_t* lkeys = reinterpret_cast<const uint64_t*>(smem_raw + gather_off);
     const int32_t* lj = reinterpret_cast<const int32_t*>(smem_raw + gather_off + (size_t)CS * kk * 8);
-    cta_topk_t<kTcThreads>(lkeys, n_all, kk, hist, sw, [&](int o, int pp) { sel_pair[o] = lj[pp]; });
+    cta_topk_t<kTcThreads, true, true>(lkeys, n_all, kk, hist, sw, [&](int o, int pp) { sel_pair[o] = lj[pp]; });
     sel_stamp(tr, 6);
 }
 
@@ -1648,6 +1679,6 @@ bool preload_select() {
 // 0..n_ctas-1) to host memory
 extern "C" int ss_debug_sel_trace(void* host, int n_ctas) {
     if (n_ctas > 16384) n_ctas = 16384;
-    return cudaMemcpyFromSymbol(host, ss::g_sel_trace, (size_t)n_ctas * 8 * 8) == cudaSuccess ? 0 : 1;
+    return cudaMemcpyFromSymbol(host, ss::g_sel_trace, (size_t)n_ctas * 12 * 8) == cudaSuccess ? 0 : 1;
 }
 #endif

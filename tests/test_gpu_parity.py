@@ -185,6 +185,22 @@ def test_select_gqa_extreme_magnitudes(ops, scale_q, scale_k):
     _select_sel_only(ops, q, blocks, B, Hkv * G, Hkv, [n], 32)
 
 
+@pytest.mark.parametrize("G", [2, 4])
+def test_select_gqa_cluster_shapes(ops, G):
+    """The cluster form of the tensor-core select (block_select_tcc_kernel):
+    two pairs of 8192 blocks -> 16-CTA clusters of 512-block chunks; request 1
+    has 700 blocks, so 14 of its CTAs own no block and still join every cluster
+    barrier; request 0 is a copy of ONE block (every L equal: a degenerate
+    histogram, every block a candidate, local top-k before the gather)."""
+    rng = synth.rng_for(1000, 9, G)
+    B, Hkv, max_blk = 2, 1, 8192
+    blocks = synth.kv_blocks(rng, B * Hkv * max_blk, D, synth.channel_scales(rng))
+    blocks[:max_blk] = blocks[5]
+    q = rng.standard_normal((B, Hkv * G, D)).astype(np.float32)
+    for k in (1, 128):
+        _select_sel_only(ops, q, blocks, B, Hkv * G, Hkv, [max_blk, 700], k)
+
+
 def test_select_needles_selected(ops):
     sel = _select_case(ops, synth.DT_BF16, 2, 8, 8, [700, 64], 4, seed=30, needle=True)
     assert (sel[:, :, 0] >= 0).all()

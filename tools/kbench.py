@@ -60,7 +60,7 @@ def bench_select(c, iters):
         from paper_2509_24626_b200 import _lib
         lib = _lib.load()
         torch.cuda.synchronize()
-        buf = np.zeros((16384, 8), dtype=np.uint64)
+        buf = np.zeros((16384, 12), dtype=np.uint64)
         lib.ss_debug_sel_trace(ctypes.c_void_p(buf.ctypes.data), 16384)
         tr = buf[buf[:, 0] > 0].astype(np.int64)
         t0 = tr[:, 0].min()
@@ -70,7 +70,8 @@ def bench_select(c, iters):
         mg &= tr[:, 6] >= tr[:, 5]
         mg &= tr[:, 5] > t0
         print(json.dumps({"ctas": len(tr), "start_us": qq((tr[:, 0] - t0) / 1e3), "tiles_us": qq(d(0, 1)),
-                          "threshold_us": qq(d(1, 2)), "rescore_us": qq(d(2, 3)), "chunk_topk_us": qq(d(3, 4)),
+                          "threshold_us": qq(d(1, 2)), "rescore_us": qq(d(2, 3)),
+                          "rescore_data_wait_us": qq(d(2, 8, tr[:, 8] >= tr[:, 2])), "rescore_compute_us": qq(d(8, 3, tr[:, 8] >= tr[:, 2])), "chunk_topk_us": qq(d(3, 4)),
                           "n_cand": qq(tr[:, 7]), "chunk_end_us": qq((tr[:, 4] - t0) / 1e3),
                           "merges": int(mg.sum()), "merge_us": qq(d(5, 6, mg)) if mg.any() else None,
                           "merge_end_us": qq((tr[mg][:, 6] - t0) / 1e3) if mg.any() else None}))
