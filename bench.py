@@ -1050,7 +1050,11 @@ def main():
     ap.add_argument("--no-gather-alone", action="store_true",
                     help="skip the FlashH2D-alone ceiling measurement (profiling runs: keeps launch counts fixed)")
     args = ap.parse_args()
-    assert args.warmup >= 3, "W >= 3 warm-up steps"
+    if args.warmup < 3:
+        # the timing rules ask for W >= 3 untimed warm-up steps: a smaller W (e.g.
+        # a profiling command's --warmup 1) runs 3, and the JSON line reports 3
+        print(f"bench.py: --warmup {args.warmup} < 3; running 3 warm-up steps", file=sys.stderr)
+        args.warmup = 3
     if args.impl == "reference":
         # under torchrun (N > 1) rank 0 alone times the oracle; the other ranks exit
         if int(os.environ.get("RANK", "0")) == 0:
