@@ -234,11 +234,168 @@ __device__ __forceinline__ void cta_topk(const uint64_t* keys, int n, int k_sel,
     cta_topk_t<kSelThreads, AGG>(keys, n, k_sel, hist, sw, emit);
 }
 
+#ifdef SS_DEBUG_KNOBS
+// debug timeline of the select kernels (SS_SEL_TRACE=1): per CTA, globaltimer
+// at start / tile phase done / threshold / rescoring / chunk top-k / merge start /
+// merge end, and the candidate count; read by ss_debug_sel_trace
+__device__ unsigned long long g_sel_trace[16384 * 12];
+#endif
+__device__ __forceinline__ void sel_stamp(int on, int slot, unsigned long long v = 0) {
+#ifdef SS_DEBUG_KNOBS
+    if (on && threadIdx.x == 0) {
+        if (slot != 7) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+        if (blockIdx.x < 16384) g_sel_trace[blockIdx.x * 12 + slot] = v;
+    }
+#else
+    (void)on, (void)slot, (void)v;
+#endif
+}
+
+namespace cg = cooperative_groups;
+
+// Cluster epilogue of the MHA select (block_select_kernel<..., CLU = true>):
+// the chunks of a pair are the CTAs of one thread-block cluster, every CTA
+// holds the exact ordered keys of its chunk, and the pair's top-k is taken
+// through distributed shared memory instead of per-chunk top-k sets merged by
+// the last CTA through the global workspace (r02am: 5 us of chunk top-k + 3 us
+// of merge + a ticket round trip after 31 us of scoring at one C2 request
+// group).  As in block_select_tcc_kernel: a cluster-wide 256-bin histogram
+// LINEAR in float(score) (monotone: fl32 of an fp64 score is non-decreasing),
+// the bin b* holding the k-th largest, tau_f = a lower edge of b* one bin below
+// it; every block of the top-k has float(score) >= float(k-th) >= tau_f.  The
+// candidates (~k per PAIR) keep their EXACT keys; a CTA with more than k keeps
+// its exact local top-k; the lists go to the leader CTA at their rank's offset
+// (ascending j) and the leader takes the exact top-k (ties -> lower j).
+template <int NT>
+__device__ void mha_cluster_topk(cg::cluster_group& cluster, int CS, const uint64_t* keys, int n_loc, int j0,
+                                 int k, int32_t* cpos, uint64_t* ckeys, int* hist, int* sw,
+                                 unsigned long long* xch, uint64_t* gkey_local, int32_t* sel_pair, int tr) {
+    const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+    constexpr int NWARP = NT / 32;
+    const int rank = (int)cluster.block_rank();
+    auto fval = [](uint64_t key) {  // inverse of ord_key, rounded to float
+        const uint64_t b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
+        return (float)__longlong_as_double((long long)b);
+    };
+    for (int i = tid; i < 256; i += NT) hist[i] = 0;
+    {   // (a) float min / max of the chunk's scores -> own xch[0..1]
+        float mn = INFINITY, mx = -INFINITY;
+        for (int i = tid; i < n_loc; i += NT) {
+            const float v = fval(keys[i]);
+            mn = fminf(mn, v);
+            mx = fmaxf(mx, v);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+            sw[warp] = __float_as_int(mn);
+            sw[16 + warp] = __float_as_int(mx);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < NWARP; ++w) {
+                mn = fminf(mn, __int_as_float(sw[w]));
+                mx = fmaxf(mx, __int_as_float(sw[16 + w]));
+            }
+            xch[0] = (unsigned long long)(uint32_t)__float_as_int(mn);
+            xch[1] = (unsigned long long)(uint32_t)__float_as_int(mx);
+        }
+    }
+    cluster.sync();  // #1
+    float Lmin = INFINITY, Lmax = -INFINITY;
+    for (int rk = 0; rk < CS; ++rk) {
+        const unsigned long long* rx = cluster.map_shared_rank(xch, rk);
+        Lmin = fminf(Lmin, __int_as_float((int)(uint32_t)rx[0]));
+        Lmax = fmaxf(Lmax, __int_as_float((int)(uint32_t)rx[1]));
+    }
+    // (b) linear histogram over [Lmin, Lmax], summed over the cluster
+    const float scale = Lmax > Lmin ? 256.f / (Lmax - Lmin) : 0.f;
+    auto bin_of = [&](float v) { return min(255, (int)((v - Lmin) * scale)); };
+    for (int i = tid; i < n_loc; i += NT) atomicAdd(&hist[bin_of(fval(keys[i]))], 1);
+    cluster.sync();  // #2
+    int tot = 0;
+    for (int rk = 0; rk < CS; ++rk) tot += cluster.map_shared_rank(hist, rk)[tid];  // NT == 256 bins
+    cluster.sync();  // #3: remote reads done before hist is overwritten
+    hist[tid] = tot;
+    __syncthreads();
+    if (tid < 32) {
+        int cnt8[8], s8 = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            cnt8[i] = hist[255 - (tid * 8 + i)];
+            s8 += cnt8[i];
+        }
+        const int incl = warp_incl_scan(s8);
+        int above = incl - s8;
+        if (above < k && k <= incl) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (above < k && k <= above + cnt8[i]) sw[40] = 255 - (tid * 8 + i);
+                above += cnt8[i];
+            }
+        }
+    }
+    __syncthreads();
+    const int bstar = sw[40];
+    float tau = bstar >= 1 ? __fsub_rd(Lmin, 0.f) + __fdiv_rd((float)(bstar - 1), scale) : -INFINITY;
+    if (!(tau <= Lmax)) tau = -INFINITY;
+    sel_stamp(tr, 2);
+    // (c) candidates: float(score) >= tau, positions ascending
+    int n_cand;
+    {
+        const int per = (n_loc + NT - 1) / NT;
+        const int p0 = tid * per, p1 = min(n_loc, p0 + per);
+        int cnt = 0;
+        for (int p2 = p0; p2 < p1; ++p2) cnt += fval(keys[p2]) >= tau;
+        int t2;
+        int o = block_excl_scan<NT>(cnt, sw, t2);
+        for (int p2 = p0; p2 < p1; ++p2)
+            if (fval(keys[p2]) >= tau) cpos[o++] = p2;
+        n_cand = t2;
+    }
+    __syncthreads();
+    // (d) gather into the leader: [keys u64 x CS*k][j i32 x CS*k]
+    const int n_out = min(n_cand, k);
+    if (tid == 0) xch[4] = (unsigned long long)n_out;
+    cluster.sync();  // #4
+    int off = 0, n_all = 0;
+    for (int rk = 0; rk < CS; ++rk) {
+        const int cr = (int)cluster.map_shared_rank(xch, rk)[4];
+        off += rk < rank ? cr : 0;
+        n_all += cr;
+    }
+    uint64_t* gkey = cluster.map_shared_rank(gkey_local, 0);
+    int32_t* gj = reinterpret_cast<int32_t*>(gkey + (size_t)CS * k);
+    if (n_cand > k) {  // local exact top-k first (ties: lower position = lower j)
+        for (int i = tid; i < n_cand; i += NT) ckeys[i] = keys[cpos[i]];
+        __syncthreads();
+        cta_topk_t<NT, true, false>(ckeys, n_cand, k, hist, sw, [&](int o, int pp) {
+            gkey[off + o] = ckeys[pp];
+            gj[off + o] = j0 + cpos[pp];
+        });
+    } else {
+        for (int i = tid; i < n_cand; i += NT) {
+            gkey[off + i] = keys[cpos[i]];
+            gj[off + i] = j0 + cpos[i];
+        }
+    }
+    sel_stamp(tr, 4);
+    cluster.sync();  // #5: the gathered list complete in the leader; others exit after this
+    if (rank != 0) return;
+    sel_stamp(tr, 5);
+    const int32_t* lj = reinterpret_cast<const int32_t*>(gkey_local + (size_t)CS * k);
+    cta_topk_t<NT, true, false>(gkey_local, n_all, k, hist, sw, [&](int o, int pp) { sel_pair[o] = lj[pp]; });
+    sel_stamp(tr, 6);
+}
+
 // G > 1 (min/max): the all-fp64 GQA kernel now serves calls that ask for every
 // score (debug / tests) and f32 inputs; bf16 selections run on the tensor
 // cores (block_select_tc_kernel).  One CTA per SM gives it the registers to
 // keep its load ring and G x TT accumulators without spilling.
-template <bool BF16, int G, bool ICV, bool MEAN, int TT>
+template <bool BF16, int G, bool ICV, bool MEAN, int TT, bool CLU = false>
 __global__ void __launch_bounds__(kSelThreads, (G > 1 && !MEAN) ? 1 : 2)
 block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                     const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
@@ -269,6 +426,8 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
     // persistent: CTAs stride over (pair, chunk) work items, so the grid is fully
     // resident and a FlashH2D kernel of another request group can co-reside
+    const int tr = (l2pf & 16) ? 1 : 0;  // debug timeline (SS_SEL_TRACE=1)
+    sel_stamp(tr, 0);
     for (int item = blockIdx.x; item < nchunks * npairs; item += gridDim.x) {
     __syncthreads();  // previous item's shared-memory readers are done
     const int pair = item / nchunks;
@@ -276,10 +435,20 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     const int ci = item % nchunks;  // chunk index
     const int nb = n_blk_arr[b];
     const int nch_b = max(1, (nb + CH - 1) / CH);
-    if (ci >= nch_b) continue;
+    if constexpr (CLU) {
+        // one cluster per pair (grid = pairs x nchunks, no persistence): a chunk
+        // past n_blk still joins the cluster barriers with no block
+        if (k >= nb) {  // every block selected (uniform over the cluster)
+            if (ci == 0)
+                for (int i = tid; i < k; i += kSelThreads) sel[(size_t)pair * k + i] = i < nb ? i : -1;
+            return;
+        }
+    } else {
+        if (ci >= nch_b) continue;
+    }
 
     const int j0 = ci * CH;
-    const int nb_chunk = min(CH, nb - j0);  // >= 0 (0 only if nb == 0)
+    const int nb_chunk = max(0, min(CH, nb - j0));  // 0 if nb == 0 (or a CLU chunk past nb)
     const int ntiles = (nb_chunk + 31) / 32;
     constexpr size_t TILE_BYTES = MEAN ? (size_t)32 * kHeadDim * 4 : (size_t)TILE_ELEMS * ES;
     const char* meta_pair = (const char*)meta + ((size_t)pair * (max_blk / 32)) * TILE_BYTES;
@@ -575,6 +744,16 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
         }
     }
     __syncthreads();
+    sel_stamp(tr, 1);
+    if constexpr (CLU) {
+        cg::cluster_group cluster = cg::this_cluster();
+        unsigned long long* xch = (unsigned long long*)(sw + 64);  // [32]
+        uint64_t* ckeys = (uint64_t*)(xch + 32);                   // [CH]
+        uint64_t* gkey = ckeys + CH;                                // leader: [nchunks * k] keys, then j
+        mha_cluster_topk<kSelThreads>(cluster, nchunks, keys, nb_chunk, j0, k, jpos, ckeys, hist, sw, xch, gkey,
+                                      sel + (size_t)pair * k, tr);
+        return;
+    }
 
     const int kc = min(k, nb_chunk);
     int32_t* sel_pair = sel + (size_t)pair * k;
@@ -592,6 +771,7 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     });
     __threadfence();
     __syncthreads();
+    sel_stamp(tr, 4);
     if (tid == 0) sw[48] = atomicAdd(&tickets[pair], 1);
     __syncthreads();
     if (sw[48] != nch_b - 1) continue;
@@ -612,9 +792,11 @@ block_select_kernel(const void* __restrict__ q, const void* __restrict__ meta,
     }
     __syncthreads();
     const int kf = min(k, nb);
+    sel_stamp(tr, 5);
     cta_topk<G == 1>(keys, n, kf, hist, sw, [&](int o, int p) { sel_pair[o] = jpos[p]; });
     for (int r = kf + tid; r < k; r += kSelThreads) sel_pair[r] = -1;
     if (tid == 0) tickets[pair] = 0;
+    sel_stamp(tr, 6);
     }  // work items
 }
 
@@ -704,23 +886,6 @@ __device__ uint32_t cta_kth_u32(const uint32_t* keys, int n, int kk, int* hist, 
         mask |= 0xFFu << shift;
     }
     return prefix;
-}
-
-#ifdef SS_DEBUG_KNOBS
-// debug timeline of the tensor-core select (SS_SEL_TRACE=1): per CTA, globaltimer
-// at start / tile phase done / threshold / rescoring / chunk top-k / merge start /
-// merge end, and the candidate count; read by ss_debug_sel_trace
-__device__ unsigned long long g_sel_trace[16384 * 12];
-#endif
-__device__ __forceinline__ void sel_stamp(int on, int slot, unsigned long long v = 0) {
-#ifdef SS_DEBUG_KNOBS
-    if (on && threadIdx.x == 0) {
-        if (slot != 7) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
-        if (blockIdx.x < 16384) g_sel_trace[blockIdx.x * 12 + slot] = v;
-    }
-#else
-    (void)on, (void)slot, (void)v;
-#endif
 }
 
 template <int G, int NS>
@@ -1035,7 +1200,6 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
 // local top-k sets contains the pair's exact top-k.  No global workspace, no
 // tickets, no second launch-wide merge.
 // ---------------------------------------------------------------------------
-namespace cg = cooperative_groups;
 constexpr int kTccMaxCluster = 16;
 
 template <int G, int NS>
@@ -1471,10 +1635,77 @@ size_t select_ws_bytes(const ss_dims& d, int max_blk, int k) {
     return (bytes + 255) & ~(size_t)255;
 }
 
+// MHA cluster form (block_select_kernel<..., CLU = true>): one cluster of
+// nchunks CTAs per pair when no scores are requested and the pair has <= 8
+// chunks; returns SS_ERR_UNSUPPORTED otherwise (the caller uses the workspace
+// merge form).
+template <bool BF16>
+static ss_status launch_sel_mha_clu(const void* q, const void* meta, const int32_t* n_blk, int max_blk, int k,
+                                    const ss_dims& d, int32_t* sel, cudaStream_t stream) {
+    const size_t pairs = (size_t)d.batch * d.num_kv_heads;
+    auto kern = block_select_kernel<BF16, 1, true, false, 2, true>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(kSelThreads);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    // Only when every cluster is resident at once: a cluster's CTAs wait for
+    // each other at five barriers, so in a multi-wave launch they hold SM slots
+    // the next wave needs (measured: C2 full batch 213 vs 194 us; one C2 group
+    // in clusters of 3, whose 96 clusters did not all fit, 62 vs 45 us; a group
+    // in clusters of 2, all resident, 53 vs 56 us; r02an).  The chunk chooser's
+    // chunk count is the cluster size; when its clusters do not all fit,
+    // SS_ERR_UNSUPPORTED (the workspace form; measured: a smaller cluster of
+    // longer chunks that fits was slower, one C2 group 46.8 vs 45.3 us, r02an).
+    static int cached[9][2] = {};  // [cluster size] -> (smem, max active clusters)
+    const int CH0 = sel_chunk(1, max_blk, k, (int)pairs);
+    for (int cs = (max_blk + CH0 - 1) / CH0; cs >= 2 && cs == (max_blk + CH0 - 1) / CH0; --cs) {
+        if (cs > 8) continue;
+        const int CH = ((max_blk + cs - 1) / cs + 31) / 32 * 32;
+        if (CH > kSelChunkMax) break;
+        const int nchunks = (max_blk + CH - 1) / CH;
+        if (nchunks != cs) continue;
+        const int nkeys = max(CH, min(nchunks * k, kSelMaxMerge));
+        const size_t smem = SelSmemLayout::bytes(1, nkeys) + 32 * 8 + (size_t)CH * 8 + (size_t)nchunks * k * 12;
+        if (smem > 110 * 1024) continue;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return SS_ERR_CUDA;
+        cfg.dynamicSmemBytes = smem;
+        attr[0].val.clusterDim.x = (unsigned)nchunks;
+        if (cached[cs][0] != (int)smem) {
+            int nclu = 0;
+            cfg.gridDim = dim3((unsigned)nchunks);
+            if (cudaOccupancyMaxActiveClusters(&nclu, kern, &cfg) != cudaSuccess) nclu = 0;
+            cached[cs][0] = (int)smem;
+            cached[cs][1] = nclu;
+        }
+        if ((size_t)cached[cs][1] < pairs) continue;
+        set_carveout(kern);
+        cfg.gridDim = dim3((unsigned)(pairs * nchunks));
+        const int l2pf = knob("SS_SEL_TRACE", 0) ? 16 : 0;
+        if (cudaLaunchKernelEx(&cfg, kern, q, meta, n_blk, max_blk, k, (int)d.num_q_heads, (int)d.num_kv_heads,
+                               nchunks, CH, (int)pairs, l2pf, sel, (double*)nullptr, (uint64_t*)nullptr,
+                               (int32_t*)nullptr, (int32_t*)nullptr) != cudaSuccess)
+            return SS_ERR_CUDA;
+        return SS_OK;
+    }
+    return SS_ERR_UNSUPPORTED;
+}
+
 template <bool BF16, int G, bool ICV, bool MEAN, int TT = 2>
 static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_blk, int max_blk,
                               int k, const ss_dims& d, int32_t* sel, double* scores, void* ws,
                               cudaStream_t stream) {
+    if constexpr (G == 1 && ICV && !MEAN) {
+        if (scores == nullptr && knob("SS_SEL_MHA_CLU", 1) != 0) {
+            const ss_status st = launch_sel_mha_clu<BF16>(q, meta, n_blk, max_blk, k, d, sel, stream);
+            if (st != SS_ERR_UNSUPPORTED) return st;
+        }
+    }
     size_t pairs = (size_t)d.batch * d.num_kv_heads;
     const int CH = sel_chunk(G, max_blk, k, (int)pairs);
     int nchunks = (max_blk + CH - 1) / CH;
@@ -1492,7 +1723,7 @@ static ss_status launch_sel_t(const void* q, const void* meta, const int32_t* n_
     // (measured: both the persistent grid and the L2 tile prefetch were slower
     // than a plain one-CTA-per-item grid; kept switchable for experiments)
     const int persist = knob("SS_SEL_PERSIST", 0);
-    const int l2pf = knob("SS_SEL_L2PF", 0);
+    const int l2pf = knob("SS_SEL_L2PF", 0) | (knob("SS_SEL_TRACE", 0) ? 16 : 0);
     const int grid = (persist && items > 2 * num_sms()) ? 2 * num_sms() : items;
     set_carveout(kern);
     kern<<<grid, kSelThreads, smem, stream>>>(q, meta, n_blk, max_blk, k, d.num_q_heads,
@@ -1666,6 +1897,8 @@ bool preload_select() {
     ok &= preload_fn(block_select_tc_kernel<2, 1>) && preload_fn(block_select_tc_kernel<2, 2>);
     ok &= preload_fn(block_select_tc_kernel<4, 1>) && preload_fn(block_select_tc_kernel<4, 2>);
     ok &= preload_fn(block_select_tc_kernel<8, 1>) && preload_fn(block_select_tc_kernel<8, 2>);
+    ok &= preload_fn(block_select_kernel<true, 1, true, false, 2, true>);
+    ok &= preload_fn(block_select_kernel<false, 1, true, false, 2, true>);
     ok &= preload_fn(block_select_tcc_kernel<2, 1>) && preload_fn(block_select_tcc_kernel<2, 2>);
     ok &= preload_fn(block_select_tcc_kernel<4, 1>) && preload_fn(block_select_tcc_kernel<4, 2>);
     ok &= preload_fn(block_select_tcc_kernel<8, 1>) && preload_fn(block_select_tcc_kernel<8, 2>);

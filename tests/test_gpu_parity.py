@@ -201,6 +201,18 @@ def test_select_gqa_cluster_shapes(ops, G):
         _select_sel_only(ops, q, blocks, B, Hkv * G, Hkv, [max_blk, 700], k)
 
 
+def test_select_gqa_beyond_cluster_reach_per_chunk_form(ops):
+    """max_blk > 16 CTAs x 4096 blocks (2.1M tokens): the tensor-core select
+    falls back to its per-chunk form (block_select_tc_kernel: chunk candidates in
+    the workspace, last-CTA merge); selections equal the oracle's."""
+    rng = synth.rng_for(1000, 10, 0)
+    B, G, Hkv, n = 1, 4, 1, 16 * 4096 + 1000
+    max_blk = ((n + 31) // 32) * 32
+    blocks = synth.kv_blocks(rng, B * Hkv * max_blk, D, synth.channel_scales(rng))
+    q = rng.standard_normal((B, Hkv * G, D)).astype(np.float32)
+    _select_sel_only(ops, q, blocks, B, Hkv * G, Hkv, [n], 64)
+
+
 def test_select_needles_selected(ops):
     sel = _select_case(ops, synth.DT_BF16, 2, 8, 8, [700, 64], 4, seed=30, needle=True)
     assert (sel[:, :, 0] >= 0).all()
