@@ -87,6 +87,44 @@ __device__ __forceinline__ double f32_scaled(uint32_t x) {
     return __hiloint2double(((int32_t)x >> 3) & (int32_t)0x8FFFFFFF, (int32_t)(x << 29));
 }
 
+// Ordered compaction: the positions p in [0, n) with pred(p), ascending, into
+// out[]; returns their count.  Each warp owns a contiguous range and walks it
+// 32 consecutive positions at a time (ballot + popc ranks): conflict-free
+// shared-memory reads.  (The per-thread contiguous ranges it replaces read with
+// a stride of n / NT words -- a 32-way bank conflict at 4096 positions: 8.9 us
+// of the C3 select's epilogue, r02ah.)  Contains __syncthreads().
+template <int NT, typename Pred>
+__device__ int cta_compact(int n, int* sw, int32_t* out, Pred pred) {
+    constexpr int NWARP = NT / 32;
+    const int lane = lane_id(), w = warp_id();
+    const int per_w = ((n + NWARP - 1) / NWARP + 31) / 32 * 32;
+    const int a = min(n, w * per_w), b = min(n, a + per_w);
+    int cnt = 0;
+    for (int base = a; base < b; base += 32) {
+        const int p = base + lane;
+        cnt += __popc(__ballot_sync(0xffffffffu, p < b && pred(p)));
+    }
+    __syncthreads();  // sw may still be read by a previous scan
+    if (lane == 0) sw[w] = cnt;
+    __syncthreads();
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < NWARP; ++i) {
+        const int c = sw[i];
+        off += i < w ? c : 0;
+        tot += c;
+    }
+    for (int base = a; base < b; base += 32) {
+        const int p = base + lane;
+        const bool f = p < b && pred(p);
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (f) out[off + __popc(m & ((1u << lane) - 1u))] = p;
+        off += __popc(m);
+    }
+    __syncthreads();
+    return tot;
+}
+
 // ---------------------------------------------------------------------------
 // CTA-wide top-k over keys[0..n): largest keys, ties -> lower position.
 // Writes the selected positions, ascending, to out_pos (smem or global via
@@ -198,31 +236,55 @@ __device__ void cta_topk_t(const uint64_t* keys, int n, int k_sel, int* hist, in
         prefix = 0;
         rem = n;  // all (every key matches the empty prefix)
     }
-    // Compaction in position order.  Thread t owns positions [t*per, (t+1)*per).
-    const int per = (n + NT - 1) / NT;
-    const int p0 = tid * per, p1 = min(n, p0 + per);
+    // Compaction in position order: each warp owns a contiguous range, walked 32
+    // consecutive positions at a time (ballots; conflict-free shared reads --
+    // per-thread contiguous ranges read with a stride of n / NT, see cta_compact).
+    // Keys equal to the k-th take the remaining rem places in position order.
+    constexpr int NWARP = NT / 32;
+    const int lane = lane_id(), w = warp_id();
+    const int per_w = ((n + NWARP - 1) / NWARP + 31) / 32 * 32;
+    const int a = min(n, w * per_w), b = min(n, a + per_w);
+    const unsigned lt = (1u << lane) - 1u;
     int eq = 0;
-    for (int p = p0; p < p1; ++p) eq += ((keys[p] & mask) == prefix);
-    int tot;
-    int eq_base = block_excl_scan<NT>(eq, sw, tot);
+    for (int base = a; base < b; base += 32) {
+        const int p = base + lane;
+        eq += __popc(__ballot_sync(0xffffffffu, p < b && (keys[p] & mask) == prefix));
+    }
+    __syncthreads();
+    if (lane == 0) sw[w] = eq;
+    __syncthreads();
+    int er0 = 0;
+#pragma unroll
+    for (int i = 0; i < NWARP; ++i) er0 += i < w ? sw[i] : 0;
+    __syncthreads();
     int nsel = 0;
     {
-        int er = eq_base;
-        for (int p = p0; p < p1; ++p) {
-            uint64_t km = keys[p] & mask;
-            bool s = km > prefix || (km == prefix && er < rem);
-            er += (km == prefix);
-            nsel += s;
+        int er = er0;
+        for (int base = a; base < b; base += 32) {
+            const int p = base + lane;
+            const uint64_t km = p < b ? (keys[p] & mask) : 0;
+            const unsigned me = __ballot_sync(0xffffffffu, p < b && km == prefix);
+            const bool s = p < b && (km > prefix || (km == prefix && er + __popc(me & lt) < rem));
+            nsel += __popc(__ballot_sync(0xffffffffu, s));
+            er += __popc(me);
         }
     }
-    int out_base = block_excl_scan<NT>(nsel, sw, tot);
+    if (lane == 0) sw[w] = nsel;
+    __syncthreads();
+    int o = 0;
+#pragma unroll
+    for (int i = 0; i < NWARP; ++i) o += i < w ? sw[i] : 0;
     {
-        int er = eq_base, o = out_base;
-        for (int p = p0; p < p1; ++p) {
-            uint64_t km = keys[p] & mask;
-            bool s = km > prefix || (km == prefix && er < rem);
-            er += (km == prefix);
-            if (s) emit(o++, p);
+        int er = er0;
+        for (int base = a; base < b; base += 32) {
+            const int p = base + lane;
+            const uint64_t km = p < b ? (keys[p] & mask) : 0;
+            const unsigned me = __ballot_sync(0xffffffffu, p < b && km == prefix);
+            const bool s = p < b && (km > prefix || (km == prefix && er + __popc(me & lt) < rem));
+            const unsigned ms = __ballot_sync(0xffffffffu, s);
+            if (s) emit(o + __popc(ms & lt), p);
+            o += __popc(ms);
+            er += __popc(me);
         }
     }
     __syncthreads();
@@ -344,19 +406,7 @@ __device__ void mha_cluster_topk(cg::cluster_group& cluster, int CS, const uint6
     if (!(tau <= Lmax)) tau = -INFINITY;
     sel_stamp(tr, 2);
     // (c) candidates: float(score) >= tau, positions ascending
-    int n_cand;
-    {
-        const int per = (n_loc + NT - 1) / NT;
-        const int p0 = tid * per, p1 = min(n_loc, p0 + per);
-        int cnt = 0;
-        for (int p2 = p0; p2 < p1; ++p2) cnt += fval(keys[p2]) >= tau;
-        int t2;
-        int o = block_excl_scan<NT>(cnt, sw, t2);
-        for (int p2 = p0; p2 < p1; ++p2)
-            if (fval(keys[p2]) >= tau) cpos[o++] = p2;
-        n_cand = t2;
-    }
-    __syncthreads();
+    const int n_cand = cta_compact<NT>(n_loc, sw, cpos, [&](int p2) { return fval(keys[p2]) >= tau; });
     // (d) gather into the leader: [keys u64 x CS*k][j i32 x CS*k]
     const int n_out = min(n_cand, k);
     if (tid == 0) xch[4] = (unsigned long long)n_out;
@@ -1059,18 +1109,7 @@ block_select_tc_kernel(const void* __restrict__ q, const void* __restrict__ meta
     // to the end of hi[] (the region and lo / hi are dead by then)
     int32_t* jpos = (int32_t*)smem_raw;
     uint64_t* ckeys = (uint64_t*)(smem_raw + (size_t)CH * 4);
-    int n_cand;
-    {
-        const int per = (nb_chunk + kTcThreads - 1) / kTcThreads;
-        const int p0 = tid * per, p1 = min(nb_chunk, p0 + per);
-        int cnt = 0;
-        for (int p = p0; p < p1; ++p) cnt += ord32(hi[p]) >= tau;
-        int tot;
-        int o = block_excl_scan<kTcThreads>(cnt, sw, tot);
-        for (int p = p0; p < p1; ++p)
-            if (ord32(hi[p]) >= tau) jpos[o++] = p;
-        n_cand = tot;
-    }
+    const int n_cand = cta_compact<kTcThreads>(nb_chunk, sw, jpos, [&](int p) { return ord32(hi[p]) >= tau; });
     __syncthreads();
     sel_stamp(tr, 2);
     sel_stamp(tr, 7, (unsigned long long)n_cand);
@@ -1206,7 +1245,8 @@ template <int G, int NS>
 __global__ void __launch_bounds__(kTcThreads, NS == 1 ? 2 : 1)
 block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ meta,
                         const int32_t* __restrict__ n_blk_arr, int max_blk, int k, int Hq, int Hkv,
-                        int CS, int CH, int region_bytes, int tr, int32_t* __restrict__ sel) {
+                        int CS, int CH, int region_bytes, int tr, int32_t* __restrict__ sel,
+                        const __grid_constant__ CUtensorMap tm_cand) {
     extern __shared__ __align__(128) unsigned char tc_smem[];
     unsigned char* smem_raw = tc_smem;
     // [region: tile stages | candidate positions, keys, rescoring stage | leader
@@ -1249,6 +1289,7 @@ block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ met
     if (lane == 0) {
 #pragma unroll
         for (int st = 0; st < NS; ++st) mbar_init(&bars[warp * NS + st], 1);
+        if (warp == 0) mbar_init(&bars[kTcWarps * NS], 1);  // candidate rescoring loads
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     const int r = lane >> 2, c = lane & 3;
@@ -1472,36 +1513,38 @@ block_select_tcc_kernel(const void* __restrict__ q, const void* __restrict__ met
     // ---- 3. candidates of this chunk (U >= tau'), rescored exactly ----
     int32_t* jpos = (int32_t*)smem_raw;                    // [<= CH]
     uint64_t* ckeys = (uint64_t*)(smem_raw + (size_t)CH * 4);
-    int n_cand;
-    {
-        const int per = (nb_chunk + kTcThreads - 1) / kTcThreads;
-        const int p0 = tid * per, p1 = min(nb_chunk, p0 + per);
-        int cnt = 0;
-        for (int p2 = p0; p2 < p1; ++p2) cnt += hi[p2] >= tau;
-        int tot;
-        int o = block_excl_scan<kTcThreads>(cnt, sw, tot);
-        for (int p2 = p0; p2 < p1; ++p2)
-            if (hi[p2] >= tau) jpos[o++] = p2;
-        n_cand = tot;
-    }
+    const int n_cand = cta_compact<kTcThreads>(nb_chunk, sw, jpos, [&](int p2) { return hi[p2] >= tau; });
     sel_stamp(tr, 7, (unsigned long long)n_cand);
     __syncthreads();
+    sel_stamp(tr, 9);
     {
+        uint32_t rphase = 0;
         unsigned char* cstage = smem_raw + (((size_t)CH * 4 + (size_t)n_cand * 8 + 127) & ~(size_t)127);
         const int stage_end = region_bytes + 8 * CH;
         const int batch = max(1, min(kTcThreads, (stage_end - (int)(cstage - smem_raw)) / 512));
         for (int base = 0; base < n_cand; base += batch) {
             const int nbt = min(batch, n_cand - base);
-            for (int i = tid; i < nbt * 32; i += kTcThreads) {
-                const int ci2 = i >> 5, pc = i & 31;
-                const int p2 = jpos[base + ci2];
-                const char* src = meta_pair + (size_t)(j0 / 32 + p2 / 32) * kTileBytes + (size_t)pc * 512 + (p2 % 32) * 16;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(cstage + ci2 * 512 + pc * 16)),
-                             "l"(src)
-                             : "memory");
+            // one 2-D TMA per candidate: its 32 16-byte pieces (one per (channel
+            // chunk, min|max) row of its tile, 512 B apart) as ONE box of the
+            // [rows][256] bf16 view of the metadata -- instead of 32 cp.async per
+            // candidate (~600 outstanding 16-byte requests per CTA, r02ah)
+            if (tid == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&bars[kTcWarps * NS], (uint32_t)(nbt * 512));
             }
-            asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
             __syncthreads();
+            if (tid < nbt) {
+                const int p2 = jpos[base + tid];
+                const int64_t blk = (int64_t)pair * max_blk + j0 + p2;  // the block's index in the whole array
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(cstage + tid * 512)),
+                    "l"(reinterpret_cast<uint64_t>(&tm_cand)), "r"((int)(blk % 32) * 8), "r"((int)(blk / 32) * 32),
+                    "r"(smem_u32(&bars[kTcWarps * NS]))
+                    : "memory");
+            }
+            mbar_wait(&bars[kTcWarps * NS], rphase);
+            rphase ^= 1u;
             if (base == 0) sel_stamp(tr, 8);
             if (tid < nbt) {
                 const uint4* cp = reinterpret_cast<const uint4*>(cstage + tid * 512);
@@ -1795,7 +1838,22 @@ static ss_status launch_sel_tcc(const void* q, const void* meta, const int32_t* 
     const int gather_end = CH * 12 + CS * k * 12;
     const int region = std::max(kTcWarps * ns * kTileBytes, ((gather_end - 8 * CH) + 127) / 128 * 128);
     const size_t smem = (size_t)region + (size_t)CH * 8 + (size_t)kHeadDim * G * 12 + 256 * 4 + 64 * 4 + 32 * 8 +
-                        (size_t)kTcWarps * ns * 8;
+                        (size_t)kTcWarps * ns * 8 + 8;
+    // candidate loads: the metadata as [B*Hkv*max_blk][256] bf16 rows of 512 B
+    // (row 32T + 2s + mm of tile T = its channel chunk s, min|max), box 8 x 32
+    CUtensorMap tm_cand;
+    {
+        auto enc = tensor_map_encoder();
+        if (enc == nullptr) return SS_ERR_CUDA;
+        const cuuint64_t gdim[2] = {256, (cuuint64_t)pairs * max_blk};
+        const cuuint64_t gstride[1] = {512};
+        const cuuint32_t box[2] = {8, 32};
+        const cuuint32_t estride[2] = {1, 1};
+        if (enc(&tm_cand, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(meta), gdim, gstride, box, estride,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return SS_ERR_CUDA;
+    }
     if (smem > (size_t)(ns == 1 ? 113 * 1024 : 227 * 1024)) return SS_ERR_UNSUPPORTED;
     auto kern = ns == 2 ? block_select_tcc_kernel<G, 2> : block_select_tcc_kernel<G, 1>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -1817,7 +1875,7 @@ static ss_status launch_sel_tcc(const void* q, const void* meta, const int32_t* 
     cfg.numAttrs = 1;
     const int tr = knob("SS_SEL_TRACE", 0);
     if (cudaLaunchKernelEx(&cfg, kern, q, meta, n_blk, max_blk, k, (int)d.num_q_heads, (int)d.num_kv_heads, CS, CH,
-                           region, tr, sel) != cudaSuccess)
+                           region, tr, sel, tm_cand) != cudaSuccess)
         return SS_ERR_CUDA;
     return SS_OK;
 }

@@ -1086,21 +1086,6 @@ size_t attn_ws_bytes(const ss_dims& d, int k, ss_dtype dt) {
     return attn_ws_bytes_core(d, dt) + (attn_trace_on() ? (size_t)attn_total_warps(dt) * kTraceSlots * 8 : 0);
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-    });
-    return fn;
-}
-
 // [rows][128] bf16 view of a KV array (row = one token's K or V vector of a
 // head-block; block b = rows 64b .. 64b+63), 32 x 64 boxes, 128-byte swizzle.
 static bool encode_kv_map(CUtensorMap* m, const void* base, uint64_t rows) {

@@ -77,7 +77,7 @@ def bench_select(c, iters):
         else:
           print(json.dumps({"ctas": len(tr), "start_us": qq((tr[:, 0] - t0) / 1e3), "tiles_us": qq(d(0, 1)),
                           "threshold_us": qq(d(1, 2)), "rescore_us": qq(d(2, 3)),
-                          "rescore_data_wait_us": qq(d(2, 8, tr[:, 8] >= tr[:, 2])), "rescore_compute_us": qq(d(8, 3, tr[:, 8] >= tr[:, 2])), "chunk_topk_us": qq(d(3, 4)),
+                          "rescore_compaction_us": qq(d(2, 9, tr[:, 9] >= tr[:, 2])), "rescore_data_wait_us": qq(d(9, 8, tr[:, 8] >= tr[:, 9])), "rescore_compute_us": qq(d(8, 3, tr[:, 8] >= tr[:, 2])), "chunk_topk_us": qq(d(3, 4)),
                           "n_cand": qq(tr[:, 7]), "chunk_end_us": qq((tr[:, 4] - t0) / 1e3),
                           "merges": int(mg.sum()), "merge_us": qq(d(5, 6, mg)) if mg.any() else None,
                           "merge_end_us": qq((tr[mg][:, 6] - t0) / 1e3) if mg.any() else None}))
