@@ -531,6 +531,28 @@ def test_cache_fused_form_bit_exact(ops):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+def test_select_attention_alternative_forms_bit_exact(ops):
+    """The forms the default paths fall back to, forced through the debug
+    build (libsparseserve_debug.so): the per-chunk tensor-core select with its
+    workspace merge (SS_SEL_TCC=0), the MHA select's workspace-merge form
+    (SS_SEL_MHA_CLU=0) and the attention's register merge at the range end
+    (SS_ATTN_MERGE_BULK=0) -- the select and attention parity tests re-run in a
+    subprocess against the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    from paper_2509_24626_b200 import build as _build
+    if not os.path.exists(_build.LIB_DEBUG):
+        pytest.skip("debug library not built (python -m paper_2509_24626_b200.build --debug)")
+    env = dict(os.environ, SS_SEL_TCC="0", SS_SEL_MHA_CLU="0", SS_ATTN_MERGE_BULK="0", SS_LIB_VARIANT="debug")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"),
+                        "-k", "(select or attention) and not alternative_forms and not beyond_cluster"],
+                       env=env, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("dt", [synth.DT_BF16, synth.DT_F32])
 @pytest.mark.parametrize("G", [1, 4])
 def test_attention_split_hits_misses_merge(ops, dt, G):
