@@ -1826,6 +1826,38 @@ static ss_status launch_sel_tcc(const void* q, const void* meta, const int32_t* 
     if ((max_blk + CS - 1) / CS > kSelChunkMax) return SS_ERR_UNSUPPORTED;
     const int64_t target = (int64_t)2 * num_sms() * 4 / 5;
     while (CS < kTccMaxCluster && pairs * CS < target && (max_blk + 2 * CS - 1) / (2 * CS) >= 256) CS *= 2;
+    if (CS == 16 && pairs * 12 >= target / 2) {
+        // 16-CTA clusters (8 SMs each at two CTAs per SM) do not all fit in the
+        // GPCs once there are more than ~8 of them; 12-CTA clusters (6 SMs) do
+        // (measured: two C3 requests 95 us in 16-CTA clusters with a partial
+        // second wave, 109 us in 8-CTA clusters at one CTA per SM, r02av)
+        int nclu = 0;
+        cudaLaunchConfig_t oc = {};
+        cudaLaunchAttribute oa[1];
+        oa[0].id = cudaLaunchAttributeClusterDimension;
+        oa[0].val.clusterDim.x = 16;
+        oa[0].val.clusterDim.y = 1;
+        oa[0].val.clusterDim.z = 1;
+        oc.attrs = oa;
+        oc.numAttrs = 1;
+        oc.gridDim = dim3(16);
+        oc.blockDim = dim3(kTcThreads);
+        // max active 16-CTA clusters of the 2-CTA-per-SM form, cached per shared-memory size
+        static size_t fit_smem = 0;
+        static int fit16 = 0;
+        const int ch16 = ((max_blk + 15) / 16 + 31) / 32 * 32;
+        oc.dynamicSmemBytes = (size_t)std::max(kTcWarps * kTileBytes, ch16 * 4 + 16 * k * 12) + (size_t)ch16 * 8 +
+                              (size_t)kHeadDim * G * 12 + 256 * 4 + 64 * 4 + 32 * 8 + kTcWarps * 8 + 8;
+        if (fit_smem != oc.dynamicSmemBytes) {
+            auto k1 = block_select_tcc_kernel<G, 1>;
+            cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oc.dynamicSmemBytes);
+            cudaFuncSetAttribute(k1, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (cudaOccupancyMaxActiveClusters(&nclu, k1, &oc) != cudaSuccess) nclu = 0;
+            fit16 = nclu;
+            fit_smem = oc.dynamicSmemBytes;
+        }
+        if (fit16 < pairs) CS = 12;
+    }
     const int CH = ((max_blk + CS - 1) / CS + 31) / 32 * 32;
     // two stages per warp (one CTA per SM) when the launch has at most one CTA
     // per SM -- except for 16-CTA clusters, which need 16 SMs of one GPC at one
