@@ -42,7 +42,14 @@ namespace ss {
 
 constexpr int kAttnPartStride = 132;
 // floats per (warp, seg, g) partial: m, l, pad, pad, o[128]
-constexpr int kMinUnitsPerWarp = 8;  // measured: C3 26.6 us at 8 vs 30.7 at 4 / 16, C2 unchanged
+// at least this many units per warp: fewer, longer ranges when the problem is
+// small.  Measured back to back with the bulk-load merge (profiles/r02_attn_min_units.txt):
+// GQA (G = 4) two / one C3 request 17.3 / 16.5 us at 4 vs 18.6 / 18.5 at 8, but the
+// full C3 batch (where 4 would already occupy every warp) 20.5 at 4 vs 20.0 at 8;
+// MHA one C2 request group 25.7-25.9 us at 12 vs 26.7-26.8 at 8
+constexpr int kMinUnitsPerWarpGqaSmall = 4;
+constexpr int kMinUnitsPerWarpGqa = 8;
+constexpr int kMinUnitsPerWarpMha = 12;
 constexpr int kTraceSlots = 12;       // debug timeline words per warp (AttnArgs::trace)
 
 struct AttnArgs {
@@ -1219,10 +1226,13 @@ ss_status launch_sparse_attn(const void* q, const void* pool_kv, const int32_t* 
     const int G = d.num_q_heads / d.num_kv_heads;
     a.U = (int64_t)d.batch * d.num_kv_heads * (k + 1);
     a.merge_bulk = knob("SS_ATTN_MERGE_BULK", 1);
-    // at least kMinUnitsPerWarp units (128 KiB in bf16) per warp: fewer, longer
+    // at least kMinUnitsPerWarpGqa / Mha units (16 KiB each in bf16) per warp: fewer, longer
     // ranges when the problem is small (C3: ~16 partials per pair to merge instead
     // of ~28); W <= U keeps every range non-empty
-    const int min_units = knob("SS_ATTN_MIN_UNITS", kMinUnitsPerWarp);
+    const int min_units_dflt =
+        G == 1 ? kMinUnitsPerWarpMha
+               : (a.U >= (int64_t)num_sms() * 6 * kMinUnitsPerWarpGqaSmall ? kMinUnitsPerWarpGqa : kMinUnitsPerWarpGqaSmall);
+    const int min_units = knob("SS_ATTN_MIN_UNITS", min_units_dflt);
     // bf16 tensor-core path (SS_ATTN_MMA=0 selects the CUDA-core FMA path)
     const int use_mma = knob("SS_ATTN_MMA", 1);
     const int ns = mma_stages();
