@@ -46,10 +46,12 @@ constexpr int kAttnPartStride = 132;
 // small.  Measured back to back with the bulk-load merge (profiles/r02_attn_min_units.txt):
 // GQA (G = 4) two / one C3 request 17.3 / 16.5 us at 4 vs 18.6 / 18.5 at 8, but the
 // full C3 batch (where 4 would already occupy every warp) 20.5 at 4 vs 20.0 at 8;
-// MHA one C2 request group 25.7-25.9 us at 12 vs 26.7-26.8 at 8
+// MHA one C2 request group 25.7-25.9 us at 12 vs 26.7-26.8 at 8 alone, but the C2 step
+// (request groups co-running) read 1476 tok/s with 12 against 1483-1511 over eight runs
+// at 8 (r02bc), so MHA keeps 8
 constexpr int kMinUnitsPerWarpGqaSmall = 4;
 constexpr int kMinUnitsPerWarpGqa = 8;
-constexpr int kMinUnitsPerWarpMha = 12;
+constexpr int kMinUnitsPerWarpMha = 8;
 constexpr int kTraceSlots = 12;       // debug timeline words per warp (AttnArgs::trace)
 
 struct AttnArgs {
